@@ -1,0 +1,204 @@
+"""Seeded synthetic inputs for QQA (INPUT GENERATION ONLY -- no method arithmetic).
+
+Shared read-only by the CUDA path's tests / bench and by ``oracle/``. Nothing
+here computes any part of the QQA update; it only builds graphs (symmetric CSR)
+and names the five BASELINE.json workloads with the hyper-parameters SURVEY.md
+§8(d) fixes for them.
+
+Stand-ins (Appendix E, Table 12; §5.1 Table 2):
+  c1  MIS, random 3-regular, N=256                         (tiny sanity case)
+  c2  MIS, 16 x ER G(N, 0.15), N in [700, 800]              (ER-[700-800])
+  c3  Max-Cut, random 5-regular, N=10,000                   (Fig. 1 / Table 5 family)
+  c4  MIS, ER with N in [9000, 11000], mean degree ~100      (ER-[9000-11000])
+  c5  MIS, random 20-regular, N=1,000,000                    (Table 2 RRG d=20)
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libqqagen.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "graphgen.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-o", _SO, src, "-lm"])
+    return _SO
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+        i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+        lib.gen_splitmix64.restype = ctypes.c_uint64
+        lib.gen_splitmix64.argtypes = [ctypes.c_uint64]
+        lib.gen_er_edges.restype = ctypes.c_int64
+        lib.gen_er_edges.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, i32p, i32p, ctypes.c_int64]
+        lib.gen_rrg_edges.restype = ctypes.c_int64
+        lib.gen_rrg_edges.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, i32p, i32p]
+        lib.edges_to_csr.restype = ctypes.c_int
+        lib.edges_to_csr.argtypes = [ctypes.c_int32, ctypes.c_int64, i32p, i32p, i64p, i32p]
+        _lib = lib
+    return _lib
+
+
+def splitmix64(x: int) -> int:
+    return int(_L().gen_splitmix64(ctypes.c_uint64(x & 0xFFFFFFFFFFFFFFFF)))
+
+
+@dataclasses.dataclass
+class Graph:
+    """Undirected simple graph as symmetric CSR (rows sorted, no loops/duplicates)."""
+    n: int
+    rowptr: np.ndarray  # int64 [n+1]
+    colidx: np.ndarray  # int32 [nnz]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rowptr[-1])
+
+    @property
+    def n_edges(self) -> int:
+        return self.nnz // 2
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.rowptr)
+
+    def edges(self) -> tuple[np.ndarray, np.ndarray]:
+        """Each undirected edge once, as (u, v) with u < v."""
+        u = np.repeat(np.arange(self.n, dtype=np.int32), self.degrees())
+        keep = u < self.colidx
+        return u[keep], self.colidx[keep]
+
+
+def from_edges(n: int, u, v) -> Graph:
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    colidx = np.zeros(2 * len(u), dtype=np.int32)
+    rc = _L().edges_to_csr(n, len(u), u, v, rowptr, colidx)
+    if rc != 0:
+        raise ValueError(f"edges_to_csr failed ({rc}): self-loop, range or duplicate edge")
+    return Graph(n, rowptr, colidx)
+
+
+def erdos_renyi(n: int, p: float, seed: int) -> Graph:
+    mean = p * n * (n - 1) / 2
+    cap = int(mean + 12 * np.sqrt(mean + 1) + 64)
+    while True:
+        u = np.empty(cap, np.int32)
+        v = np.empty(cap, np.int32)
+        m = _L().gen_er_edges(n, p, seed & 0xFFFFFFFFFFFFFFFF, u, v, cap)
+        if m >= 0:
+            return from_edges(n, u[:m], v[:m])
+        cap *= 2
+
+
+def random_regular(n: int, d: int, seed: int) -> Graph:
+    m = n * d // 2
+    u = np.empty(max(m, 1), np.int32)
+    v = np.empty(max(m, 1), np.int32)
+    rc = _L().gen_rrg_edges(n, d, seed & 0xFFFFFFFFFFFFFFFF, u, v)
+    if rc < 0:
+        raise ValueError(f"random_regular(n={n}, d={d}) failed ({rc})")
+    return from_edges(n, u[:m], v[:m])
+
+
+def edgeless(n: int) -> Graph:
+    return Graph(n, np.zeros(n + 1, np.int64), np.zeros(0, np.int32))
+
+
+def cycle(n: int) -> Graph:
+    u = np.arange(n, dtype=np.int32)
+    v = (u + 1) % n
+    return from_edges(n, np.minimum(u, v), np.maximum(u, v))
+
+
+def grid(r: int, c: int) -> Graph:
+    idx = np.arange(r * c).reshape(r, c)
+    u = np.concatenate([idx[:, :-1].ravel(), idx[:-1, :].ravel()])
+    v = np.concatenate([idx[:, 1:].ravel(), idx[1:, :].ravel()])
+    return from_edges(r * c, u, v)
+
+
+def random_bipartite(a: int, b: int, p: float, seed: int) -> Graph:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    mask = rng.random((a, b)) < p
+    u, v = np.nonzero(mask)
+    return from_edges(a + b, u.astype(np.int32), (v + a).astype(np.int32))
+
+
+# ------------------------------------------------------------------ configs
+PROBLEMS = {"mis": 0, "maxcut": 1, "maxclique": 2}
+
+
+@dataclasses.dataclass
+class Workload:
+    """One BASELINE.json config as concrete synthetic inputs."""
+    name: str
+    problem: str
+    graphs: list  # list[Graph] (one per instance)
+    seeds: list   # state seed per instance
+    S: int
+    steps: int
+    gamma_min: float = -2.0
+    gamma_max: float = 0.1
+    alpha: int = 2
+    penalty: float = 2.0
+    comm: float = 0.1
+    lr: float = 1.0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.01
+    init_lo: float = -0.01
+    init_hi: float = 0.01
+    recipe: str = ""
+
+    def hparams(self) -> dict:
+        return dict(problem=self.problem, alpha=self.alpha, penalty=self.penalty, comm=self.comm,
+                    lr=self.lr, beta1=self.beta1, beta2=self.beta2, eps=self.eps,
+                    weight_decay=self.weight_decay, init_lo=self.init_lo, init_hi=self.init_hi)
+
+
+def c2_sizes() -> list[int]:
+    return [700 + splitmix64(2000 + k) % 101 for k in range(16)]
+
+
+def c4_size() -> int:
+    return 9000 + splitmix64(4000) % 2001
+
+
+def workload(name: str, n_instances: int | None = None) -> Workload:
+    """Build config ``name`` in {c1..c5}. ``n_instances`` truncates c2's 16 instances."""
+    if name == "c1":
+        return Workload("c1", "mis", [random_regular(256, 3, 1)], [1], S=16, steps=1000,
+                        recipe="MIS, random 3-regular N=256 (config model + swap repair, seed 1); S=16; 1000 steps")
+    if name == "c2":
+        k_n = 16 if n_instances is None else n_instances
+        sizes = c2_sizes()[:k_n]
+        gs = [erdos_renyi(n, 0.15, 2000 + k) for k, n in enumerate(sizes)]
+        return Workload("c2", "mis", gs, [2000 + k for k in range(k_n)], S=100, steps=3000,
+                        recipe="MIS, 16 x ER G(N, 0.15), N = 700 + splitmix64(2000+k) mod 101; S=100; 3000 steps")
+    if name == "c3":
+        return Workload("c3", "maxcut", [random_regular(10_000, 5, 3)], [3], S=256, steps=5000,
+                        gamma_min=-20.0,
+                        recipe="Max-Cut, random 5-regular N=10,000 (seed 3); S=256; 5000 steps; gamma -20 -> 0.1")
+    if name == "c4":
+        n = c4_size()
+        return Workload("c4", "mis", [erdos_renyi(n, 100.0 / (n - 1), 4000)], [4000], S=512, steps=5000,
+                        recipe="MIS, ER N = 9000 + splitmix64(4000) mod 2001, p = 100/(N-1); S=512; 5000 steps")
+    if name == "c5":
+        return Workload("c5", "mis", [random_regular(1_000_000, 20, 5)], [5], S=64, steps=3000,
+                        recipe="MIS, random 20-regular N=1,000,000 (seed 5); S=64; 3000 steps")
+    raise KeyError(name)

@@ -1,0 +1,327 @@
+/*
+ * oracle/contract.c -- QQA oracle, fp32 CONTRACT mode.   TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library. The product path
+ * (paper_2409_02135_b200/, libqqa.so) shares no code with it.
+ *
+ * Plain single-threaded loops (an optional OpenMP pragma over independent
+ * rows does not change any arithmetic). Build: gcc -O2 -ffp-contract=off
+ * (no FMA contraction, no fast-math); x86-64 SSE gives IEEE binary32/64.
+ *
+ * WHAT IT COMPUTES (PAPER.md lines "P:nnn"):
+ *   p = sigmoid(theta)                                              P:143, BASELINE north_star
+ *   dR/dp = dl/dp + gamma ds/dp + d(-S a_c sum STD)/dp               Eq. 6, 7, 10
+ *     MIS / clique-as-MIS-on-complement: dl/dp_i = -1 + lam q_i
+ *     Max-Cut:                          dl/dp_i = -deg_i + 2 q_i
+ *     q_i = sum_{j in N(i)} p_j
+ *     gamma ds/dp = -2 alpha gamma (2p - 1)^(alpha-1)
+ *     comm: -a_c (p - mu_i) / STD_i  (0 if STD_i < 1e-6)              P:196-198, R6
+ *   dR/dtheta = dR/dp * p (1 - p)
+ *   AdamW, decoupled weight decay
+ *   x = Theta(p - 1/2) evaluated as theta >= 0
+ *   energies from integer counts
+ *
+ * THE fp32 CONTRACT: every element follows one fixed sequence
+ * of IEEE round-to-nearest operations, so an implementation that performs the
+ * same sequence gets bit-identical results:
+ *   - gather q = ((0 + p_j1) + p_j2) + ...  in ascending CSR order;
+ *   - sigmoid: exp by Cody-Waite reduction + degree-7 Taylor (Horner) in fp32
+ *     (oc_exp_neg), p = 1/(1+E) for theta >= 0 else E/(1+E);
+ *   - cross-replica stats as exact int64 fixed-point sums (scale 2^40) of
+ *     d = p - c_i and fl(d*d), c_i = the previous step's mean (1/2 at init);
+ *   - per-step scalars computed in double on the host, rounded to fp32.
+ * The contract is pinned against the fp64 definition (oracle/definition.py)
+ * in tests/test_oracle_contract.py.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { OC_MIS = 0, OC_MAXCUT = 1, OC_MAXCLIQUE = 2 };
+
+typedef struct {
+    int32_t problem;     /* 0 MIS, 1 Max-Cut, 2 max clique (caller passes the complement CSR) */
+    int32_t alpha;       /* entropy exponent (even >= 2) */
+    float penalty;       /* lambda */
+    float comm;          /* alpha_c, communication strength */
+    float lr, beta1, beta2, eps, weight_decay;
+    float init_lo, init_hi;
+    uint64_t seed;
+    int32_t S;           /* replicas (the oracle always holds all of them) */
+    int32_t threads;     /* OpenMP threads for the row loop (<=1: serial) */
+} oc_cfg;
+
+/* ------------------------------------------------------------ sigmoid ---- */
+/* E = exp(-a) for 0 <= a <= 87, in fp32: a = k ln2 + r, exp(r) by Taylor. */
+float oc_exp_neg(float a) {
+    const float x = -a;
+    const float kf = rintf(x * 1.44269504088896341f);       /* nearest k */
+    const float r = (x - kf * 0.693145751953125f)             /* ln2 hi (exact products) */
+                    - kf * 1.428606765330187e-6f;              /* ln2 lo */
+    float P = 1.0f / 5040.0f;                                  /* 1/7! */
+    P = P * r + 1.0f / 720.0f;
+    P = P * r + 1.0f / 120.0f;
+    P = P * r + 1.0f / 24.0f;
+    P = P * r + 1.0f / 6.0f;
+    P = P * r + 1.0f / 2.0f;
+    P = P * r + 1.0f;
+    P = P * r + 1.0f;
+    int k = (int)kf;                                           /* in [-126, 0] */
+    union { uint32_t u; float f; } two_k;
+    two_k.u = (uint32_t)(k + 127) << 23;
+    return P * two_k.f;
+}
+
+float oc_sigmoid(float theta) {
+    const float a = fabsf(theta);
+    const float E = (a > 87.0f) ? 0.0f : oc_exp_neg(a);
+    const float den = 1.0f + E;
+    return (theta >= 0.0f) ? 1.0f / den : E / den;
+}
+
+/* ------------------------------------------------------ step scalars ---- */
+/* out = { k_t = -2 alpha gamma_t, a_t = 1 - lr wd, s_t = lr/(1-b1^t), r_t = 1/sqrt(1-b2^t) } */
+void oc_step_scalars(const oc_cfg* c, int64_t t, float gamma_t, float* out) {
+    out[0] = (float)(-2.0 * (double)c->alpha * (double)gamma_t);
+    out[1] = (float)(1.0 - (double)c->lr * (double)c->weight_decay);
+    out[2] = (float)((double)c->lr / (1.0 - pow((double)c->beta1, (double)t)));
+    out[3] = (float)(1.0 / sqrt(1.0 - pow((double)c->beta2, (double)t)));
+}
+
+/* gamma_t = gmin + (gmax - gmin) t / (T - 1), t = 0..T-1 (reading R10) */
+void oc_schedule(float gmin, float gmax, int64_t T, float* out) {
+    for (int64_t t = 0; t < T; ++t)
+        out[t] = (T == 1) ? gmin
+                          : (float)((double)gmin + (((double)gmax - (double)gmin) * (double)t) / (double)(T - 1));
+}
+
+/* ----------------------------------------------------------- stats ------ */
+static void finalize_stats(float c, int64_t sD, int64_t sD2, int32_t S, float* mu, float* sd) {
+    const double md = ((double)sD * 0x1p-40) / (double)S;
+    *mu = (float)((double)c + md);
+    const double ex2 = ((double)sD2 * 0x1p-40) / (double)S;
+    const double var = ex2 - md * md;
+    *sd = (float)sqrt(var > 0.0 ? var : 0.0);
+}
+
+static void row_sums(const float* prow, int32_t S, float c, int64_t* sD, int64_t* sD2) {
+    int64_t a = 0, b = 0;
+    for (int32_t s = 0; s < S; ++s) {
+        const float d = prow[s] - c;
+        a += llrintf(d * 0x1p40f);
+        const float dd = d * d;
+        b += llrintf(dd * 0x1p40f);
+    }
+    *sD = a; *sD2 = b;
+}
+
+/* public: mean and STD of one row from its sums (for tests) */
+void oc_finalize(float c, int64_t sD, int64_t sD2, int32_t S, float* mu_sd) {
+    finalize_stats(c, sD, sD2, S, &mu_sd[0], &mu_sd[1]);
+}
+
+/* ------------------------------------------------------------ init ------ */
+static uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+/* theta_0 ~ U(lo, hi) by a counter hash keyed (seed, i, s); m = v = 0; p = sigmoid(theta);
+ * c = 1/2; sums of p with shift 1/2. Arrays are [n][S] row-major. */
+void oc_init(int32_t n, const oc_cfg* cf, float* theta, float* m, float* v, float* p,
+             float* c, int64_t* sumD, int64_t* sumD2) {
+    const int32_t S = cf->S;
+    const uint64_t base = mix64(cf->seed);
+    const double lo = (double)cf->init_lo, hi = (double)cf->init_hi;
+    for (int32_t i = 0; i < n; ++i) {
+        for (int32_t s = 0; s < S; ++s) {
+            const uint64_t key = base + (uint64_t)i * (uint64_t)S + (uint64_t)s;
+            const uint64_t k = mix64(key) >> 40;
+            const size_t at = (size_t)i * S + s;
+            theta[at] = (float)(lo + (hi - lo) * (double)k * 0x1p-24);
+            m[at] = 0.0f;
+            v[at] = 0.0f;
+            p[at] = oc_sigmoid(theta[at]);
+        }
+        c[i] = 0.5f;
+        row_sums(p + (size_t)i * S, S, 0.5f, &sumD[i], &sumD2[i]);
+    }
+}
+
+/* ------------------------------------------------------------ one row --- */
+/* Update row i. Reads p (old values, all rows) and the row's stats (c_i, sums);
+ * updates th/mm/vv (row i, length S) in place; writes p_new (row i) and the
+ * row's new stats (shift = this step's mean). */
+static void update_row(int32_t i, const int64_t* rowptr, const int32_t* colidx, const oc_cfg* cf,
+                       const float* sc, const float* p, float* th, float* mm, float* vv,
+                       float c_i, int64_t sD_i, int64_t sD2_i,
+                       float* p_new, float* c_new, int64_t* sD_new, int64_t* sD2_new, float* q) {
+    const int32_t S = cf->S;
+    const float kt = sc[0], at = sc[1], st = sc[2], rt = sc[3];
+    const float b1 = cf->beta1, b2 = cf->beta2, eps = cf->eps;
+    const float c1 = (float)(1.0 - (double)cf->beta1), c2 = (float)(1.0 - (double)cf->beta2);
+    const float lam = cf->penalty, ac = cf->comm;
+    const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+    const float degf = (float)(e1 - e0);
+    const float* pown = p + (size_t)i * S;
+
+    float mu, sd;
+    finalize_stats(c_i, sD_i, sD2_i, S, &mu, &sd);
+
+    /* q_i^s = sum_{j in N(i)} p_j^s, ascending CSR order */
+    for (int32_t s = 0; s < S; ++s) q[s] = 0.0f;
+    for (int64_t e = e0; e < e1; ++e) {
+        const float* pj = p + (size_t)colidx[e] * S;
+        for (int32_t s = 0; s < S; ++s) q[s] = q[s] + pj[s];
+    }
+
+    for (int32_t s = 0; s < S; ++s) {
+        const float pi = pown[s];
+        /* gradient dR/dp */
+        const float e = 2.0f * pi - 1.0f;
+        float ep = e;
+        for (int32_t a = 2; a < cf->alpha; ++a) ep = ep * e;   /* (2p-1)^(alpha-1) */
+        const float ent = kt * ep;
+        const float obj = (cf->problem == OC_MAXCUT) ? (2.0f * q[s] - degf) : (lam * q[s] - 1.0f);
+        const float com = (sd >= 1e-6f) ? (-ac) * ((pi - mu) / sd) : 0.0f;
+        const float gp = (obj + ent) + com;
+        const float g = gp * (pi * (1.0f - pi));
+        /* AdamW */
+        float t1 = th[s] * at;
+        const float m1 = b1 * mm[s] + c1 * g;
+        const float v1 = b2 * vv[s] + (c2 * g) * g;
+        const float den = sqrtf(v1) * rt + eps;
+        t1 = t1 - st * (m1 / den);
+        th[s] = t1; mm[s] = m1; vv[s] = v1;
+        p_new[s] = oc_sigmoid(t1);
+    }
+    *c_new = mu;
+    row_sums(p_new, S, mu, sD_new, sD2_new);
+}
+
+static int nonfinite_row(const float* x, int32_t S) {
+    for (int32_t s = 0; s < S; ++s) if (!isfinite(x[s])) return 1;
+    return 0;
+}
+
+/* Run n_steps annealing steps. gamma[k] is gamma for step k; Adam index t = t0 + k + 1.
+ * State arrays are updated in place (p/c/sums hold the state of the current p).
+ * Returns 0, or 5 if a non-finite theta appeared (SPEC.md:396 abort). */
+int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg* cf,
+           const float* gamma, int64_t n_steps, int64_t t0,
+           float* theta, float* m, float* v, float* p, float* c, int64_t* sumD, int64_t* sumD2) {
+    const int32_t S = cf->S;
+    const size_t NS = (size_t)n * S;
+    float* p2 = (float*)malloc(sizeof(float) * (NS ? NS : 1));
+    float* c2 = (float*)malloc(sizeof(float) * (n ? n : 1));
+    int64_t* d2a = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    int64_t* d2b = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    int bad = 0;
+    for (int64_t k = 0; k < n_steps && !bad; ++k) {
+        float sc[4];
+        oc_step_scalars(cf, t0 + k + 1, gamma[k], sc);
+        const int thr = cf->threads > 1 ? cf->threads : 1;
+        (void)thr;
+#pragma omp parallel num_threads(thr)
+        {
+            float* q = (float*)malloc(sizeof(float) * (S ? S : 1));
+#pragma omp for schedule(static)
+            for (int32_t i = 0; i < n; ++i) {
+                const size_t r = (size_t)i * S;
+                update_row(i, rowptr, colidx, cf, sc, p, theta + r, m + r, v + r,
+                           c[i], sumD[i], sumD2[i], p2 + r, &c2[i], &d2a[i], &d2b[i], q);
+            }
+            free(q);
+        }
+        memcpy(p, p2, sizeof(float) * NS);
+        memcpy(c, c2, sizeof(float) * n);
+        memcpy(sumD, d2a, sizeof(int64_t) * n);
+        memcpy(sumD2, d2b, sizeof(int64_t) * n);
+        for (int32_t i = 0; i < n && !bad; ++i) bad = nonfinite_row(theta + (size_t)i * S, S);
+    }
+    free(p2); free(c2); free(d2a); free(d2b);
+    return bad ? 5 : 0;
+}
+
+/* One step for a subset of rows only (sampled checks at full size).
+ * Inputs: the full p/c/sums at the start of the step, and theta/m/v of the
+ * selected rows ([nrows][S]). Outputs for rows[k]: theta/m/v/p [nrows][S],
+ * c/sums [nrows]. */
+void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg* cf,
+                  float gamma_t, int64_t t, const float* p, const float* c, const int64_t* sumD,
+                  const int64_t* sumD2, const float* theta_rows, const float* m_rows, const float* v_rows,
+                  const int32_t* rows, int32_t nrows,
+                  float* theta_out, float* m_out, float* v_out, float* p_out,
+                  float* c_out, int64_t* sD_out, int64_t* sD2_out) {
+    const int32_t S = cf->S;
+    (void)n;
+    float sc[4];
+    oc_step_scalars(cf, t, gamma_t, sc);
+    float* q = (float*)malloc(sizeof(float) * (S ? S : 1));
+    for (int32_t k = 0; k < nrows; ++k) {
+        const int32_t i = rows[k];
+        const size_t r = (size_t)k * S;
+        memcpy(theta_out + r, theta_rows + r, sizeof(float) * S);
+        memcpy(m_out + r, m_rows + r, sizeof(float) * S);
+        memcpy(v_out + r, v_rows + r, sizeof(float) * S);
+        update_row(i, rowptr, colidx, cf, sc, p, theta_out + r, m_out + r, v_out + r,
+                   c[i], sumD[i], sumD2[i], p_out + r, &c_out[k], &sD_out[k], &sD2_out[k], q);
+    }
+    free(q);
+}
+
+/* ------------------------------------------------------- evaluation ---- */
+/* x = [theta >= 0]; counts[s][3] = (size, violations, cut) with each
+ * undirected edge counted once (j > i); energy[s] = -size + lam*viol
+ * (MIS / clique on the complement) or -cut (Max-Cut); *best = argmin energy,
+ * lowest index on ties. */
+void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t problem, float lam,
+             int32_t S, const float* theta, int64_t* counts, double* energy, int32_t* best) {
+    memset(counts, 0, sizeof(int64_t) * 3 * (size_t)S);
+    for (int32_t i = 0; i < n; ++i) {
+        for (int32_t s = 0; s < S; ++s) {
+            const int xi = theta[(size_t)i * S + s] >= 0.0f;
+            counts[3 * s + 0] += xi;
+            for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                const int32_t j = colidx[e];
+                if (j <= i) continue;
+                const int xj = theta[(size_t)j * S + s] >= 0.0f;
+                counts[3 * s + 1] += xi & xj;
+                counts[3 * s + 2] += xi ^ xj;
+            }
+        }
+    }
+    int32_t b = 0;
+    for (int32_t s = 0; s < S; ++s) {
+        energy[s] = (problem == OC_MAXCUT) ? -(double)counts[3 * s + 2]
+                                           : -(double)counts[3 * s + 0] + (double)lam * (double)counts[3 * s + 1];
+        if (energy[s] < energy[b]) b = s;
+    }
+    *best = b;
+}
+
+/* -------------------------------------------------------- complement --- */
+/* Complement of a simple graph (for max clique = MIS on the complement).
+ * Pass colidx_out = NULL to get the nnz only. Returns nnz of the complement. */
+int64_t oc_complement(int32_t n, const int64_t* rowptr, const int32_t* colidx,
+                      int64_t* rowptr_out, int32_t* colidx_out) {
+    int64_t nnz = 0;
+    char* mark = (char*)calloc((size_t)n ? (size_t)n : 1, 1);
+    for (int32_t i = 0; i < n; ++i) {
+        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) mark[colidx[e]] = 1;
+        if (rowptr_out) rowptr_out[i] = nnz;
+        for (int32_t j = 0; j < n; ++j) {
+            if (j == i || mark[j]) continue;
+            if (colidx_out) colidx_out[nnz] = j;
+            ++nnz;
+        }
+        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) mark[colidx[e]] = 0;
+    }
+    if (rowptr_out) rowptr_out[n] = nnz;
+    free(mark);
+    return nnz;
+}

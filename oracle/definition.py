@@ -1,0 +1,273 @@
+"""QQA oracle, fp64 DEFINITION mode.  TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this module. The product path
+(``paper_2409_02135_b200``) never does.
+
+Plain fp64 numpy, written equation by equation from PAPER.md (cited as P:<line>):
+
+  * relaxed objectives (Appendix D):  MIS  l = -c^T x + lambda x^T A x / 2
+                                      Max-Cut l = -sum_{(i,j) in E} A_ij (1-(2x_i-1)(2x_j-1))/2
+                                      max clique = MIS on the complement graph (reading R14)
+  * alpha-entropy s(p) = sum_i 1 - (2 p_i - 1)^alpha                          (Eq. 7)
+  * QQA objective r = l(p) + gamma s(p)                                       (Eq. 6)
+  * ensemble objective R = sum_s r_s - S alpha_c sum_i STD_i, population STD  (Eq. 10)
+  * p = sigmoid(theta)                                                        (BASELINE.json north_star)
+  * AdamW (decoupled weight decay)
+  * gamma linear from gamma_min to gamma_max over the steps
+  * rounding x = Theta(p - 1/2)  (evaluated as theta >= 0, Theta(0) = 1)
+
+Every function here is pinned by ``tests/test_oracle_definition.py`` against
+things other than itself: SPEC.md worked values, central finite differences,
+closed forms (Prop. A.2, Theorem 1 limits), and brute force on tiny graphs.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+MIS, MAXCUT, MAXCLIQUE = 0, 1, 2
+PROBLEM_IDS = {"mis": MIS, "maxcut": MAXCUT, "maxclique": MAXCLIQUE}
+
+# STD below this is treated as a non-differentiable point: comm gradient 0
+# (reading R6; 0 lies in the subgradient set of sqrt at 0).
+STD_FLOOR = 1e-6
+
+
+def _pid(problem) -> int:
+    return PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
+
+
+# --------------------------------------------------------------- graphs
+def dense_adjacency(n: int, rowptr, colidx) -> np.ndarray:
+    A = np.zeros((n, n), dtype=np.float64)
+    for i in range(n):
+        for e in range(int(rowptr[i]), int(rowptr[i + 1])):
+            A[i, int(colidx[e])] = 1.0
+    return A
+
+
+def complement_adjacency(A: np.ndarray) -> np.ndarray:
+    """Adjacency of the complement graph ("MIS on the dual graph")."""
+    n = A.shape[0]
+    return (1.0 - A) - np.eye(n)
+
+
+def problem_adjacency(problem, A: np.ndarray) -> np.ndarray:
+    """The adjacency the relaxed objective is built on (complement for max clique)."""
+    return complement_adjacency(A) if _pid(problem) == MAXCLIQUE else A
+
+
+# ------------------------------------------------------- energies (App. D)
+def relaxed_objective(problem, A: np.ndarray, P: np.ndarray, lam: float = 2.0) -> np.ndarray:
+    """l_hat(p) per replica. P is [N][S]; returns [S].
+
+    MIS: -1^T p + lam * p^T A p / 2.
+    Max-Cut: -sum_{i<j} A_ij (1 - (2p_i-1)(2p_j-1))/2, each undirected edge once.
+    Max clique: MIS on the complement.
+    """
+    pid = _pid(problem)
+    if pid in (MIS, MAXCLIQUE):
+        B = problem_adjacency(pid, A)
+        return -P.sum(axis=0) + lam * np.einsum("is,ij,js->s", P, B, P) / 2.0
+    if pid == MAXCUT:
+        Z = 2.0 * P - 1.0
+        iu, ju = np.nonzero(np.triu(A, 1))  # each undirected edge once (reading R15)
+        w = A[iu, ju][:, None]
+        return -(w * (1.0 - Z[iu] * Z[ju]) / 2.0).sum(axis=0)
+    raise ValueError(problem)
+
+
+def discrete_energy(problem, A: np.ndarray, X: np.ndarray, lam: float = 2.0) -> np.ndarray:
+    """l(x) per replica at binary X [N][S] (Eq. 2 with the App. D energies)."""
+    return relaxed_objective(problem, A, X.astype(np.float64), lam)
+
+
+def printed_clique_energy(A: np.ndarray, x: np.ndarray, lam: float = 2.0) -> float:
+    """The max-clique energy exactly as printed at P:715:
+    -c^T x + (lam/2)(1^T x (1^T x - 1) - x^T A x)."""
+    x = x.astype(np.float64)
+    s = x.sum()
+    return -s + lam / 2.0 * (s * (s - 1.0) - x @ A @ x)
+
+
+def entropy(P: np.ndarray, alpha: int) -> np.ndarray:
+    """alpha-entropy per replica (Eq. 7): sum_i 1 - (2 p_i - 1)^alpha."""
+    return (1.0 - (2.0 * P - 1.0) ** alpha).sum(axis=0)
+
+
+def std_rows(P: np.ndarray) -> np.ndarray:
+    """Empirical population STD over replicas per variable, two-pass."""
+    S = P.shape[1]
+    mu = P.sum(axis=1) / S
+    return np.sqrt(((P - mu[:, None]) ** 2).sum(axis=1) / S)
+
+
+def comm_term(P: np.ndarray, comm: float) -> float:
+    """-S * alpha_c * sum_i STD_i (Eq. 10)."""
+    return -P.shape[1] * comm * std_rows(P).sum()
+
+
+def R_hat(problem, A, P, gamma, alpha, lam, comm) -> float:
+    """Ensemble objective (Eq. 10) = sum_s [l_hat_s + gamma s_s] + comm term."""
+    return float((relaxed_objective(problem, A, P, lam) + gamma * entropy(P, alpha)).sum()
+                 + comm_term(P, comm))
+
+
+# ----------------------------------------------------- analytic gradients
+def grad_objective(problem, A, P, lam) -> np.ndarray:
+    """d l_hat / d p, [N][S].  MIS: -1 + lam (A p)_i ; Max-Cut: -deg_i + 2 (A p)_i."""
+    pid = _pid(problem)
+    if pid in (MIS, MAXCLIQUE):
+        B = problem_adjacency(pid, A)
+        return -1.0 + lam * (B @ P)
+    if pid == MAXCUT:
+        return -A.sum(axis=1)[:, None] + 2.0 * (A @ P)
+    raise ValueError(problem)
+
+
+def grad_entropy(P, alpha) -> np.ndarray:
+    """d s / d p = -2 alpha (2p - 1)^(alpha - 1)."""
+    return -2.0 * alpha * (2.0 * P - 1.0) ** (alpha - 1)
+
+
+def grad_comm(P, comm) -> np.ndarray:
+    """d/dp_i^s of -S alpha_c STD_i = -alpha_c (p_i^s - mu_i) / STD_i (0 where STD_i < floor)."""
+    S = P.shape[1]
+    mu = P.sum(axis=1) / S
+    sd = std_rows(P)
+    out = np.zeros_like(P)
+    ok = sd >= STD_FLOOR
+    out[ok] = -comm * (P[ok] - mu[ok, None]) / sd[ok, None]
+    return out
+
+
+def grad_p(problem, A, P, gamma, alpha, lam, comm) -> np.ndarray:
+    return grad_objective(problem, A, P, lam) + gamma * grad_entropy(P, alpha) + grad_comm(P, comm)
+
+
+def sigmoid(theta):
+    return 1.0 / (1.0 + np.exp(-theta))
+
+
+def grad_theta(problem, A, theta, gamma, alpha, lam, comm) -> np.ndarray:
+    """Chain rule through p = sigmoid(theta): dR/dtheta = dR/dp * p (1 - p)."""
+    P = sigmoid(theta)
+    return grad_p(problem, A, P, gamma, alpha, lam, comm) * P * (1.0 - P)
+
+
+# -------------------------------------------------------------- optimizer
+def adamw_step(theta, m, v, g, t, lr, beta1, beta2, eps, wd):
+    """One AdamW step (Loshchilov & Hutter, cited at P:221), t = 1, 2, ...
+
+    theta <- theta (1 - lr wd);  m <- b1 m + (1-b1) g;  v <- b2 v + (1-b2) g^2;
+    theta <- theta - lr * mhat / (sqrt(vhat) + eps),  mhat = m/(1-b1^t), vhat = v/(1-b2^t).
+    """
+    theta = theta * (1.0 - lr * wd)
+    m = beta1 * m + (1.0 - beta1) * g
+    v = beta2 * v + (1.0 - beta2) * g * g
+    mhat = m / (1.0 - beta1 ** t)
+    vhat = v / (1.0 - beta2 ** t)
+    theta = theta - lr * mhat / (np.sqrt(vhat) + eps)
+    return theta, m, v
+
+
+def gamma_schedule(gamma_min: float, gamma_max: float, total: int) -> np.ndarray:
+    """Linear gamma, both endpoints used (reading R10)."""
+    if total == 1:
+        return np.array([gamma_min], dtype=np.float64)
+    return gamma_min + (gamma_max - gamma_min) * np.arange(total) / (total - 1)
+
+
+# ----------------------------------------------------------- initial state
+def _splitmix64(z: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = (z + np.uint64(0x9E3779B97F4A7C15)).astype(np.uint64)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def init_theta(n: int, S_total: int, seed: int, lo: float = -0.01, hi: float = 0.01) -> np.ndarray:
+    """theta_0[i][s] ~ U(lo, hi) from a counter hash (BASELINE.json configs[0]; paper silent).
+
+    key = splitmix64(seed) + i*S_total + s;  k = top 24 bits of splitmix64(key);
+    theta = lo + (hi - lo) * k * 2^-24.  Returned in fp64 (exact values of the
+    fp32 contract's double intermediate before its final rounding)."""
+    base = _splitmix64(np.array([seed], dtype=np.uint64))[0]
+    i = np.arange(n, dtype=np.uint64)[:, None]
+    s = np.arange(S_total, dtype=np.uint64)[None, :]
+    with np.errstate(over="ignore"):
+        key = base + i * np.uint64(S_total) + s
+    k = (_splitmix64(key) >> np.uint64(40)).astype(np.float64)
+    lo64, hi64 = float(np.float32(lo)), float(np.float32(hi))
+    return lo64 + (hi64 - lo64) * k * 2.0 ** -24
+
+
+# --------------------------------------------------------------- the loop
+def run(problem, A, theta0, gammas, alpha=2, lam=2.0, comm=0.1, lr=1.0, beta1=0.9,
+        beta2=0.999, eps=1e-8, wd=0.01, m0=None, v0=None, t0=0):
+    """PQQA with AdamW on theta, fp64. Returns (theta, m, v)."""
+    theta = np.array(theta0, dtype=np.float64)
+    m = np.zeros_like(theta) if m0 is None else np.array(m0, dtype=np.float64)
+    v = np.zeros_like(theta) if v0 is None else np.array(v0, dtype=np.float64)
+    for k, gamma in enumerate(gammas):
+        g = grad_theta(problem, A, theta, float(gamma), alpha, lam, comm)
+        theta, m, v = adamw_step(theta, m, v, g, t0 + k + 1, lr, beta1, beta2, eps, wd)
+    return theta, m, v
+
+
+def round_x(theta: np.ndarray) -> np.ndarray:
+    """x = Theta(sigmoid(theta) - 1/2) with Theta(0)=1, i.e. theta >= 0 (reading R12)."""
+    return (theta >= 0).astype(np.int64)
+
+
+def counts(problem, A: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """Per replica [S][3] = (size, violations, cut), each undirected edge once.
+
+    violations: #{(i<j) in E' : x_i = x_j = 1} with E' = E (MIS, Max-Cut) or the
+    complement (max clique); cut: #{(i<j) in E : x_i != x_j}."""
+    pid = _pid(problem)
+    B = problem_adjacency(pid, A)
+    X = X.astype(np.int64)
+    n, S = X.shape
+    out = np.zeros((S, 3), dtype=np.int64)
+    iu, ju = np.nonzero(np.triu(B, 1))
+    for s in range(S):
+        x = X[:, s]
+        out[s, 0] = x.sum()
+        out[s, 1] = int((x[iu] & x[ju]).sum())
+        if pid == MAXCUT:
+            ia, ja = np.nonzero(np.triu(A, 1))
+            out[s, 2] = int((x[ia] ^ x[ja]).sum())
+        else:
+            out[s, 2] = int((x[iu] ^ x[ju]).sum())
+    return out
+
+
+def energy_from_counts(problem, c: np.ndarray, lam: float = 2.0) -> np.ndarray:
+    pid = _pid(problem)
+    if pid == MAXCUT:
+        return -c[:, 2].astype(np.float64)
+    return -c[:, 0].astype(np.float64) + lam * c[:, 1].astype(np.float64)
+
+
+def best_replica(energies: np.ndarray) -> int:
+    """argmin energy, lowest replica index on ties (reading R13)."""
+    return int(np.flatnonzero(energies == energies.min())[0])
+
+
+def brute_force(problem, A: np.ndarray, lam: float = 2.0):
+    """Exhaustive argmin of the discrete energy l(x) over {0,1}^N (N <= 20).
+
+    Returns (min_energy, list of minimisers)."""
+    n = A.shape[0]
+    if n > 22:
+        raise ValueError("brute force limited to N <= 22")
+    best, arg = np.inf, []
+    X = np.array(list(itertools.product([0, 1], repeat=n)), dtype=np.float64).T  # [N][2^N]
+    E = relaxed_objective(problem, A, X, lam)
+    best = E.min()
+    arg = [X[:, k].astype(np.int64) for k in np.flatnonzero(np.isclose(E, best, atol=1e-9))]
+    return float(best), arg
