@@ -1,0 +1,328 @@
+#!/usr/bin/env python3
+"""Benchmark of the PQQA hot path (BASELINE.json metric) -- one JSON line on rank 0.
+
+A bench "step" is one pass of the whole hot path over one batch of input:
+re-initialise the replicas (K1), run all annealing steps of the workload's
+schedule (K2 x T, + the per-step NCCL all-reduce when N > 1), round, evaluate
+and pick the best replica (K3-K5). ``value`` = replica-variable updates/s of the
+whole job = N_vars * S_total * T * steps / (max over ranks of the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU); replicas are sharded
+(S_local = S / N) -- strong scaling of the fixed S of BASELINE.json configs[4].
+``--impl reference`` times the CPU oracle (oracle/, the reference arm of this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "replica-variable updates/sec (S*N per step) and % of B200 HBM roofline"
+UNIT = "replica-variable updates/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def algorithmic_bytes(n: int, nnz: int, S_local: int) -> int:
+    """BASELINE.json north_star byte model per step and GPU:
+    CSR indices (4 nnz + 4 (n+1)) + gathered neighbour values (4 nnz S_l) + theta/m/v read+write (24 n S_l)."""
+    return 4 * nnz + 4 * (n + 1) + 4 * nnz * S_local + 24 * n * S_local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, measured)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 4 + k and s[4 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max((float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+def cpu_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def oracle_sample(w, n_steps: int, threads: int):
+    """Time the fp32 contract oracle (as it stands) for n_steps annealing steps of w."""
+    import oracle
+    g, seed = w.graphs[0], w.seeds[0]
+    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
+    cfg = oracle.make_cfg(w.problem, S=w.S, seed=seed, threads=threads, **hp)
+    gam = oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:n_steps]
+    st = oracle.init(g, cfg)
+    t0 = time.perf_counter()
+    oracle.run(g, cfg, gam, state=st)
+    dt = time.perf_counter() - t0
+    return g.n * w.S * n_steps / dt, dt
+
+
+def run_reference(args, w):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    cores, model = cpu_info()
+    n_sample = args.ref_sample_steps
+    times = []
+    for _ in range(args.warmup):
+        oracle_sample(w, n_sample, cores)
+    for _ in range(args.steps):
+        _, dt = oracle_sample(w, n_sample, cores)
+        times.append(dt)
+    t = sum(times)
+    g = w.graphs[0]
+    value = g.n * w.S * n_sample * args.steps / t
+    sample = (f"{n_sample} of {w.steps} annealing steps of {w.name} per bench step at full size "
+              f"(N={g.n}, nnz={g.nnz}, S={w.S}); oracle/contract.c, OpenMP over rows")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload_config(w, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": model},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(w, world):
+    g = w.graphs[0]
+    S_l = w.S // world
+    state_bytes = 5 * g.n * ((S_l + 7) // 8 * 8) * 4
+    return {"workload": w.name, "problem": w.problem, "recipe": w.recipe, "N": g.n, "nnz": g.nnz, "S": w.S,
+            "S_local": S_l, "anneal_steps": w.steps, "instances": len(w.graphs),
+            "parallelism": f"replica-sharded x{world}" if world > 1 else "single GPU",
+            "l2": f"inputs larger than L2: {state_bytes / 1e9:.2f} GB of replica state per GPU"
+                  if state_bytes > 132e6 else "state fits L2 (no flush)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--anneal-steps", type=int, default=None, help="override T (diagnostics only)")
+    ap.add_argument("--cpu-sample-steps", type=int, default=3)
+    ap.add_argument("--ref-sample-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    import gen
+    w = gen.workload(args.workload, n_instances=1 if args.workload == "c2" else None)
+    if args.anneal_steps:
+        w.steps = args.anneal_steps
+    if args.impl == "reference":
+        run_reference(args, w)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_02135_b200 as Q
+
+    rank, local_rank, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if w.S % world:
+        raise SystemExit(f"S={w.S} is not divisible by {world} GPUs")
+    S_l = w.S // world
+    g, seed = w.graphs[0], w.seeds[0]
+    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
+    cfg = Q.make_config(w.problem, S_total=w.S, seed=seed, replica_offset=rank * S_l, S_local=S_l, **hp)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream)
+    if world > 1:
+        uid = [Q.Solver.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sol.attach_comm(uid[0], rank, world)
+
+    def solve(s):
+        s.reset()
+        s.run_linear(w.gamma_min, w.gamma_max, w.steps)
+        return s.round_evaluate(want_x=True, want_replicas=False)
+
+    for _ in range(args.warmup):
+        solve(sol)
+
+    # ------------------------------------------------------- timed region
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sol.profile(True)
+    l0 = sol.launch_count()
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = solve(sol)
+        ev1.record(stream)
+        barrier()
+    l1 = sol.launch_count()
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    kern_ms, kern_launches = sol.profile_read()
+    sol.profile(False)
+    clocks = clk.summary()
+
+    total_updates = g.n * w.S * w.steps * args.steps
+    value = total_updates / (t_ms / 1e3)
+    B = algorithmic_bytes(g.n, g.nnz, S_l)
+    avg_kernel_s = kern_ms / 1e3 / max(kern_launches, 1)
+    peak, peak_src = measured_peaks()
+    achieved = B / avg_kernel_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{w.name}_x{world}")
+
+    # ------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        rp = torch.from_numpy(g.rowptr).pin_memory().numpy()
+        ci = torch.from_numpy(g.colidx).pin_memory().numpy()
+        ws = sol.workspace
+        sol.close()
+        del sol
+
+        def e2e_step():
+            s = Q.Solver(rp, ci, cfg, device=dev, stream=stream, workspace=ws)
+            if world > 1:
+                u = [Q.Solver.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(u, src=0)
+                s.attach_comm(u[0], rank, world)
+            s.run_linear(w.gamma_min, w.gamma_max, w.steps)
+            r = s.round_evaluate(want_x=True, want_replicas=True)
+            s.close()
+            return r
+
+        e2e_step()  # warm
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        te = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": total_updates / (te / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(g.rowptr.nbytes + g.colidx.nbytes),
+               "d2h_bytes_per_step": int(S_l * 48 + g.n + 4 + 8 + 4),
+               "ms_per_step": te / args.steps,
+               "path": "qqa_create (pinned host CSR -> HBM) + qqa_run_linear + qqa_round_evaluate (results -> host)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores, model = cpu_info()
+        v, dt = oracle_sample(w, args.cpu_sample_steps, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": model,
+               "sample": f"{args.cpu_sample_steps} of {w.steps} annealing steps of {w.name} at full size "
+                         f"(N={g.n}, S={w.S}), {dt:.1f} s; oracle/contract.c with OpenMP over rows"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": workload_config(w, world),
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "kernel": "qqa::k_step (fused gather + gradient + AdamW + stats)",
+                             "bytes_per_launch": B, "avg_launch_ms": avg_kernel_s * 1e3,
+                             "launches_timed": kern_launches, "peak_source": peak_src,
+                             "step_kernel_share": kern_ms / t_ms},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": l1 - l0, "clocks": clocks,
+                "result": {"best_replica": res.best_replica, "best_energy": res.best_energy}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

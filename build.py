@@ -1,0 +1,65 @@
+#!/usr/bin/env python3
+"""Build every native artefact in-tree.
+
+  paper_2409_02135_b200/lib/libqqa.so   CUDA (sm_100a) + host engine, C ABI of include/qqa.h
+  oracle/liboracle.so                   the C oracle (test infrastructure; building is not using it)
+  gen/libqqagen.so                      seeded input generators
+
+Usage: python build.py [--verbose] [--force]
+"""
+from __future__ import annotations
+
+import argparse
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+PKG = os.path.join(ROOT, "paper_2409_02135_b200")
+LIB = os.path.join(PKG, "lib", "libqqa.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dir() -> str:
+    import nvidia.nccl  # pip NCCL 2.28 -- the same copy torch loads (one NCCL per process)
+    return os.path.dirname(list(nvidia.nccl.__path__)[0] + "/")
+
+
+def build_qqa(force=False, verbose=False) -> str:
+    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
+    deps = srcs + sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "qqa.h")]
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps):
+        return LIB
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    nd = nccl_dir()
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
+           "-fmad=false",                        # fp32 contract: never contract a*b+c
+           "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
+           "-o", LIB, *srcs]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    return LIB
+
+
+def build_all(force=False, verbose=False) -> None:
+    sys.path.insert(0, ROOT)
+    import gen
+    import oracle
+    gen.build(force=force)
+    oracle.build(force=force)
+    build_qqa(force=force, verbose=verbose)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    a = ap.parse_args()
+    build_all(force=a.force, verbose=a.verbose)
+    print("built:", LIB)

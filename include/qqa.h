@@ -1,0 +1,179 @@
+/*
+ * qqa.h -- C ABI of libqqa.so: the data-parallel hot path of Parallel
+ * Quasi-Quantum Annealing (PQQA, arXiv 2409.02135) on NVIDIA B200 (sm_100a).
+ *
+ * "P:nnn" cites a line of the paper's text. The path, per step and
+ * per replica s of the S parallel runs:
+ *
+ *   p      = sigmoid(theta)                                    P:143 (north_star)
+ *   q_i    = sum_{j in N(i)} p_j                               CSR gather
+ *   dR/dp  = dl/dp + gamma * ds/dp - alpha_c (p - mu_i)/STD_i   Eq. 6, 7, 10
+ *            MIS / max-clique-on-complement: dl/dp = -1 + lambda q
+ *            Max-Cut:                        dl/dp = -deg + 2 q
+ *            ds/dp = -2 alpha (2p - 1)^(alpha - 1)                     (Eq. 7)
+ *   theta  <- AdamW(theta, dR/dp * p (1 - p))
+ *   gamma  linear from gamma_min to gamma_max
+ *   x      = Theta(p - 1/2)  (theta >= 0, Theta(0) = 1)
+ *   energy = -size + lambda * violations  |  -cut
+ *   best   = argmin energy (lowest global replica on ties)
+ *
+ * Every floating-point result follows the fp32 arithmetic contract written in
+ * DESIGN.md §3 (fixed IEEE operation order, fixed-point int64 replica stats),
+ * so results are bit-identical to the reference oracle and independent of the
+ * number of GPUs the replicas are sharded over.
+ *
+ * CONVENTIONS
+ *  - Every function returns a qqa_status (0 = OK) and never aborts; the
+ *    thread-local qqa_last_error() describes the last failure.
+ *  - All device work is enqueued on the caller's CUDA stream given at create.
+ *    Functions marked (sync) synchronise that stream before returning.
+ *    Asynchronous failures (non-finite values, NCCL errors) are reported by
+ *    the next (sync) call.
+ *  - Host pointers are only read/written during the call. The device
+ *    workspace belongs to the caller and must outlive the handle.
+ *  - Layout of all replica-state arrays crossing this ABI: row-major
+ *    [n][S_local] float32 (variable-major, replica-contiguous), no padding.
+ */
+#ifndef QQA_H_
+#define QQA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QQA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define QQA_API __attribute__((visibility("default")))
+#else
+#define QQA_API
+#endif
+
+typedef enum {
+  QQA_OK = 0,
+  QQA_ERR_INVALID_ARG = 1,   /* bad sizes / hyper-parameters / null pointers          */
+  QQA_ERR_BAD_GRAPH = 2,     /* CSR not symmetric, unsorted, duplicate, loop, range    */
+  QQA_ERR_CUDA = 3,          /* CUDA runtime failure (incl. no device)                 */
+  QQA_ERR_COMM = 4,          /* NCCL failure                                           */
+  QQA_ERR_NONFINITE = 5,     /* a non-finite theta appeared (SPEC.md:396 abort)        */
+  QQA_ERR_UNSUPPORTED = 6,   /* valid input outside what this build implements         */
+  QQA_ERR_WORKSPACE = 7      /* workspace null, misaligned or too small                */
+} qqa_status;
+
+typedef enum {
+  QQA_MIS = 0,        /* maximum independent set, l = -1^T x + lambda x^T A x / 2       */
+  QQA_MAXCUT = 1,     /* max cut, l = -sum_{(i,j) in E} (1 - (2x_i-1)(2x_j-1))/2       */
+  QQA_MAXCLIQUE = 2   /* max clique, solved as MIS on the complement graph (the library
+                         builds the complement on the host at create; n <= 65536)                */
+} qqa_problem;
+
+/* Hyper-parameters and the replica shard of this process. Copied at create. */
+typedef struct {
+  int32_t problem;        /* qqa_problem                                                    */
+  int32_t alpha;          /* alpha-entropy exponent, even, 2..16 (Eq. 7)                   */
+  float penalty;          /* lambda (2); ignored for Max-Cut                        */
+  float comm;             /* alpha_c >= 0, communication strength (Eq. 10)                 */
+  float lr, beta1, beta2, eps, weight_decay;   /* AdamW                     */
+  float init_lo, init_hi; /* theta_0 ~ U(init_lo, init_hi) by a counter hash of
+                             (seed, variable, global replica)                              */
+  uint64_t seed;
+  int32_t S_total;        /* replicas over all ranks (S of Eq. 10), 1..2^20                */
+  int32_t replica_offset; /* first global replica held here                                */
+  int32_t S_local;        /* replicas held here, 1..1024                                   */
+} qqa_config;
+
+/* Undirected simple graph as symmetric CSR, host memory, copied at create.
+ * rowptr[n+1] (rowptr[0] = 0, non-decreasing, rowptr[n] = nnz), colidx[nnz]
+ * strictly ascending within each row, no self-loops, (i,j) present iff (j,i). */
+typedef struct {
+  int32_t n;
+  int64_t nnz;            /* < 2^31 in this build                                          */
+  const int64_t* rowptr;
+  const int32_t* colidx;
+} qqa_graph;
+
+/* Evaluation of one rounded replica (integer counts: bit-exact, order-free). */
+typedef struct {
+  int64_t size;           /* sum_i x_i                                                     */
+  int64_t violations;     /* #{(i<j) in E' : x_i = x_j = 1}, E' = E (complement for clique) */
+  int64_t cut;            /* #{(i<j) in E' : x_i != x_j}                                   */
+  double energy;          /* -size + lambda*violations (MIS, clique) or -cut (Max-Cut)     */
+  int32_t feasible;       /* violations == 0 (always 1 for Max-Cut)                        */
+  int32_t replica;        /* global replica index                                          */
+} qqa_replica_result;
+
+typedef struct qqa_handle qqa_handle;
+
+QQA_API int qqa_version(void);                          /* QQA_ABI_VERSION                          */
+QQA_API const char* qqa_last_error(void);               /* thread-local message of the last failure */
+QQA_API const char* qqa_status_string(int status);
+
+/* Device bytes the workspace must have for (graph, config). Host-only. */
+QQA_API int qqa_workspace_bytes(const qqa_graph* g, const qqa_config* cfg, size_t* bytes);
+
+/* Validate and copy the graph, carve the workspace, initialise the replicas
+ * (theta_0, m = v = 0, p_0, replica statistics). d_workspace: device pointer,
+ * 256-byte aligned, >= qqa_workspace_bytes. stream: cudaStream_t (NULL = legacy
+ * default stream). (sync) */
+QQA_API int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg,
+               void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* Re-initialise the replica state from the seed (as at create); step counter 0.
+ * With a communicator attached this is collective. Async. */
+QQA_API int qqa_reset(qqa_handle* h);
+
+/* Multi-GPU (one process per GPU, replicas sharded: rank r holds
+ * [replica_offset, replica_offset + S_local), S_local equal on all ranks).
+ * Rank 0 calls qqa_nccl_unique_id and broadcasts the 128 bytes; every rank
+ * then calls qqa_attach_comm (collective), which re-initialises the replica
+ * state as qqa_reset does (theta_0 depends only on the global replica index,
+ * so every sharding starts from the same ensemble). Each step then
+ * all-reduces the 2n int64 statistic sums over NCCL. (sync) */
+QQA_API int qqa_nccl_unique_id(uint8_t out[128]);
+QQA_API int qqa_attach_comm(qqa_handle* h, const uint8_t id[128], int rank, int nranks);
+
+/* Run n_steps annealing steps with the given per-step gamma (host float[n_steps]).
+ * The Adam step counter persists across calls. Async. */
+QQA_API int qqa_run(qqa_handle* h, const float* gamma_host, int64_t n_steps);
+
+/* Run steps t0..t1-1 of the linear schedule gamma_t = gmin + (gmax-gmin) t/(T-1)
+ * over total_steps = T; T = 1 gives gmin. Async. */
+QQA_API int qqa_run_linear(qqa_handle* h, float gmin, float gmax, int64_t total_steps, int64_t t0, int64_t t1);
+
+/* Round, evaluate every replica, pick the best over all ranks.
+ * per_replica: host [S_local] or NULL; best_x: host uint8[n] (the best replica's
+ * x on every rank) or NULL. Returns QQA_ERR_NONFINITE if any step produced a
+ * non-finite theta. (sync) */
+QQA_API int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica,
+                       int32_t* best_replica, double* best_energy, uint8_t* best_x);
+
+/* Checkpoint / inspection: host [n][S_local] float arrays, NULL to skip.
+ * p = sigmoid(theta) as used by the next step; step = Adam steps taken. (sync) */
+QQA_API int qqa_get_state(qqa_handle* h, float* theta, float* m, float* v, float* p, int64_t* step);
+/* Replica statistics of the current p: c (shift, float[n]) and the int64 sums
+ * (sumD, sumD2: int64[n], already reduced over ranks). (sync) */
+QQA_API int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2);
+/* Resume from a checkpoint: theta/m/v host [n][S_local]; c = shift of the
+ * statistics (float[n], NULL = 1/2); step = Adam steps taken. Collective with a
+ * communicator. (sync) */
+QQA_API int qqa_set_state(qqa_handle* h, const float* theta, const float* m, const float* v,
+                  const float* c, int64_t step);
+
+/* Time every step-kernel launch with CUDA events on the handle's stream. */
+QQA_API int qqa_profile(qqa_handle* h, int enable);
+/* Sum of step-kernel durations (ms) and launch count since enable. (sync) */
+QQA_API int qqa_profile_read(qqa_handle* h, double* step_kernel_ms, int64_t* step_launches);
+
+/* Kernels launched by this handle since create (all kinds). Host-only. */
+QQA_API int qqa_launch_count(qqa_handle* h, int64_t* launches);
+
+/* Free the handle (and its communicator); the workspace is not freed. (sync) */
+QQA_API int qqa_destroy(qqa_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QQA_H_ */

@@ -59,6 +59,8 @@ def _L():
         cfgp = ctypes.POINTER(OcCfg)
         lib.oc_sigmoid.restype = ctypes.c_float
         lib.oc_sigmoid.argtypes = [ctypes.c_float]
+        lib.oc_sigmoid_array.restype = None
+        lib.oc_sigmoid_array.argtypes = [ctypes.c_int64, f32, f32]
         lib.oc_exp_neg.restype = ctypes.c_float
         lib.oc_exp_neg.argtypes = [ctypes.c_float]
         lib.oc_step_scalars.restype = None
@@ -112,8 +114,9 @@ class State:
 # ------------------------------------------------------------ primitives
 def sigmoid(theta) -> np.ndarray:
     th = np.ascontiguousarray(theta, dtype=np.float32).ravel()
-    f = _L().oc_sigmoid
-    return np.array([f(float(x)) for x in th], dtype=np.float32).reshape(np.shape(theta))
+    out = np.empty_like(th)
+    _L().oc_sigmoid_array(th.size, th, out)
+    return out.reshape(np.shape(theta))
 
 
 def exp_neg(a: float) -> float:

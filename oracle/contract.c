@@ -81,6 +81,10 @@ float oc_sigmoid(float theta) {
     return (theta >= 0.0f) ? 1.0f / den : E / den;
 }
 
+void oc_sigmoid_array(int64_t n, const float* in, float* out) {
+    for (int64_t k = 0; k < n; ++k) out[k] = oc_sigmoid(in[k]);
+}
+
 /* ------------------------------------------------------ step scalars ---- */
 /* out = { k_t = -2 alpha gamma_t, a_t = 1 - lr wd, s_t = lr/(1-b1^t), r_t = 1/sqrt(1-b2^t) } */
 void oc_step_scalars(const oc_cfg* c, int64_t t, float gamma_t, float* out) {

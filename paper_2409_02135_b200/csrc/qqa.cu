@@ -1,0 +1,686 @@
+// qqa.cu -- host engine and C ABI of libqqa.so (declared in include/qqa.h).
+//
+// One handle = one GPU's shard of the replica ensemble. Per annealing step the
+// engine launches ONE fused kernel (k_step) on the caller's stream; with a
+// communicator attached it follows it with one ncclAllReduce of the 2n int64
+// replica-statistic sums (the only cross-GPU exchange of the method, Eq. 10).
+#include "qqa.h"
+#include "qqa_kernels.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+#define QQA_CUDA(call)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(QQA_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define QQA_NCCL(call)                                                                      \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      return fail(QQA_ERR_COMM, std::string(#call) + ": " + ncclGetErrorString(r_));        \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Shape {
+  int n = 0;
+  int64_t nnz = 0;   // of the graph the kernels walk (complement for max clique)
+  int S_local = 0, S_total = 0, S_p = 0, S_p4 = 0, W = 0, lanes = 0, vpl = 0;
+};
+
+struct Layout {
+  size_t rowptr, colidx, theta, m, v, p0, p1, c0, c1, s0, s1, flag, X, counts, energy, best, beste, xbuf, total;
+};
+
+Layout make_layout(const Shape& s) {
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = up(o + std::max<size_t>(bytes, 1), kAlign); return at; };
+  const size_t ns = (size_t)s.n * s.S_p * sizeof(float);
+  L.rowptr = take(((size_t)s.n + 1) * sizeof(int));
+  L.colidx = take((size_t)s.nnz * sizeof(int));
+  L.theta = take(ns);
+  L.m = take(ns);
+  L.v = take(ns);
+  L.p0 = take(ns);
+  L.p1 = take(ns);
+  L.c0 = take((size_t)s.n * sizeof(float));
+  L.c1 = take((size_t)s.n * sizeof(float));
+  L.s0 = take(2 * (size_t)s.n * sizeof(long long));
+  L.s1 = take(2 * (size_t)s.n * sizeof(long long));
+  L.flag = take(4 * sizeof(int));
+  L.X = take((size_t)s.n * s.W * sizeof(uint32_t));
+  L.counts = take(3 * (size_t)s.S_total * sizeof(long long));
+  L.energy = take((size_t)s.S_total * sizeof(double));
+  L.best = take(sizeof(int));
+  L.beste = take(sizeof(double));
+  L.xbuf = take((size_t)s.n);
+  L.total = o;
+  return L;
+}
+
+int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
+
+int check_config(const qqa_config* c) {
+  if (!c) return fail(QQA_ERR_INVALID_ARG, "config is NULL");
+  if (c->problem < 0 || c->problem > 2) return fail(QQA_ERR_INVALID_ARG, "problem must be 0 (MIS), 1 (Max-Cut) or 2 (max clique)");
+  if (c->alpha < 2 || c->alpha > 16 || (c->alpha & 1)) return fail(QQA_ERR_INVALID_ARG, "alpha must be even, 2..16 (Eq. 7)");
+  if (c->S_total < 1 || c->S_total > (1 << 20)) return fail(QQA_ERR_INVALID_ARG, "S_total must be in 1..2^20");
+  if (c->S_local < 1) return fail(QQA_ERR_INVALID_ARG, "S_local must be >= 1");
+  if (c->S_local > 1024) return fail(QQA_ERR_UNSUPPORTED, "S_local > 1024 replicas per GPU is not supported by this build");
+  if (c->replica_offset < 0 || (int64_t)c->replica_offset + c->S_local > c->S_total)
+    return fail(QQA_ERR_INVALID_ARG, "replica shard [offset, offset+S_local) must lie in [0, S_total)");
+  if (!std::isfinite(c->lr) || !std::isfinite(c->penalty) || !std::isfinite(c->comm) || c->comm < 0.0f ||
+      !(c->beta1 >= 0.0f && c->beta1 < 1.0f) || !(c->beta2 >= 0.0f && c->beta2 < 1.0f) || !(c->eps >= 0.0f) ||
+      !std::isfinite(c->weight_decay) || !std::isfinite(c->init_lo) || !std::isfinite(c->init_hi))
+    return fail(QQA_ERR_INVALID_ARG, "hyper-parameter out of range (lr, penalty, comm>=0, 0<=beta<1, eps>=0 ...)");
+  return QQA_OK;
+}
+
+int check_graph(const qqa_graph* g) {
+  if (!g) return fail(QQA_ERR_INVALID_ARG, "graph is NULL");
+  if (g->n < 0 || g->nnz < 0) return fail(QQA_ERR_INVALID_ARG, "negative n or nnz");
+  if (g->n > 0 && !g->rowptr) return fail(QQA_ERR_INVALID_ARG, "rowptr is NULL");
+  if (g->nnz > 0 && !g->colidx) return fail(QQA_ERR_INVALID_ARG, "colidx is NULL");
+  if (g->nnz >= (int64_t)INT32_MAX) return fail(QQA_ERR_UNSUPPORTED, "nnz >= 2^31 not supported by this build");
+  if (g->n == 0) return QQA_OK;
+  if (g->rowptr[0] != 0 || g->rowptr[g->n] != g->nnz) return fail(QQA_ERR_BAD_GRAPH, "rowptr[0] != 0 or rowptr[n] != nnz");
+  for (int i = 0; i < g->n; ++i)
+    if (g->rowptr[i + 1] < g->rowptr[i]) return fail(QQA_ERR_BAD_GRAPH, "rowptr is not non-decreasing");
+  return QQA_OK;
+}
+
+int64_t problem_nnz(const qqa_graph* g, int problem) {
+  if (problem == QQA_MAXCLIQUE) return (int64_t)g->n * (g->n - 1) - g->nnz;
+  return g->nnz;
+}
+
+int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
+  int st = check_graph(g);
+  if (st) return st;
+  if ((st = check_config(c))) return st;
+  if (c->problem == QQA_MAXCLIQUE && g->n > 65536) return fail(QQA_ERR_UNSUPPORTED, "max clique: n > 65536 (dense complement)");
+  s.n = g->n;
+  s.nnz = problem_nnz(g, c->problem);
+  if (s.nnz >= (int64_t)INT32_MAX) return fail(QQA_ERR_UNSUPPORTED, "complement nnz >= 2^31");
+  s.S_local = c->S_local;
+  s.S_total = c->S_total;
+  s.S_p = (c->S_local + 7) / 8 * 8;
+  s.S_p4 = s.S_p / 4;
+  s.W = (c->S_local + 31) / 32;
+  s.lanes = std::min(32, next_pow2(s.S_p4));
+  s.vpl = next_pow2((s.S_p4 + s.lanes - 1) / s.lanes);
+  return QQA_OK;
+}
+
+// Complement CSR (max clique = MIS on the complement graph).
+void build_complement(const qqa_graph* g, std::vector<int>& rp, std::vector<int>& ci) {
+  const int n = g->n;
+  rp.assign((size_t)n + 1, 0);
+  ci.clear();
+  ci.reserve((size_t)((int64_t)n * (n - 1) - g->nnz));
+  std::vector<char> mark((size_t)n, 0);
+  for (int i = 0; i < n; ++i) {
+    for (int64_t e = g->rowptr[i]; e < g->rowptr[i + 1]; ++e) mark[g->colidx[e]] = 1;
+    for (int j = 0; j < n; ++j)
+      if (j != i && !mark[j]) ci.push_back(j);
+    for (int64_t e = g->rowptr[i]; e < g->rowptr[i + 1]; ++e) mark[g->colidx[e]] = 0;
+    rp[i + 1] = (int)ci.size();
+  }
+}
+
+}  // namespace
+
+struct qqa_handle {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  qqa_config cfg{};
+  Shape s;
+  Layout L{};
+  char* ws = nullptr;
+  int* rowptr = nullptr;
+  int* colidx = nullptr;
+  float *theta = nullptr, *m = nullptr, *v = nullptr, *p[2] = {nullptr, nullptr}, *c[2] = {nullptr, nullptr};
+  long long* sums[2] = {nullptr, nullptr};
+  int* flag = nullptr;
+  uint32_t* X = nullptr;
+  unsigned long long* counts = nullptr;
+  double* energy = nullptr;
+  int* best = nullptr;
+  double* beste = nullptr;
+  uint8_t* xbuf = nullptr;
+  int cur = 0;
+  int64_t step = 0;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  int grid_step = 0, grid_init = 0;
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;  // pairs (start, end)
+  size_t ev_used = 0;
+  int64_t prof_launches = 0;
+  double prof_ms = 0.0;
+  int64_t launches = 0;
+};
+
+namespace {
+
+using StepKernel = void (*)(const qqa::StepParams);
+using InitKernel = void (*)(const qqa::InitParams);
+
+bool pick_kernels(int lanes, int vpl, StepKernel& ks, InitKernel& ki) {
+#define QQA_CASE(L, V)                                   \
+  if (lanes == L && vpl == V) {                          \
+    ks = qqa::k_step<L, V>;                              \
+    ki = qqa::k_init<L, V>;                              \
+    return true;                                         \
+  }
+  QQA_CASE(2, 1) QQA_CASE(4, 1) QQA_CASE(8, 1) QQA_CASE(16, 1)
+  QQA_CASE(32, 1) QQA_CASE(32, 2) QQA_CASE(32, 4) QQA_CASE(32, 8)
+#undef QQA_CASE
+  return false;
+}
+
+int grid_for(const void* kernel, int sm_count, int n, int lanes, int& grid) {
+  int per_sm = 0;
+  QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
+  const int need = (int)std::max<int64_t>(1, ((int64_t)n * lanes + 255) / 256);
+  grid = std::max(1, std::min(need, std::max(1, per_sm) * sm_count));
+  return QQA_OK;
+}
+
+int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
+  StepKernel ks;
+  InitKernel ki;
+  pick_kernels(h->s.lanes, h->s.vpl, ks, ki);
+  qqa::InitParams P{};
+  P.theta = h->theta; P.m = h->m; P.v = h->v; P.p0 = h->p[0]; P.p1 = h->p[1];
+  P.c = h->c[0]; P.sums = h->sums[0];
+  P.n = h->s.n; P.S_p4 = h->s.S_p4; P.S_local = h->s.S_local; P.S_total = h->s.S_total;
+  P.replica_offset = h->cfg.replica_offset;
+  // base = mix64(seed), computed on the host with the same mixer
+  uint64_t z = h->cfg.seed + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  P.base = z ^ (z >> 31);
+  P.lo = (double)h->cfg.init_lo;
+  P.hi = (double)h->cfg.init_hi;
+  P.use_given = use_given ? 1 : 0;
+  P.c_given = c_given;
+  if (h->s.n > 0) {
+    ki<<<h->grid_init, 256, 0, h->stream>>>(P);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  if (h->comm) {
+    QQA_NCCL(ncclAllReduce(h->sums[0], h->sums[0], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
+  }
+  h->cur = 0;
+  QQA_CUDA(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
+  return QQA_OK;
+}
+
+int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
+  if (n_steps < 0) return fail(QQA_ERR_INVALID_ARG, "n_steps < 0");
+  if (n_steps > 0 && !gamma) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
+  StepKernel ks;
+  InitKernel ki;
+  pick_kernels(h->s.lanes, h->s.vpl, ks, ki);
+  const qqa_config& c = h->cfg;
+  qqa::StepParams P{};
+  P.rowptr = h->rowptr; P.colidx = h->colidx; P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
+  P.n = h->s.n; P.S_p4 = h->s.S_p4; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
+  P.problem = c.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;  // clique = MIS on the complement
+  P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
+  P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
+  P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
+  P.eps = c.eps;
+  for (int64_t k = 0; k < n_steps; ++k) {
+    const int64_t t = h->step + 1;  // Adam step index (reading R11)
+    P.kt = (float)(-2.0 * (double)c.alpha * (double)gamma[k]);
+    P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
+    P.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
+    P.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
+    const int a = h->cur, b = h->cur ^ 1;
+    P.p_cur = h->p[a]; P.p_next = h->p[b];
+    P.c_cur = h->c[a]; P.c_next = h->c[b];
+    P.sums_cur = h->sums[a]; P.sums_next = h->sums[b];
+    if (h->s.n > 0) {
+      if (h->profiling) {
+        if (h->ev_used + 2 > h->ev.size()) {
+          for (int e = 0; e < 256; ++e) {
+            cudaEvent_t x;
+            QQA_CUDA(cudaEventCreate(&x));
+            h->ev.push_back(x);
+          }
+        }
+        QQA_CUDA(cudaEventRecord(h->ev[h->ev_used], h->stream));
+      }
+      ks<<<h->grid_step, 256, 0, h->stream>>>(P);
+      QQA_CUDA(cudaGetLastError());
+      h->launches++;
+      if (h->profiling) {
+        QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
+        h->ev_used += 2;
+        h->prof_launches++;
+      }
+    }
+    if (h->comm) {
+      QQA_NCCL(ncclAllReduce(h->sums[b], h->sums[b], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
+    }
+    h->cur = b;
+    h->step = t;
+  }
+  return QQA_OK;
+}
+
+int set_device(qqa_handle* h) {
+  int cur = -1;
+  QQA_CUDA(cudaGetDevice(&cur));
+  if (cur != h->device) QQA_CUDA(cudaSetDevice(h->device));
+  return QQA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qqa_version(void) { return QQA_ABI_VERSION; }
+
+const char* qqa_last_error(void) { return g_last_error.c_str(); }
+
+const char* qqa_status_string(int status) {
+  switch (status) {
+    case QQA_OK: return "ok";
+    case QQA_ERR_INVALID_ARG: return "invalid argument";
+    case QQA_ERR_BAD_GRAPH: return "bad graph";
+    case QQA_ERR_CUDA: return "cuda error";
+    case QQA_ERR_COMM: return "communication error";
+    case QQA_ERR_NONFINITE: return "non-finite value";
+    case QQA_ERR_UNSUPPORTED: return "unsupported";
+    case QQA_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int qqa_workspace_bytes(const qqa_graph* g, const qqa_config* cfg, size_t* bytes) {
+  if (!bytes) return fail(QQA_ERR_INVALID_ARG, "bytes is NULL");
+  Shape s;
+  int st = make_shape(g, cfg, s);
+  if (st) return st;
+  *bytes = make_layout(s).total;
+  return QQA_OK;
+}
+
+int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void* d_workspace,
+               size_t workspace_bytes, void* stream) {
+  if (!out) return fail(QQA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  Shape s;
+  int st = make_shape(g, cfg, s);
+  if (st) return st;
+  const Layout L = make_layout(s);
+  if (!d_workspace || ((uintptr_t)d_workspace % kAlign) != 0)
+    return fail(QQA_ERR_WORKSPACE, "workspace is NULL or not 256-byte aligned");
+  if (workspace_bytes < L.total)
+    return fail(QQA_ERR_WORKSPACE, "workspace has " + std::to_string(workspace_bytes) + " bytes, needs " +
+                                       std::to_string(L.total));
+  int dev = 0, ndev = 0;
+  QQA_CUDA(cudaGetDeviceCount(&ndev));
+  QQA_CUDA(cudaGetDevice(&dev));
+  cudaPointerAttributes attr{};
+  QQA_CUDA(cudaPointerGetAttributes(&attr, d_workspace));
+  if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
+    return fail(QQA_ERR_WORKSPACE, "workspace is not device memory");
+
+  qqa_handle* h = new qqa_handle();
+  h->device = attr.device;
+  h->stream = (cudaStream_t)stream;
+  h->cfg = *cfg;
+  h->s = s;
+  h->L = L;
+  auto cleanup = [&](int status) { delete h; return status; };
+  if ((st = set_device(h))) return cleanup(st);
+  {
+    cudaError_t e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+    if (e != cudaSuccess) return cleanup(fail(QQA_ERR_CUDA, cudaGetErrorString(e)));
+  }
+  char* ws = (char*)d_workspace;
+  h->ws = ws;
+  h->rowptr = (int*)(ws + L.rowptr);
+  h->colidx = (int*)(ws + L.colidx);
+  h->theta = (float*)(ws + L.theta);
+  h->m = (float*)(ws + L.m);
+  h->v = (float*)(ws + L.v);
+  h->p[0] = (float*)(ws + L.p0);
+  h->p[1] = (float*)(ws + L.p1);
+  h->c[0] = (float*)(ws + L.c0);
+  h->c[1] = (float*)(ws + L.c1);
+  h->sums[0] = (long long*)(ws + L.s0);
+  h->sums[1] = (long long*)(ws + L.s1);
+  h->flag = (int*)(ws + L.flag);
+  h->X = (uint32_t*)(ws + L.X);
+  h->counts = (unsigned long long*)(ws + L.counts);
+  h->energy = (double*)(ws + L.energy);
+  h->best = (int*)(ws + L.best);
+  h->beste = (double*)(ws + L.beste);
+  h->xbuf = (uint8_t*)(ws + L.xbuf);
+
+  // Graph -> device (int32 offsets). Max clique walks the complement graph.
+  std::vector<int> rp32, ci_c;
+  const int32_t* ci_src = g->colidx;
+  if (cfg->problem == QQA_MAXCLIQUE) {
+    build_complement(g, rp32, ci_c);
+    ci_src = ci_c.data();
+  } else {
+    rp32.resize((size_t)s.n + 1);
+    for (int i = 0; i <= s.n; ++i) rp32[i] = (int)(s.n ? g->rowptr[i] : 0);
+  }
+#define QQA_CUDA_C(call)                                                                        \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return cleanup(fail(QQA_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)));   \
+  } while (0)
+  QQA_CUDA_C(cudaMemcpyAsync(h->rowptr, rp32.data(), rp32.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  if (s.nnz > 0)
+    QQA_CUDA_C(cudaMemcpyAsync(h->colidx, ci_src, (size_t)s.nnz * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  QQA_CUDA_C(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
+  // theta/m/v padding and both p buffers start at zero / sigmoid(0)
+  for (float* buf : {h->theta, h->m, h->v})
+    QQA_CUDA_C(cudaMemsetAsync(buf, 0, (size_t)s.n * s.S_p * sizeof(float), h->stream));
+  if (cfg->problem != QQA_MAXCLIQUE && s.n > 0 && s.nnz > 0) {
+    const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
+    qqa::k_validate<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, s.n, h->flag);
+    QQA_CUDA_C(cudaGetLastError());
+    h->launches++;
+    int flag = 0;
+    QQA_CUDA_C(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    QQA_CUDA_C(cudaStreamSynchronize(h->stream));
+    if (flag) {
+      std::string why;
+      if (flag & 2) why += " column out of range;";
+      if (flag & 4) why += " row not strictly ascending (unsorted or duplicate);";
+      if (flag & 8) why += " self-loop;";
+      if (flag & 16) why += " not symmetric;";
+      return cleanup(fail(QQA_ERR_BAD_GRAPH, "graph rejected:" + why));
+    }
+  }
+  StepKernel ks;
+  InitKernel ki;
+  if (!pick_kernels(s.lanes, s.vpl, ks, ki)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
+  if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
+  if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
+  if ((st = launch_init(h, false, nullptr))) return cleanup(st);
+  QQA_CUDA_C(cudaStreamSynchronize(h->stream));
+#undef QQA_CUDA_C
+  *out = h;
+  return QQA_OK;
+}
+
+int qqa_reset(qqa_handle* h) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  h->step = 0;
+  return launch_init(h, false, nullptr);
+}
+
+int qqa_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return fail(QQA_ERR_INVALID_ARG, "out is NULL");
+  ncclUniqueId id;
+  QQA_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out, &id, 128);
+  return QQA_OK;
+}
+
+int qqa_attach_comm(qqa_handle* h, const uint8_t id[128], int rank, int nranks) {
+  if (!h || !id) return fail(QQA_ERR_INVALID_ARG, "handle or id is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(QQA_ERR_INVALID_ARG, "bad rank / nranks");
+  if ((int64_t)h->s.S_local * nranks != h->s.S_total || h->cfg.replica_offset != rank * h->s.S_local)
+    return fail(QQA_ERR_INVALID_ARG, "sharding must be S_total = nranks * S_local and replica_offset = rank * S_local");
+  int st = set_device(h);
+  if (st) return st;
+  if (h->comm) {
+    ncclCommDestroy(h->comm);
+    h->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  QQA_NCCL(ncclCommInitRank(&h->comm, nranks, uid, rank));
+  h->rank = rank;
+  h->nranks = nranks;
+  h->step = 0;
+  if ((st = launch_init(h, false, nullptr))) return st;
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  return QQA_OK;
+}
+
+int qqa_run(qqa_handle* h, const float* gamma_host, int64_t n_steps) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  return do_steps(h, gamma_host, n_steps);
+}
+
+int qqa_run_linear(qqa_handle* h, float gmin, float gmax, int64_t total_steps, int64_t t0, int64_t t1) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  if (total_steps < 1 || t0 < 0 || t1 < t0 || t1 > total_steps)
+    return fail(QQA_ERR_INVALID_ARG, "need 0 <= t0 <= t1 <= total_steps, total_steps >= 1");
+  int st = set_device(h);
+  if (st) return st;
+  std::vector<float> gam((size_t)(t1 - t0));
+  for (int64_t t = t0; t < t1; ++t)  // P:245, P:667 (reading R10)
+    gam[(size_t)(t - t0)] = (total_steps == 1)
+        ? gmin
+        : (float)((double)gmin + (((double)gmax - (double)gmin) * (double)t) / (double)(total_steps - 1));
+  return do_steps(h, gam.data(), t1 - t0);
+}
+
+int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* best_replica,
+                       double* best_energy, uint8_t* best_x) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  const Shape& s = h->s;
+  const int off = h->cfg.replica_offset;
+  // K3: round + pack
+  if (s.n > 0) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)s.n * s.W * 32 + 255) / 256, (int64_t)h->sm_count * 16));
+    qqa::k_pack<<<blocks, 256, 0, h->stream>>>(h->theta, h->X, s.n, s.S_p, s.S_local, s.W);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  // K4: counts of the local replicas, placed at their global slots
+  QQA_CUDA(cudaMemsetAsync(h->counts, 0, 3 * (size_t)s.S_total * sizeof(long long), h->stream));
+  if (s.n > 0) {
+    const int R = (int)std::max<int64_t>(1, std::min<int64_t>(s.n, (int64_t)h->sm_count * 64 / s.W));
+    const int64_t warps = (int64_t)s.W * R;
+    const int blocks = (int)((warps + 7) / 8);
+    qqa::k_eval<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, h->X, s.n, s.W, R, s.S_local,
+                                               h->counts + 3 * (size_t)off);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  if (h->comm && h->nranks > 1) {
+    QQA_NCCL(ncclAllGather(h->counts + 3 * (size_t)off, h->counts, 3 * (size_t)s.S_local, ncclInt64, h->comm, h->stream));
+  }
+  // K5: energies + argmin over all replicas
+  qqa::k_argmin<<<1, 1024, 0, h->stream>>>((const long long*)h->counts, s.S_total,
+                                            h->cfg.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS,
+                                            (double)h->cfg.penalty, h->energy, h->best, h->beste);
+  QQA_CUDA(cudaGetLastError());
+  h->launches++;
+  int best = 0, flag = 0;
+  double be = 0.0;
+  QQA_CUDA(cudaMemcpyAsync(&best, h->best, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  QQA_CUDA(cudaMemcpyAsync(&be, h->beste, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  QQA_CUDA(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  std::vector<long long> cnt;
+  std::vector<double> en;
+  if (per_replica) {
+    cnt.resize(3 * (size_t)s.S_local);
+    en.resize((size_t)s.S_local);
+    QQA_CUDA(cudaMemcpyAsync(cnt.data(), h->counts + 3 * (size_t)off, cnt.size() * sizeof(long long),
+                             cudaMemcpyDeviceToHost, h->stream));
+    QQA_CUDA(cudaMemcpyAsync(en.data(), h->energy + off, en.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                             h->stream));
+  }
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  if (best_x && s.n > 0) {
+    const int owner = best / s.S_local;
+    if (!h->comm || h->nranks == 1 || owner == h->rank) {
+      qqa::k_extract<<<std::max(1, std::min((s.n + 255) / 256, h->sm_count * 4)), 256, 0, h->stream>>>(
+          h->X, s.n, s.W, best - off, h->xbuf);
+      QQA_CUDA(cudaGetLastError());
+      h->launches++;
+    }
+    if (h->comm && h->nranks > 1) {
+      QQA_NCCL(ncclBroadcast(h->xbuf, h->xbuf, (size_t)s.n, ncclUint8, owner, h->comm, h->stream));
+    }
+    QQA_CUDA(cudaMemcpyAsync(best_x, h->xbuf, (size_t)s.n, cudaMemcpyDeviceToHost, h->stream));
+    QQA_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  if (h->comm) {
+    ncclResult_t async_err = ncclSuccess;
+    ncclCommGetAsyncError(h->comm, &async_err);
+    if (async_err != ncclSuccess) return fail(QQA_ERR_COMM, ncclGetErrorString(async_err));
+  }
+  if (per_replica) {
+    for (int k = 0; k < s.S_local; ++k) {
+      qqa_replica_result& r = per_replica[k];
+      r.size = cnt[3 * k + 0];
+      r.violations = cnt[3 * k + 1];
+      r.cut = cnt[3 * k + 2];
+      r.energy = en[k];
+      r.feasible = (h->cfg.problem == QQA_MAXCUT) ? 1 : (r.violations == 0);
+      r.replica = off + k;
+    }
+  }
+  if (best_replica) *best_replica = best;
+  if (best_energy) *best_energy = be;
+  if (flag & 1) return fail(QQA_ERR_NONFINITE, "a non-finite theta appeared during the run");
+  return QQA_OK;
+}
+
+int qqa_get_state(qqa_handle* h, float* theta, float* m, float* v, float* p, int64_t* step) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  const Shape& s = h->s;
+  const size_t dp = (size_t)s.S_p * sizeof(float), hp = (size_t)s.S_local * sizeof(float);
+  const float* src[4] = {h->theta, h->m, h->v, h->p[h->cur]};
+  float* dst[4] = {theta, m, v, p};
+  for (int k = 0; k < 4; ++k)
+    if (dst[k] && s.n > 0)
+      QQA_CUDA(cudaMemcpy2DAsync(dst[k], hp, src[k], dp, hp, (size_t)s.n, cudaMemcpyDeviceToHost, h->stream));
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  if (step) *step = h->step;
+  return QQA_OK;
+}
+
+int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  const size_t n = (size_t)h->s.n;
+  if (c && n) QQA_CUDA(cudaMemcpyAsync(c, h->c[h->cur], n * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (sumD && n)
+    QQA_CUDA(cudaMemcpyAsync(sumD, h->sums[h->cur], n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  if (sumD2 && n)
+    QQA_CUDA(cudaMemcpyAsync(sumD2, h->sums[h->cur] + n, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  return QQA_OK;
+}
+
+int qqa_set_state(qqa_handle* h, const float* theta, const float* m, const float* v, const float* c, int64_t step) {
+  if (!h || !theta || !m || !v) return fail(QQA_ERR_INVALID_ARG, "handle, theta, m or v is NULL");
+  if (step < 0) return fail(QQA_ERR_INVALID_ARG, "step < 0");
+  int st = set_device(h);
+  if (st) return st;
+  const Shape& s = h->s;
+  const size_t dp = (size_t)s.S_p * sizeof(float), hp = (size_t)s.S_local * sizeof(float);
+  for (float* buf : {h->theta, h->m, h->v})
+    QQA_CUDA(cudaMemsetAsync(buf, 0, (size_t)s.n * dp, h->stream));
+  const float* src[3] = {theta, m, v};
+  float* dst[3] = {h->theta, h->m, h->v};
+  for (int k = 0; k < 3; ++k)
+    if (s.n > 0)
+      QQA_CUDA(cudaMemcpy2DAsync(dst[k], dp, src[k], hp, hp, (size_t)s.n, cudaMemcpyHostToDevice, h->stream));
+  const float* cdev = nullptr;
+  if (c && s.n > 0) {
+    QQA_CUDA(cudaMemcpyAsync(h->c[1], c, (size_t)s.n * sizeof(float), cudaMemcpyHostToDevice, h->stream));
+    cdev = h->c[1];
+  }
+  if ((st = launch_init(h, true, cdev))) return st;
+  h->step = step;
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  return QQA_OK;
+}
+
+int qqa_profile(qqa_handle* h, int enable) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  h->profiling = enable != 0;
+  h->ev_used = 0;
+  h->prof_launches = 0;
+  h->prof_ms = 0.0;
+  return QQA_OK;
+}
+
+int qqa_profile_read(qqa_handle* h, double* step_kernel_ms, int64_t* step_launches) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  double total = h->prof_ms;
+  for (size_t k = 0; k + 1 < h->ev_used; k += 2) {
+    float ms = 0.f;
+    QQA_CUDA(cudaEventElapsedTime(&ms, h->ev[k], h->ev[k + 1]));
+    total += ms;
+  }
+  h->prof_ms = total;
+  h->ev_used = 0;
+  if (step_kernel_ms) *step_kernel_ms = total;
+  if (step_launches) *step_launches = h->prof_launches;
+  return QQA_OK;
+}
+
+int qqa_launch_count(qqa_handle* h, int64_t* launches) {
+  if (!h || !launches) return fail(QQA_ERR_INVALID_ARG, "handle or launches is NULL");
+  *launches = h->launches;
+  return QQA_OK;
+}
+
+int qqa_destroy(qqa_handle* h) {
+  if (!h) return QQA_OK;
+  int st = set_device(h);
+  if (st) return st;
+  cudaStreamSynchronize(h->stream);
+  if (h->comm) ncclCommDestroy(h->comm);
+  for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  delete h;
+  return QQA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""Thin Python binding of the C ABI (include/qqa.h): argument marshalling only.
+
+Torch supplies device memory (the workspace), the CUDA stream and, for
+multi-GPU, the process group used to share the NCCL unique id. Every step of
+the method runs in libqqa.so's kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import Config, Graph, ReplicaResult, check, lib
+
+DEFAULTS = dict(alpha=2, penalty=2.0, comm=0.1, lr=1.0, beta1=0.9, beta2=0.999, eps=1e-8,
+                weight_decay=0.01, init_lo=-0.01, init_hi=0.01)
+
+
+def make_config(problem="mis", S_total=16, seed=1, replica_offset=0, S_local=None, **hp) -> Config:
+    kw = dict(DEFAULTS)
+    kw.update(hp)
+    pid = _lib.PROBLEMS[problem] if isinstance(problem, str) else int(problem)
+    return Config(pid, int(kw["alpha"]), kw["penalty"], kw["comm"], kw["lr"], kw["beta1"], kw["beta2"],
+                  kw["eps"], kw["weight_decay"], kw["init_lo"], kw["init_hi"], seed & 0xFFFFFFFFFFFFFFFF,
+                  int(S_total), int(replica_offset), int(S_total if S_local is None else S_local))
+
+
+def _as_graph(rowptr: np.ndarray, colidx: np.ndarray) -> Graph:
+    n = len(rowptr) - 1
+    return Graph(n, int(rowptr[-1]) if n >= 0 else 0, rowptr.ctypes.data, colidx.ctypes.data)
+
+
+def workspace_bytes(rowptr, colidx, cfg: Config) -> int:
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    colidx = np.ascontiguousarray(colidx, np.int32)
+    g = _as_graph(rowptr, colidx)
+    out = ctypes.c_size_t(0)
+    check(lib.qqa_workspace_bytes(ctypes.byref(g), ctypes.byref(cfg), ctypes.byref(out)))
+    return int(out.value)
+
+
+@dataclass
+class Result:
+    best_replica: int
+    best_energy: float
+    best_x: np.ndarray | None
+    per_replica: np.ndarray | None  # structured: size, violations, cut, energy, feasible, replica
+
+
+class Solver:
+    """One GPU's shard of the PQQA replica ensemble behind the C ABI."""
+
+    def __init__(self, rowptr, colidx, cfg: Config, device=None, stream=None, workspace=None):
+        import torch
+
+        self._torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.cfg = cfg
+        self.rowptr = np.ascontiguousarray(rowptr, np.int64)
+        self.colidx = np.ascontiguousarray(colidx, np.int32)
+        self.n = len(self.rowptr) - 1
+        self.S_local = cfg.S_local
+        g = _as_graph(self.rowptr, self.colidx)
+        nbytes = ctypes.c_size_t(0)
+        check(lib.qqa_workspace_bytes(ctypes.byref(g), ctypes.byref(cfg), ctypes.byref(nbytes)))
+        self.workspace_bytes = int(nbytes.value)
+        if workspace is None or workspace.numel() < self.workspace_bytes:
+            workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+        self.workspace = workspace
+        self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
+        self._h = ctypes.c_void_p(0)
+        with torch.cuda.device(self.device):
+            check(lib.qqa_create(ctypes.byref(self._h), ctypes.byref(g), ctypes.byref(cfg),
+                                 ctypes.c_void_p(workspace.data_ptr()), ctypes.c_size_t(workspace.numel()),
+                                 ctypes.c_void_p(self.stream.cuda_stream)))
+
+    # ------------------------------------------------------------------ run
+    def reset(self):
+        check(lib.qqa_reset(self._h))
+
+    def run(self, gammas):
+        g = np.ascontiguousarray(gammas, np.float32)
+        check(lib.qqa_run(self._h, g.ctypes.data, len(g)))
+
+    def run_linear(self, gamma_min, gamma_max, total_steps, t0=0, t1=None):
+        t1 = total_steps if t1 is None else t1
+        check(lib.qqa_run_linear(self._h, gamma_min, gamma_max, total_steps, t0, t1))
+
+    def round_evaluate(self, want_x=True, want_replicas=True) -> Result:
+        per = (ReplicaResult * self.S_local)() if want_replicas else None
+        x = np.zeros(self.n, np.uint8) if want_x else None
+        best = ctypes.c_int32(-1)
+        be = ctypes.c_double(0.0)
+        check(lib.qqa_round_evaluate(self._h, ctypes.cast(per, ctypes.c_void_p) if per is not None else None,
+                                     ctypes.byref(best), ctypes.byref(be),
+                                     x.ctypes.data if x is not None else None))
+        arr = None
+        if per is not None:
+            arr = np.ctypeslib.as_array(per).copy()
+        return Result(int(best.value), float(be.value), x, arr)
+
+    # --------------------------------------------------------------- state
+    def get_state(self):
+        shp = (self.n, self.S_local)
+        th, m, v, p = (np.empty(shp, np.float32) for _ in range(4))
+        step = ctypes.c_int64(0)
+        check(lib.qqa_get_state(self._h, th.ctypes.data, m.ctypes.data, v.ctypes.data, p.ctypes.data,
+                                ctypes.byref(step)))
+        return dict(theta=th, m=m, v=v, p=p, step=int(step.value))
+
+    def get_stats(self):
+        c = np.empty(self.n, np.float32)
+        a = np.empty(self.n, np.int64)
+        b = np.empty(self.n, np.int64)
+        check(lib.qqa_get_stats(self._h, c.ctypes.data, a.ctypes.data, b.ctypes.data))
+        return dict(c=c, sumD=a, sumD2=b)
+
+    def set_state(self, theta, m, v, step, c=None):
+        th = np.ascontiguousarray(theta, np.float32)
+        mm = np.ascontiguousarray(m, np.float32)
+        vv = np.ascontiguousarray(v, np.float32)
+        cc = None if c is None else np.ascontiguousarray(c, np.float32)
+        check(lib.qqa_set_state(self._h, th.ctypes.data, mm.ctypes.data, vv.ctypes.data,
+                                cc.ctypes.data if cc is not None else None, int(step)))
+
+    # ------------------------------------------------------------ multi-GPU
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        check(lib.qqa_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def attach_comm(self, uid: bytes, rank: int, nranks: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        check(lib.qqa_attach_comm(self._h, buf, rank, nranks))
+
+    # ------------------------------------------------------------ profiling
+    def profile(self, enable=True):
+        check(lib.qqa_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        ms = ctypes.c_double(0)
+        k = ctypes.c_int64(0)
+        check(lib.qqa_profile_read(self._h, ctypes.byref(ms), ctypes.byref(k)))
+        return float(ms.value), int(k.value)
+
+    def launch_count(self) -> int:
+        k = ctypes.c_int64(0)
+        check(lib.qqa_launch_count(self._h, ctypes.byref(k)))
+        return int(k.value)
+
+    def close(self):
+        if self._h:
+            check(lib.qqa_destroy(self._h))
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
