@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -40,25 +41,32 @@ int fail(int status, const std::string& msg) {
   } while (0)
 
 constexpr size_t kAlign = 256;
+constexpr double kL2BlockBudget = 64.0 * 1024 * 1024;  // bytes of p gathered per replica block
 size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Shape {
   int n = 0;
   int64_t nnz = 0;   // of the graph the kernels walk (complement for max clique)
-  int S_local = 0, S_total = 0, S_p = 0, S_p4 = 0, W = 0, lanes = 0, vpl = 0;
+  int S_local = 0, S_total = 0;
+  int SB = 0, B = 0, S_p = 0;  // replica blocks: S_p = B * SB local columns, layout [B][n+1][SB]
+  int W = 0, lanes = 0, vpl = 0;
+  int64_t nnz_pad = 0;         // row-padded CSR (rows rounded up to 4 entries)
 };
 
 struct Layout {
-  size_t rowptr, colidx, theta, m, v, p0, p1, c0, c1, s0, s1, flag, X, counts, energy, best, beste, xbuf, total;
+  size_t rowptr, colidx, rowptr_pad, colidx_pad, theta, m, v, p0, p1, c0, c1, s0, s1, s2, flag, X, counts, energy,
+      best, beste, xbuf, total;
 };
 
 Layout make_layout(const Shape& s) {
   Layout L{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = up(o + std::max<size_t>(bytes, 1), kAlign); return at; };
-  const size_t ns = (size_t)s.n * s.S_p * sizeof(float);
+  const size_t ns = ((size_t)s.n + 1) * s.S_p * sizeof(float);
   L.rowptr = take(((size_t)s.n + 1) * sizeof(int));
   L.colidx = take((size_t)s.nnz * sizeof(int));
+  L.rowptr_pad = take(((size_t)s.n + 1) * sizeof(int));
+  L.colidx_pad = take((size_t)s.nnz_pad * sizeof(int));
   L.theta = take(ns);
   L.m = take(ns);
   L.v = take(ns);
@@ -68,6 +76,7 @@ Layout make_layout(const Shape& s) {
   L.c1 = take((size_t)s.n * sizeof(float));
   L.s0 = take(2 * (size_t)s.n * sizeof(long long));
   L.s1 = take(2 * (size_t)s.n * sizeof(long long));
+  L.s2 = take(2 * (size_t)s.n * sizeof(long long));
   L.flag = take(4 * sizeof(int));
   L.X = take((size_t)s.n * s.W * sizeof(uint32_t));
   L.counts = take(3 * (size_t)s.S_total * sizeof(long long));
@@ -125,11 +134,35 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   if (s.nnz >= (int64_t)INT32_MAX) return fail(QQA_ERR_UNSUPPORTED, "complement nnz >= 2^31");
   s.S_local = c->S_local;
   s.S_total = c->S_total;
-  s.S_p = (c->S_local + 7) / 8 * 8;
-  s.S_p4 = s.S_p / 4;
+  // Replica blocking: when one copy of p is larger than the L2
+  // budget, split the replicas into blocks of SB (a power of two >= 8) so that
+  // one block of p -- the gathered working set while the grid sweeps it -- fits.
+  const int S8 = (c->S_local + 7) / 8 * 8;
+  const double p_bytes = (double)s.n * S8 * sizeof(float);
+  int SB = S8;
+  const char* env = std::getenv("QQA_BLOCK_REPLICAS");
+  if (env && std::atoi(env) > 0) {
+    SB = std::max(8, next_pow2(std::atoi(env)));
+  } else if (p_bytes > kL2BlockBudget && s.n > 0) {
+    SB = 8;
+    while (SB * 2 < S8 && (double)s.n * (SB * 2) * sizeof(float) <= kL2BlockBudget) SB *= 2;
+  }
+  if (SB >= S8) SB = S8;
+  s.SB = SB;
+  s.B = (S8 + SB - 1) / SB;
+  s.S_p = s.B * SB;
   s.W = (c->S_local + 31) / 32;
-  s.lanes = std::min(32, next_pow2(s.S_p4));
-  s.vpl = next_pow2((s.S_p4 + s.lanes - 1) / s.lanes);
+  const int SB8 = SB / 8;  // 8-replica vectors (one 256-bit access) per item
+  s.lanes = std::min(32, next_pow2(SB8));
+  s.vpl = next_pow2((SB8 + s.lanes - 1) / s.lanes);
+  s.nnz_pad = 0;
+  for (int i = 0; i < s.n; ++i) {
+    const int64_t deg = (c->problem == QQA_MAXCLIQUE) ? (int64_t)(s.n - 1) - (g->rowptr[i + 1] - g->rowptr[i])
+                                                      : g->rowptr[i + 1] - g->rowptr[i];
+    s.nnz_pad += (deg + 3) / 4 * 4;
+  }
+  if (s.nnz_pad >= (int64_t)INT32_MAX) return fail(QQA_ERR_UNSUPPORTED, "padded nnz >= 2^31");
+  if ((int64_t)s.B * ((int64_t)s.n + 1) * s.SB >= (int64_t)1 << 40) return fail(QQA_ERR_UNSUPPORTED, "state too large");
   return QQA_OK;
 }
 
@@ -161,8 +194,10 @@ struct qqa_handle {
   char* ws = nullptr;
   int* rowptr = nullptr;
   int* colidx = nullptr;
+  int* rowptr_pad = nullptr;
+  int* colidx_pad = nullptr;
   float *theta = nullptr, *m = nullptr, *v = nullptr, *p[2] = {nullptr, nullptr}, *c[2] = {nullptr, nullptr};
-  long long* sums[2] = {nullptr, nullptr};
+  long long* sums[3] = {nullptr, nullptr, nullptr};
   int* flag = nullptr;
   uint32_t* X = nullptr;
   unsigned long long* counts = nullptr;
@@ -170,7 +205,8 @@ struct qqa_handle {
   int* best = nullptr;
   double* beste = nullptr;
   uint8_t* xbuf = nullptr;
-  int cur = 0;
+  int cur = 0;   // p / c buffer of the current step (mod 2)
+  int scur = 0;  // sums buffer of the current step (mod 3)
   int64_t step = 0;
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
@@ -195,16 +231,16 @@ bool pick_kernels(int lanes, int vpl, StepKernel& ks, InitKernel& ki) {
     ki = qqa::k_init<L, V>;                              \
     return true;                                         \
   }
-  QQA_CASE(2, 1) QQA_CASE(4, 1) QQA_CASE(8, 1) QQA_CASE(16, 1)
-  QQA_CASE(32, 1) QQA_CASE(32, 2) QQA_CASE(32, 4) QQA_CASE(32, 8)
+  QQA_CASE(1, 1) QQA_CASE(2, 1) QQA_CASE(4, 1) QQA_CASE(8, 1) QQA_CASE(16, 1)
+  QQA_CASE(32, 1) QQA_CASE(32, 2) QQA_CASE(32, 4)
 #undef QQA_CASE
   return false;
 }
 
-int grid_for(const void* kernel, int sm_count, int n, int lanes, int& grid) {
+int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& grid) {
   int per_sm = 0;
   QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
-  const int need = (int)std::max<int64_t>(1, ((int64_t)n * lanes + 255) / 256);
+  const int need = (int)std::max<int64_t>(1, std::min<int64_t>(INT32_MAX, (items * lanes + 255) / 256));
   grid = std::max(1, std::min(need, std::max(1, per_sm) * sm_count));
   return QQA_OK;
 }
@@ -216,7 +252,7 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   qqa::InitParams P{};
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.p0 = h->p[0]; P.p1 = h->p[1];
   P.c = h->c[0]; P.sums = h->sums[0];
-  P.n = h->s.n; P.S_p4 = h->s.S_p4; P.S_local = h->s.S_local; P.S_total = h->s.S_total;
+  P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = h->s.S_total;
   P.replica_offset = h->cfg.replica_offset;
   // base = mix64(seed), computed on the host with the same mixer
   uint64_t z = h->cfg.seed + 0x9E3779B97F4A7C15ull;
@@ -227,6 +263,9 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   P.hi = (double)h->cfg.init_hi;
   P.use_given = use_given ? 1 : 0;
   P.c_given = c_given;
+  QQA_CUDA(cudaMemsetAsync(h->sums[0], 0, 2 * (size_t)h->s.n * sizeof(long long), h->stream));
+  QQA_CUDA(cudaMemsetAsync(h->sums[1], 0, 2 * (size_t)h->s.n * sizeof(long long), h->stream));
+  QQA_CUDA(cudaMemsetAsync(h->sums[2], 0, 2 * (size_t)h->s.n * sizeof(long long), h->stream));
   if (h->s.n > 0) {
     ki<<<h->grid_init, 256, 0, h->stream>>>(P);
     QQA_CUDA(cudaGetLastError());
@@ -236,6 +275,7 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
     QQA_NCCL(ncclAllReduce(h->sums[0], h->sums[0], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
   }
   h->cur = 0;
+  h->scur = 0;
   QQA_CUDA(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
   return QQA_OK;
 }
@@ -248,8 +288,9 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   pick_kernels(h->s.lanes, h->s.vpl, ks, ki);
   const qqa_config& c = h->cfg;
   qqa::StepParams P{};
-  P.rowptr = h->rowptr; P.colidx = h->colidx; P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
-  P.n = h->s.n; P.S_p4 = h->s.S_p4; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
+  P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
+  P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
+  P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
   P.problem = c.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;  // clique = MIS on the complement
   P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
   P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
@@ -262,9 +303,11 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
     P.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
     P.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
     const int a = h->cur, b = h->cur ^ 1;
+    const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
     P.p_cur = h->p[a]; P.p_next = h->p[b];
     P.c_cur = h->c[a]; P.c_next = h->c[b];
-    P.sums_cur = h->sums[a]; P.sums_next = h->sums[b];
+    P.sums_cur = h->sums[sa]; P.sums_next = h->sums[sb];
+    P.sums_zero = (h->s.B > 1) ? h->sums[sz] : nullptr;
     if (h->s.n > 0) {
       if (h->profiling) {
         if (h->ev_used + 2 > h->ev.size()) {
@@ -286,10 +329,30 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
       }
     }
     if (h->comm) {
-      QQA_NCCL(ncclAllReduce(h->sums[b], h->sums[b], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
+      QQA_NCCL(ncclAllReduce(h->sums[sb], h->sums[sb], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
     }
     h->cur = b;
+    h->scur = sb;
     h->step = t;
+  }
+  return QQA_OK;
+}
+
+// Host [n][S_local] <-> device [B][n][SB], one 2-D copy per replica block.
+int copy_blocked(qqa_handle* h, float* host, float* dev, cudaMemcpyKind dir) {
+  const Shape& s = h->s;
+  if (s.n == 0) return QQA_OK;
+  for (int b = 0; b < s.B; ++b) {
+    const int cols = std::min(s.SB, s.S_local - b * s.SB);
+    if (cols <= 0) break;
+    float* hb = host + (size_t)b * s.SB;
+    float* db = dev + (size_t)b * ((size_t)s.n + 1) * s.SB;
+    if (dir == cudaMemcpyDeviceToHost)
+      QQA_CUDA(cudaMemcpy2DAsync(hb, (size_t)s.S_local * sizeof(float), db, (size_t)s.SB * sizeof(float),
+                                 (size_t)cols * sizeof(float), (size_t)s.n, dir, h->stream));
+    else
+      QQA_CUDA(cudaMemcpy2DAsync(db, (size_t)s.SB * sizeof(float), hb, (size_t)s.S_local * sizeof(float),
+                                 (size_t)cols * sizeof(float), (size_t)s.n, dir, h->stream));
   }
   return QQA_OK;
 }
@@ -369,6 +432,8 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   h->ws = ws;
   h->rowptr = (int*)(ws + L.rowptr);
   h->colidx = (int*)(ws + L.colidx);
+  h->rowptr_pad = (int*)(ws + L.rowptr_pad);
+  h->colidx_pad = (int*)(ws + L.colidx_pad);
   h->theta = (float*)(ws + L.theta);
   h->m = (float*)(ws + L.m);
   h->v = (float*)(ws + L.v);
@@ -378,6 +443,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   h->c[1] = (float*)(ws + L.c1);
   h->sums[0] = (long long*)(ws + L.s0);
   h->sums[1] = (long long*)(ws + L.s1);
+  h->sums[2] = (long long*)(ws + L.s2);
   h->flag = (int*)(ws + L.flag);
   h->X = (uint32_t*)(ws + L.X);
   h->counts = (unsigned long long*)(ws + L.counts);
@@ -407,8 +473,9 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     QQA_CUDA_C(cudaMemcpyAsync(h->colidx, ci_src, (size_t)s.nnz * sizeof(int), cudaMemcpyHostToDevice, h->stream));
   QQA_CUDA_C(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
   // theta/m/v padding and both p buffers start at zero / sigmoid(0)
-  for (float* buf : {h->theta, h->m, h->v})
-    QQA_CUDA_C(cudaMemsetAsync(buf, 0, (size_t)s.n * s.S_p * sizeof(float), h->stream));
+  // theta/m/v padding and the zero row n of both p buffers
+  for (float* buf : {h->theta, h->m, h->v, h->p[0], h->p[1]})
+    QQA_CUDA_C(cudaMemsetAsync(buf, 0, ((size_t)s.n + 1) * s.S_p * sizeof(float), h->stream));
   if (cfg->problem != QQA_MAXCLIQUE && s.n > 0 && s.nnz > 0) {
     const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
     qqa::k_validate<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, s.n, h->flag);
@@ -425,6 +492,19 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
       if (flag & 16) why += " not symmetric;";
       return cleanup(fail(QQA_ERR_BAD_GRAPH, "graph rejected:" + why));
     }
+  }
+  {  // row-padded CSR for the step kernel (rows rounded up to 4 entries, sentinel n)
+    std::vector<int> rp_pad((size_t)s.n + 1, 0);
+    for (int i = 0; i < s.n; ++i) rp_pad[i + 1] = rp_pad[i] + (rp32[i + 1] - rp32[i] + 3) / 4 * 4;
+    QQA_CUDA_C(cudaMemcpyAsync(h->rowptr_pad, rp_pad.data(), rp_pad.size() * sizeof(int), cudaMemcpyHostToDevice,
+                               h->stream));
+    if (s.n > 0) {
+      const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
+      qqa::k_pad_csr<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, h->rowptr_pad, h->colidx_pad, s.n);
+      QQA_CUDA_C(cudaGetLastError());
+      h->launches++;
+    }
+    QQA_CUDA_C(cudaStreamSynchronize(h->stream));  // rp_pad is pageable host memory
   }
   StepKernel ks;
   InitKernel ki;
@@ -508,7 +588,7 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
   // K3: round + pack
   if (s.n > 0) {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)s.n * s.W * 32 + 255) / 256, (int64_t)h->sm_count * 16));
-    qqa::k_pack<<<blocks, 256, 0, h->stream>>>(h->theta, h->X, s.n, s.S_p, s.S_local, s.W);
+    qqa::k_pack<<<blocks, 256, 0, h->stream>>>(h->theta, h->X, s.n, s.SB, s.S_local, s.W);
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }
@@ -588,13 +668,10 @@ int qqa_get_state(qqa_handle* h, float* theta, float* m, float* v, float* p, int
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   int st = set_device(h);
   if (st) return st;
-  const Shape& s = h->s;
-  const size_t dp = (size_t)s.S_p * sizeof(float), hp = (size_t)s.S_local * sizeof(float);
   const float* src[4] = {h->theta, h->m, h->v, h->p[h->cur]};
   float* dst[4] = {theta, m, v, p};
   for (int k = 0; k < 4; ++k)
-    if (dst[k] && s.n > 0)
-      QQA_CUDA(cudaMemcpy2DAsync(dst[k], hp, src[k], dp, hp, (size_t)s.n, cudaMemcpyDeviceToHost, h->stream));
+    if (dst[k] && (st = copy_blocked(h, dst[k], const_cast<float*>(src[k]), cudaMemcpyDeviceToHost))) return st;
   QQA_CUDA(cudaStreamSynchronize(h->stream));
   if (step) *step = h->step;
   return QQA_OK;
@@ -607,9 +684,9 @@ int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2) {
   const size_t n = (size_t)h->s.n;
   if (c && n) QQA_CUDA(cudaMemcpyAsync(c, h->c[h->cur], n * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
   if (sumD && n)
-    QQA_CUDA(cudaMemcpyAsync(sumD, h->sums[h->cur], n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    QQA_CUDA(cudaMemcpyAsync(sumD, h->sums[h->scur], n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   if (sumD2 && n)
-    QQA_CUDA(cudaMemcpyAsync(sumD2, h->sums[h->cur] + n, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    QQA_CUDA(cudaMemcpyAsync(sumD2, h->sums[h->scur] + n, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   QQA_CUDA(cudaStreamSynchronize(h->stream));
   return QQA_OK;
 }
@@ -620,14 +697,12 @@ int qqa_set_state(qqa_handle* h, const float* theta, const float* m, const float
   int st = set_device(h);
   if (st) return st;
   const Shape& s = h->s;
-  const size_t dp = (size_t)s.S_p * sizeof(float), hp = (size_t)s.S_local * sizeof(float);
   for (float* buf : {h->theta, h->m, h->v})
-    QQA_CUDA(cudaMemsetAsync(buf, 0, (size_t)s.n * dp, h->stream));
+    QQA_CUDA(cudaMemsetAsync(buf, 0, ((size_t)s.n + 1) * s.S_p * sizeof(float), h->stream));
   const float* src[3] = {theta, m, v};
   float* dst[3] = {h->theta, h->m, h->v};
   for (int k = 0; k < 3; ++k)
-    if (s.n > 0)
-      QQA_CUDA(cudaMemcpy2DAsync(dst[k], dp, src[k], hp, hp, (size_t)s.n, cudaMemcpyHostToDevice, h->stream));
+    if ((st = copy_blocked(h, const_cast<float*>(src[k]), dst[k], cudaMemcpyHostToDevice))) return st;
   const float* cdev = nullptr;
   if (c && s.n > 0) {
     QQA_CUDA(cudaMemcpyAsync(h->c[1], c, (size_t)s.n * sizeof(float), cudaMemcpyHostToDevice, h->stream));

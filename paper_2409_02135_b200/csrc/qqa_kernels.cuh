@@ -1,17 +1,33 @@
 // qqa_kernels.cuh -- sm_100a kernels of the PQQA hot path (see include/qqa.h).
 //
 // Layout in HBM (one GPU holds S_local replicas of all n variables):
-//   theta, m, v, p[2]  float [n][S_p], S_p = S_local rounded up to 8 (one 32-B
-//                      sector); row i of p is read as S_p contiguous floats by
-//                      every neighbour of i -- the SpMM gather (north_star).
+//   theta, m, v, p[2]  float [B][NR][SB]  replica-blocked: the S_p = B*SB local
+//                      replicas are split into B column blocks of SB (a multiple
+//                      of 8 = one 32-byte sector); NR = n + 1 rows per block, row
+//                      n of p is all zeros (target of CSR padding entries).
+//                      Row i of block b is read as SB contiguous floats by every
+//                      neighbour of i -- the SpMM gather of north_star.
 //   c[2]               float [n]       shift of the replica statistics
-//   sums[2]            int64 [2][n]    sum_s D and sum_s D2 (fixed point 2^40)
+//   sums[3]            int64 [2][n]    sum_s D and sum_s D2 (fixed point 2^40)
+//   colidx_pad         int32           CSR with every row padded to a multiple of
+//                                      4 entries with the sentinel n (one int4 load
+//                                      fetches 4 neighbour indices)
 //   X                  uint32 [n][W]   rounded replicas, W = ceil(S_local/32)
+//
+// Work item = (block b, variable i). The step walks b in the outer loop and i
+// in a grid-stride inner loop, so while the grid sweeps block b only that
+// block's p (NR*SB*4 bytes, chosen <= 64 MB) is being gathered and it stays
+// resident in the 126 MB L2.
+//
+// Lane mapping: one lane owns 8 consecutive replicas (one 256-bit access,
+// ld/st.global.v8.f32, new on sm_100); LANES lanes cover an item's SB replicas
+// (VPL 8-vectors per lane when SB > 256).
 //
 // Arithmetic: the fp32 contract of DESIGN.md §3. Every contract operation is
 // written with an explicit round-to-nearest intrinsic (__fadd_rn, __fmul_rn,
 // ...), which nvcc never contracts into FMA, and the file is compiled with
-// -fmad=false as a second guard.
+// -fmad=false as a second guard. Adding a padding entry adds +0.0f to a sum
+// that is never -0.0f (p >= 0, q starts at +0), which leaves it unchanged.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -19,6 +35,10 @@
 namespace qqa {
 
 enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2 };
+
+#ifndef QQA_STEP_MIN_BLOCKS
+#define QQA_STEP_MIN_BLOCKS 4  // 4 x 256 threads per SM when VPL = 1: <= 64 registers per thread
+#endif
 
 // ----------------------------------------------------------- contract math
 __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
@@ -75,109 +95,73 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ float comp(const float4& v, int k) {
-  return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
-}
-__device__ __forceinline__ void set_comp(float4& v, int k, float x) {
-  if (k == 0) v.x = x; else if (k == 1) v.y = x; else if (k == 2) v.z = x; else v.w = x;
-}
+// ------------------------------------------------------ 256-bit accesses
+struct V8 {
+  float f[8];
+};
 
-// L2 cache policies (createpolicy): the theta/m/v streams are read and written
-// once per step -> evict_first, so that the gathered p rows, reused by every
-// neighbour, stay resident (evict_last).
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ float4 ld_stream(const float4* ptr, uint64_t pol) {
-  float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(ptr), "l"(pol));
+__device__ __forceinline__ V8 zero8() {
+  V8 r;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r.f[k] = 0.0f;
   return r;
 }
-__device__ __forceinline__ void st_stream(float4* ptr, const float4& v, uint64_t pol) {
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
-               :: "l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+
+#define QQA_V8_OUT(r) "=f"(r.f[0]), "=f"(r.f[1]), "=f"(r.f[2]), "=f"(r.f[3]), \
+                      "=f"(r.f[4]), "=f"(r.f[5]), "=f"(r.f[6]), "=f"(r.f[7])
+#define QQA_V8_IN(v) "f"(v.f[0]), "f"(v.f[1]), "f"(v.f[2]), "f"(v.f[3]), \
+                     "f"(v.f[4]), "f"(v.f[5]), "f"(v.f[6]), "f"(v.f[7])
+
+// Gathered p rows: read-only during the step, reused by every neighbour -> keep in L2.
+__device__ __forceinline__ V8 ld8_gather(const float* ptr) {
+  V8 r;
+  asm volatile("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : QQA_V8_OUT(r) : "l"(ptr));
+  return r;
 }
-__device__ __forceinline__ float4 ld_gather(const float4* ptr, uint64_t pol) {
-  float4 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(ptr), "l"(pol));
+// theta / m / v: read once and written once per step -> first out of L2, bypass L1.
+__device__ __forceinline__ V8 ld8_stream(const float* ptr) {
+  V8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : QQA_V8_OUT(r) : "l"(ptr));
+  return r;
+}
+__device__ __forceinline__ void st8_stream(float* ptr, const V8& v) {
+  asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "l"(ptr), QQA_V8_IN(v) : "memory");
+}
+// p_next: gathered by the next step -> normal priority.
+__device__ __forceinline__ void st8(float* ptr, const V8& v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" :: "l"(ptr), QQA_V8_IN(v) : "memory");
+}
+__device__ __forceinline__ V8 ld8(const float* ptr) {
+  V8 r;
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : QQA_V8_OUT(r) : "l"(ptr));
   return r;
 }
 
 // ------------------------------------------------------------ parameters
 struct StepParams {
-  const int* __restrict__ rowptr;       // [n+1]
-  const int* __restrict__ colidx;       // [nnz]
-  const float* __restrict__ p_cur;      // [n][S_p]
-  float* __restrict__ p_next;           // [n][S_p]
-  float* __restrict__ theta;            // [n][S_p]
+  const int* __restrict__ rowptr;       // [n+1]   original CSR (degree for Max-Cut)
+  const int* __restrict__ rowptr_pad;   // [n+1]   multiples of 4
+  const int* __restrict__ colidx_pad;   // padded CSR, sentinel n
+  const float* __restrict__ p_cur;      // [B][NR][SB]
+  float* __restrict__ p_next;
+  float* __restrict__ theta;
   float* __restrict__ m;
   float* __restrict__ v;
   const float* __restrict__ c_cur;      // [n]
-  const long long* __restrict__ sums_cur;  // [2][n] (reduced over ranks)
+  const long long* __restrict__ sums_cur;  // [2][n] (reduced over blocks and ranks)
   float* __restrict__ c_next;
-  long long* __restrict__ sums_next;    // [2][n] (this rank's partial)
+  long long* __restrict__ sums_next;    // [2][n] this rank's sums; zero on entry when B > 1
+  long long* __restrict__ sums_zero;    // [2][n] buffer of the step after next (zeroed here), B > 1
   int* __restrict__ flag;               // bit 0: non-finite theta
-  int n, S_p4, S_local;
+  int n, SB, B, S_local;
   double S_total;
   int problem, alpha;
   float lam, comm, b1, c1, b2, c2, eps;
   float kt, at, st, rt;                 // per-step scalars (host double -> float)
 };
-
-// One lane group of LANES lanes owns one variable i at a time; lane l holds the
-// float4 columns l, l+LANES, ... (VPL of them). Gather: the group loads up to
-// LANES neighbour indices with one coalesced load, broadcasts them with
-// shuffles, and issues U neighbour-row loads before consuming them -- the sum
-// itself is sequential in CSR order (contract).
-template <int LANES, int VPL>
-__device__ __forceinline__ void gather_row(const StepParams& P, int i, int lane, unsigned gmask,
-                                           uint64_t pol, float4 (&acc)[VPL]) {
-  constexpr int U = (VPL >= 8) ? 1 : (VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8));
-  const float4* __restrict__ p4 = reinterpret_cast<const float4*>(P.p_cur);
-  const int e0 = __ldg(P.rowptr + i), e1 = __ldg(P.rowptr + i + 1);
-#pragma unroll
-  for (int w = 0; w < VPL; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int eb = e0; eb < e1; eb += LANES) {
-    const int cnt = min(LANES, e1 - eb);
-    const int myj = (lane < cnt) ? __ldg(P.colidx + eb + lane) : 0;
-    for (int k0 = 0; k0 < cnt; k0 += U) {
-      float4 buf[U][VPL];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = __shfl_sync(gmask, myj, (k0 + u) & (LANES - 1), LANES);
-        if (k0 + u < cnt) {
-          const float4* row = p4 + (size_t)j * P.S_p4;
-#pragma unroll
-          for (int w = 0; w < VPL; ++w) {
-            const int col = lane + w * LANES;
-            buf[u][w] = (col < P.S_p4) ? ld_gather(row + col, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (k0 + u < cnt) {
-#pragma unroll
-          for (int w = 0; w < VPL; ++w) {
-            acc[w].x = fadd(acc[w].x, buf[u][w].x);
-            acc[w].y = fadd(acc[w].y, buf[u][w].y);
-            acc[w].z = fadd(acc[w].z, buf[u][w].z);
-            acc[w].w = fadd(acc[w].w, buf[u][w].w);
-          }
-        }
-      }
-    }
-  }
-}
 
 // Gradient (Eq. 6/7/10 + App. D), AdamW and sigmoid for one element.
 __device__ __forceinline__ float update_element(const StepParams& P, float q, float degf, float pi,
@@ -191,7 +175,7 @@ __device__ __forceinline__ float update_element(const StepParams& P, float q, fl
   const float com = (sd >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, mu), sd)) : 0.0f;
   const float gp = fadd(fadd(obj, ent), com);
   const float g = fmul(gp, fmul(pi, fsub(1.0f, pi)));                 // chain rule through sigmoid
-  float t1 = fmul(th, P.at);                                          // decoupled weight decay
+  const float t1 = fmul(th, P.at);                                    // decoupled weight decay
   mm = fadd(fmul(P.b1, mm), fmul(P.c1, g));
   vv = fadd(fmul(P.b2, vv), fmul(fmul(P.c2, g), g));
   const float den = fadd(fmul(__fsqrt_rn(vv), P.rt), P.eps);
@@ -199,69 +183,123 @@ __device__ __forceinline__ float update_element(const StepParams& P, float q, fl
   return sigmoid_c(th);
 }
 
-// K2: the fused step. Per variable i (one lane group): gather q = A p, finalize
-// mu_i / STD_i from the previous step's sums, gradient + AdamW + sigmoid for all
-// local replicas, then this rank's fixed-point sums of p_next (warp shuffles).
+// Reduce the group's fixed-point partial sums and publish them for variable i.
+template <int LANES>
+__device__ __forceinline__ void publish_sums(long long sD, long long sD2, unsigned gmask, int lane, int i, int b,
+                                             int n, int B, float mu, long long* __restrict__ sums,
+                                             float* __restrict__ c_out, long long* __restrict__ zero) {
+#pragma unroll
+  for (int off = LANES / 2; off > 0; off >>= 1) {
+    sD += __shfl_xor_sync(gmask, sD, off, LANES);
+    sD2 += __shfl_xor_sync(gmask, sD2, off, LANES);
+  }
+  if (lane == 0) {
+    if (B == 1) {
+      sums[i] = sD;
+      sums[n + i] = sD2;
+    } else {  // blocks of one variable meet here: exact, order-free integer atomics
+      atomicAdd(reinterpret_cast<unsigned long long*>(sums + i), (unsigned long long)sD);
+      atomicAdd(reinterpret_cast<unsigned long long*>(sums + n + i), (unsigned long long)sD2);
+    }
+    if (b == 0) {
+      c_out[i] = mu;
+      if (zero) { zero[i] = 0; zero[n + i] = 0; }
+    }
+  }
+}
+
+template <int LANES>
+__device__ __forceinline__ unsigned group_mask() {
+  return (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
+}
+
+// K2: the fused step. Per item (b, i): gather q = A p over block b (4 neighbour
+// rows in flight per lane, CSR-order adds), finalize mu_i / STD_i from the
+// previous step's sums, gradient + AdamW + sigmoid for the block's replicas,
+// then the fixed-point sums of p_next (shuffles; atomics across blocks).
 template <int LANES, int VPL>
-__global__ void __launch_bounds__(256) k_step(const StepParams P) {
+__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
   const int lane = threadIdx.x & (LANES - 1);
-  const unsigned gmask = (LANES == 32) ? 0xffffffffu
-                                       : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
-  const int group = (blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-  const int ngroups = (gridDim.x * blockDim.x) / LANES;
-  const float4* __restrict__ pc4 = reinterpret_cast<const float4*>(P.p_cur);
-  float4* __restrict__ pn4 = reinterpret_cast<float4*>(P.p_next);
-  float4* __restrict__ th4 = reinterpret_cast<float4*>(P.theta);
-  float4* __restrict__ m4 = reinterpret_cast<float4*>(P.m);
-  float4* __restrict__ v4 = reinterpret_cast<float4*>(P.v);
-  const uint64_t pol_stream = policy_evict_first();
-  const uint64_t pol_gather = policy_evict_last();
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  const int SB8 = P.SB >> 3;
+  const size_t NR = (size_t)P.n + 1;
   bool bad = false;
 
-  for (int i = group; i < P.n; i += ngroups) {
-    float4 acc[VPL];
-    gather_row<LANES, VPL>(P, i, lane, gmask, pol_gather, acc);
-
-    float mu, sd;
-    finalize_stats(P.c_cur[i], P.sums_cur[i], P.sums_cur[P.n + i], P.S_total, mu, sd);
-    const float degf = (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i));
-
-    long long sD = 0, sD2 = 0;
+  for (int b = 0; b < P.B; ++b) {
+    const size_t blk = (size_t)b * NR * P.SB;     // float offset of block b
+    const float* __restrict__ pc = P.p_cur + blk;
+    for (int i = group; i < P.n; i += ngroups) {
+      // ---- gather q_i over block b
+      V8 acc[VPL];
 #pragma unroll
-    for (int w = 0; w < VPL; ++w) {
-      const int col = lane + w * LANES;
-      if (col >= P.S_p4) continue;
-      const size_t at = (size_t)i * P.S_p4 + col;
-      float4 th = ld_stream(th4 + at, pol_stream);
-      float4 mm = ld_stream(m4 + at, pol_stream);
-      float4 vv = ld_stream(v4 + at, pol_stream);
-      const float4 pp = pc4[at];
-      float4 pn = pp;
+      for (int w = 0; w < VPL; ++w) acc[w] = zero8();
+      const int e0 = __ldg(P.rowptr_pad + i), e1 = __ldg(P.rowptr_pad + i + 1);
+      for (int e = e0; e < e1; e += 4) {
+        const int4 j4 = __ldg(reinterpret_cast<const int4*>(P.colidx_pad + e));
+        const int js[4] = {j4.x, j4.y, j4.z, j4.w};
+        V8 buf[4][VPL];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (col * 4 + k >= P.S_local) continue;   // padding: never updated, no stats
-        float t = comp(th, k), a = comp(mm, k), b = comp(vv, k);
-        const float np = update_element(P, comp(acc[w], k), degf, comp(pp, k), mu, sd, t, a, b);
-        bad |= !isfinite(t);
-        set_comp(th, k, t); set_comp(mm, k, a); set_comp(vv, k, b); set_comp(pn, k, np);
-        long long D, D2;
-        stat_terms(np, mu, D, D2);
-        sD += D; sD2 += D2;
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w = 0; w < VPL; ++w) {
+            const int col8 = lane + w * LANES;
+            buf[u][w] = (VPL * LANES == 1 || col8 < SB8) ? ld8_gather(pc + (size_t)js[u] * P.SB + col8 * 8) : zero8();
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w = 0; w < VPL; ++w)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[w].f[k] = fadd(acc[w].f[k], buf[u][w].f[k]);
       }
-      st_stream(th4 + at, th, pol_stream);
-      st_stream(m4 + at, mm, pol_stream);
-      st_stream(v4 + at, vv, pol_stream);
-      pn4[at] = pn;
-    }
+
+      // ---- replica statistics of the previous step -> mu_i, STD_i
+      float mu, sd;
+      finalize_stats(P.c_cur[i], P.sums_cur[i], P.sums_cur[P.n + i], P.S_total, mu, sd);
+      const float degf = (P.problem == kMAXCUT) ? (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i)) : 0.0f;
+
+      // ---- gradient, AdamW, sigmoid, statistics of p_next
+      long long sD = 0, sD2 = 0;
 #pragma unroll
-    for (int off = LANES / 2; off > 0; off >>= 1) {
-      sD += __shfl_xor_sync(gmask, sD, off, LANES);
-      sD2 += __shfl_xor_sync(gmask, sD2, off, LANES);
-    }
-    if (lane == 0) {
-      P.sums_next[i] = sD;
-      P.sums_next[P.n + i] = sD2;
-      P.c_next[i] = mu;
+      for (int w = 0; w < VPL; ++w) {
+        const int col8 = lane + w * LANES;
+        if (col8 >= SB8) continue;
+        const size_t at = blk + (size_t)i * P.SB + col8 * 8;
+        V8 th = ld8_stream(P.theta + at);
+        V8 mm = ld8_stream(P.m + at);
+        V8 vv = ld8_stream(P.v + at);
+        const V8 pp = ld8(P.p_cur + at);
+        V8 pn = pp;
+        const int s0 = b * P.SB + col8 * 8;          // local replica index of element 0
+        if (s0 + 8 <= P.S_local) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            pn.f[k] = update_element(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k]);
+            bad |= !isfinite(th.f[k]);
+            long long D, D2;
+            stat_terms(pn.f[k], mu, D, D2);
+            sD += D; sD2 += D2;
+          }
+        } else {                                      // ragged last vector: padding is never updated
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (s0 + k < P.S_local) {
+              pn.f[k] = update_element(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k]);
+              bad |= !isfinite(th.f[k]);
+              long long D, D2;
+              stat_terms(pn.f[k], mu, D, D2);
+              sD += D; sD2 += D2;
+            }
+          }
+        }
+        st8_stream(P.theta + at, th);
+        st8_stream(P.m + at, mm);
+        st8_stream(P.v + at, vv);
+        st8(P.p_next + at, pn);
+      }
+      publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, mu, P.sums_next, P.c_next, P.sums_zero);
     }
   }
   if (bad) atomicOr(P.flag, 1);
@@ -269,81 +307,75 @@ __global__ void __launch_bounds__(256) k_step(const StepParams P) {
 
 // ------------------------------------------------------------------- K1
 struct InitParams {
-  float* theta; float* m; float* v; float* p0; float* p1;
-  float* c; long long* sums;            // c[n], sums[2][n]: this rank's partial
-  int n, S_p4, S_local, S_total, replica_offset;
+  float* theta; float* m; float* v; float* p0; float* p1;   // [B][NR][SB]
+  float* c; long long* sums;            // c[n], sums[2][n]: this rank's sums (zero on entry)
+  int n, SB, B, S_local, S_total, replica_offset;
   uint64_t base;                        // mix64(seed)
   double lo, hi;
   int use_given;                        // 1: keep theta/m/v (set_state), recompute p and stats
   const float* c_given;                 // shift per row (NULL -> 1/2)
 };
 
-// theta_0 = lo + (hi - lo) k 2^-24, k = top 24 bits of mix64(mix64(seed) + i S_total + s).
+// theta_0 = lo + (hi - lo) k 2^-24, k = top 24 bits of mix64(mix64(seed) + i S_total + s_global).
 template <int LANES, int VPL>
 __global__ void __launch_bounds__(256) k_init(const InitParams P) {
   const int lane = threadIdx.x & (LANES - 1);
-  const unsigned gmask = (LANES == 32) ? 0xffffffffu
-                                       : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
-  const int group = (blockIdx.x * blockDim.x + threadIdx.x) / LANES;
-  const int ngroups = (gridDim.x * blockDim.x) / LANES;
-  for (int i = group; i < P.n; i += ngroups) {
-    const float ci = P.c_given ? P.c_given[i] : 0.5f;
-    long long sD = 0, sD2 = 0;
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  const int SB8 = P.SB >> 3;
+  const size_t NR = (size_t)P.n + 1;
+  for (int b = 0; b < P.B; ++b) {
+    const size_t blk = (size_t)b * NR * P.SB;
+    for (int i = group; i < P.n; i += ngroups) {
+      const float ci = P.c_given ? P.c_given[i] : 0.5f;
+      long long sD = 0, sD2 = 0;
 #pragma unroll
-    for (int w = 0; w < VPL; ++w) {
-      const int col = lane + w * LANES;
-      if (col >= P.S_p4) continue;
-      const size_t at = (size_t)i * P.S_p4 + col;
-      float4 th, pp;
-      float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-      th = P.use_given ? reinterpret_cast<float4*>(P.theta)[at] : zero;
+      for (int w = 0; w < VPL; ++w) {
+        const int col8 = lane + w * LANES;
+        if (col8 >= SB8) continue;
+        const size_t at = blk + (size_t)i * P.SB + col8 * 8;
+        V8 th = P.use_given ? ld8(P.theta + at) : zero8();
+        V8 pp;
+        const int s0 = b * P.SB + col8 * 8;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int s = col * 4 + k;
-        float t = 0.0f;
-        if (s < P.S_local) {
-          if (P.use_given) {
-            t = comp(th, k);
-          } else {
-            const uint64_t key = P.base + (uint64_t)i * (uint64_t)P.S_total + (uint64_t)(P.replica_offset + s);
-            const uint64_t kk = mix64(key) >> 40;
-            const double x = __dadd_rn(P.lo, __dmul_rn(__dmul_rn(__dsub_rn(P.hi, P.lo), (double)kk), 0x1p-24));
-            t = __double2float_rn(x);
+        for (int k = 0; k < 8; ++k) {
+          const int s = s0 + k;
+          float t = 0.0f;
+          if (s < P.S_local) {
+            if (P.use_given) {
+              t = th.f[k];
+            } else {
+              const uint64_t key = P.base + (uint64_t)i * (uint64_t)P.S_total + (uint64_t)(P.replica_offset + s);
+              const uint64_t kk = mix64(key) >> 40;
+              const double x = __dadd_rn(P.lo, __dmul_rn(__dmul_rn(__dsub_rn(P.hi, P.lo), (double)kk), 0x1p-24));
+              t = __double2float_rn(x);
+            }
+          }
+          th.f[k] = t;
+          pp.f[k] = sigmoid_c(t);
+          if (s < P.S_local) {
+            long long D, D2;
+            stat_terms(pp.f[k], ci, D, D2);
+            sD += D; sD2 += D2;
           }
         }
-        set_comp(th, k, t);
-        const float pv = sigmoid_c(t);
-        set_comp(pp, k, pv);
-        if (s < P.S_local) {
-          long long D, D2;
-          stat_terms(pv, ci, D, D2);
-          sD += D; sD2 += D2;
+        st8(P.theta + at, th);
+        if (!P.use_given) {
+          st8(P.m + at, zero8());
+          st8(P.v + at, zero8());
         }
+        st8(P.p0 + at, pp);
+        st8(P.p1 + at, pp);
       }
-      reinterpret_cast<float4*>(P.theta)[at] = th;
-      if (!P.use_given) {
-        reinterpret_cast<float4*>(P.m)[at] = zero;
-        reinterpret_cast<float4*>(P.v)[at] = zero;
-      }
-      reinterpret_cast<float4*>(P.p0)[at] = pp;
-      reinterpret_cast<float4*>(P.p1)[at] = pp;
-    }
-#pragma unroll
-    for (int off = LANES / 2; off > 0; off >>= 1) {
-      sD += __shfl_xor_sync(gmask, sD, off, LANES);
-      sD2 += __shfl_xor_sync(gmask, sD2, off, LANES);
-    }
-    if (lane == 0) {
-      P.sums[i] = sD;
-      P.sums[P.n + i] = sD2;
-      P.c[i] = ci;
+      publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, ci, P.sums, P.c, nullptr);
     }
   }
 }
 
 // --------------------------------------------------------- graph checks
-// bit 1: column out of range, bit 2: unsorted / duplicate, bit 3: self-loop,
-// bit 4: asymmetric (j's row lacks i).
+// Original CSR: bit 1: column out of range, bit 2: row not strictly ascending
+// (unsorted / duplicate), bit 3: self-loop, bit 4: asymmetric (j's row lacks i).
 __global__ void k_validate(const int* __restrict__ rowptr, const int* __restrict__ colidx, int n,
                            int* __restrict__ flag) {
   int bad = 0;
@@ -367,9 +399,20 @@ __global__ void k_validate(const int* __restrict__ rowptr, const int* __restrict
   if (bad) atomicOr(flag, bad);
 }
 
+// Row-padded copy of the CSR: row i occupies [rowptr_pad[i], rowptr_pad[i+1]),
+// a multiple of 4 entries, the tail filled with the sentinel n (zero row of p).
+__global__ void k_pad_csr(const int* __restrict__ rowptr, const int* __restrict__ colidx,
+                          const int* __restrict__ rowptr_pad, int* __restrict__ colidx_pad, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int e0 = rowptr[i], e1 = rowptr[i + 1], f0 = rowptr_pad[i], f1 = rowptr_pad[i + 1];
+    for (int k = 0; k < f1 - f0; ++k) colidx_pad[f0 + k] = (e0 + k < e1) ? colidx[e0 + k] : n;
+  }
+}
+
 // ---------------------------------------------------------------- K3/K4/K5
-// K3: X[i][w] bit b = (theta[i][32w+b] >= 0) for 32w+b < S_local  (Theta(0)=1)
-__global__ void k_pack(const float* __restrict__ theta, uint32_t* __restrict__ X, int n, int S_p,
+// K3: X[i][w] bit l = (theta of local replica 32w+l >= 0) for 32w+l < S_local
+// (Theta(0)=1); theta is [B][n+1][SB].
+__global__ void k_pack(const float* __restrict__ theta, uint32_t* __restrict__ X, int n, int SB,
                        int S_local, int W) {
   const int lane = threadIdx.x & 31;
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -377,7 +420,11 @@ __global__ void k_pack(const float* __restrict__ theta, uint32_t* __restrict__ X
   for (long long it = warp; it < (long long)n * W; it += nwarps) {
     const int i = (int)(it / W), w = (int)(it % W);
     const int s = w * 32 + lane;
-    const bool x = (s < S_local) && (theta[(size_t)i * S_p + s] >= 0.0f);
+    bool x = false;
+    if (s < S_local) {
+      const int b = s / SB, col = s - b * SB;
+      x = theta[((size_t)b * (n + 1) + i) * SB + col] >= 0.0f;
+    }
     const uint32_t word = __ballot_sync(0xffffffffu, x);
     if (lane == 0) X[it] = word;
   }

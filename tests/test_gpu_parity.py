@@ -291,3 +291,26 @@ def test_profile_counts_launches(Q):
     sol.run_linear(-2.0, 0.1, 100, 0, 25)
     ms, k = sol.profile_read()
     assert k == 25 and ms > 0
+
+
+@pytest.mark.parametrize("SB", [8, 16, 32])
+@pytest.mark.parametrize("problem,S", [("mis", 100), ("maxcut", 64), ("mis", 13), ("maxclique", 40)])
+def test_replica_blocked_layout_parity(Q, monkeypatch, SB, problem, S):
+    """Forced replica blocking ([B][n][SB], atomics across blocks) is bit-identical to the oracle."""
+    monkeypatch.setenv("QQA_BLOCK_REPLICAS", str(SB))
+    g = gen.erdos_renyi(150, 0.5, 31) if problem == "maxclique" else gen.erdos_renyi(900, 0.02, 31)
+    gam = oracle.schedule(-2.0, 0.1, 300)[:50]
+    sol = gpu(Q, g, problem, S, 21, comm=0.3)
+    sol.run(gam)
+    st = oracle.run(g, ocfg(problem, S, 21, comm=0.3), gam)
+    assert_state_equal(sol, st)
+    assert_stats_equal(sol, st)
+    counts, energy, best = oracle.evaluate(g, problem, 2.0, st.theta)
+    res = sol.round_evaluate()
+    assert np.array_equal(np.stack([res.per_replica["size"], res.per_replica["violations"],
+                                    res.per_replica["cut"]], 1), counts)
+    assert res.best_replica == best
+    ck = sol.get_state()
+    sol2 = gpu(Q, g, problem, S, 5, comm=0.3)
+    sol2.set_state(ck["theta"], ck["m"], ck["v"], ck["step"], c=sol.get_stats()["c"])
+    assert np.array_equal(sol2.get_state()["p"], ck["p"])
