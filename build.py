@@ -27,24 +27,25 @@ def nccl_dir() -> str:
     return os.path.dirname(list(nvidia.nccl.__path__)[0] + "/")
 
 
-def build_qqa(force=False, verbose=False) -> str:
+def build_qqa(force=False, verbose=False, out=None, defines=()) -> str:
     srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
     deps = srcs + sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "qqa.h")]
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps):
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    lib = out or LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in deps):
+        return lib
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     nd = nccl_dir()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-fmad=false",                        # fp32 contract: never contract a*b+c
            "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
-           "-o", LIB, *srcs]
+           *[f"-D{d}" for d in defines], "-o", lib, *srcs]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 def build_all(force=False, verbose=False) -> None:
@@ -60,6 +61,14 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", nargs="*", default=None,
+                    help="experiments: build exp/libqqa_<name>.so with -D defines, e.g. u8m3=QQA_GATHER_U=8,QQA_STEP_MIN_BLOCKS=3")
     a = ap.parse_args()
-    build_all(force=a.force, verbose=a.verbose)
-    print("built:", LIB)
+    if a.variant:
+        for v in a.variant:
+            name, _, defs = v.partition("=")
+            print("built:", build_qqa(force=True, verbose=a.verbose, out=os.path.join(ROOT, "exp", f"libqqa_{name}.so"),
+                                      defines=[d for d in defs.split(",") if d]))
+    else:
+        build_all(force=a.force, verbose=a.verbose)
+        print("built:", LIB)

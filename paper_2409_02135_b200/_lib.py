@@ -10,7 +10,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libqqa.so")
+LIB_PATH = os.environ.get("QQA_LIB_PATH") or os.path.join(_HERE, "lib", "libqqa.so")  # override: experiments only
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "qqa.h")
 
 QQA_OK = 0

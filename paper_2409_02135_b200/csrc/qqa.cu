@@ -41,7 +41,7 @@ int fail(int status, const std::string& msg) {
   } while (0)
 
 constexpr size_t kAlign = 256;
-constexpr double kL2BlockBudget = 64.0 * 1024 * 1024;  // bytes of p gathered per replica block
+constexpr double kL2BlockBudget = 256.0 * 1024 * 1024;  // p larger than this is replica-blocked (measured)
 size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Shape {
@@ -54,8 +54,8 @@ struct Shape {
 };
 
 struct Layout {
-  size_t rowptr, colidx, rowptr_pad, colidx_pad, theta, m, v, p0, p1, c0, c1, s0, s1, s2, flag, X, counts, energy,
-      best, beste, xbuf, total;
+  size_t rowptr, colidx, rowptr_pad, colidx_pad, theta, m, v, p0, p1, c0, c1, ms, s0, s1, s2, flag, X, counts,
+      energy, best, beste, xbuf, total;
 };
 
 Layout make_layout(const Shape& s) {
@@ -74,6 +74,7 @@ Layout make_layout(const Shape& s) {
   L.p1 = take(ns);
   L.c0 = take((size_t)s.n * sizeof(float));
   L.c1 = take((size_t)s.n * sizeof(float));
+  L.ms = take((size_t)s.n * sizeof(float2));
   L.s0 = take(2 * (size_t)s.n * sizeof(long long));
   L.s1 = take(2 * (size_t)s.n * sizeof(long long));
   L.s2 = take(2 * (size_t)s.n * sizeof(long long));
@@ -198,6 +199,7 @@ struct qqa_handle {
   int* colidx_pad = nullptr;
   float *theta = nullptr, *m = nullptr, *v = nullptr, *p[2] = {nullptr, nullptr}, *c[2] = {nullptr, nullptr};
   long long* sums[3] = {nullptr, nullptr, nullptr};
+  float2* ms = nullptr;
   int* flag = nullptr;
   uint32_t* X = nullptr;
   unsigned long long* counts = nullptr;
@@ -210,7 +212,7 @@ struct qqa_handle {
   int64_t step = 0;
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
-  int grid_step = 0, grid_init = 0;
+  int grid_step = 0, grid_init = 0, grid_fin = 0;
   bool profiling = false;
   std::vector<cudaEvent_t> ev;  // pairs (start, end)
   size_t ev_used = 0;
@@ -305,10 +307,15 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
     const int a = h->cur, b = h->cur ^ 1;
     const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
     P.p_cur = h->p[a]; P.p_next = h->p[b];
-    P.c_cur = h->c[a]; P.c_next = h->c[b];
-    P.sums_cur = h->sums[sa]; P.sums_next = h->sums[sb];
+    P.ms = h->ms;
+    P.sums_next = h->sums[sb];
     P.sums_zero = (h->s.B > 1) ? h->sums[sz] : nullptr;
     if (h->s.n > 0) {
+      // K0: (mu_i, STD_i) of the current p, shift of the next sums
+      qqa::k_finalize<<<h->grid_fin, 256, 0, h->stream>>>(h->c[a], h->sums[sa], h->s.n, (double)h->s.S_total,
+                                                           h->ms, h->c[b]);
+      QQA_CUDA(cudaGetLastError());
+      h->launches++;
       if (h->profiling) {
         if (h->ev_used + 2 > h->ev.size()) {
           for (int e = 0; e < 256; ++e) {
@@ -444,6 +451,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   h->sums[0] = (long long*)(ws + L.s0);
   h->sums[1] = (long long*)(ws + L.s1);
   h->sums[2] = (long long*)(ws + L.s2);
+  h->ms = (float2*)(ws + L.ms);
   h->flag = (int*)(ws + L.flag);
   h->X = (uint32_t*)(ws + L.X);
   h->counts = (unsigned long long*)(ws + L.counts);
@@ -510,6 +518,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   InitKernel ki;
   if (!pick_kernels(s.lanes, s.vpl, ks, ki)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
   if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
+  h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
   if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
   if ((st = launch_init(h, false, nullptr))) return cleanup(st);
   QQA_CUDA_C(cudaStreamSynchronize(h->stream));
