@@ -192,6 +192,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2409_02135_b200 as Q
+    from paper_2409_02135_b200 import dist as qdist
 
     rank, local_rank, world = dist_env()
     if world != args.gpus:
@@ -200,12 +201,10 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    if w.S % world:
-        raise SystemExit(f"S={w.S} is not divisible by {world} GPUs")
-    S_l = w.S // world
+    offset, S_l = qdist.shard(w.S, world, rank)
     g, seed = w.graphs[0], w.seeds[0]
     hp = {k: v for k, v in w.hparams().items() if k != "problem"}
-    cfg = Q.make_config(w.problem, S_total=w.S, seed=seed, replica_offset=rank * S_l, S_local=S_l, **hp)
+    cfg = Q.make_config(w.problem, S_total=w.S, seed=seed, replica_offset=offset, S_local=S_l, **hp)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -214,17 +213,11 @@ def main():
         torch.cuda.synchronize(dev)
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return qdist.max_over_ranks(x, device=dev)
 
     sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream)
     if world > 1:
-        uid = [Q.Solver.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        sol.attach_comm(uid[0], rank, world)
+        qdist.attach(sol, rank, world)
 
     def solve(s):
         s.reset()
@@ -275,9 +268,7 @@ def main():
         def e2e_step():
             s = Q.Solver(rp, ci, cfg, device=dev, stream=stream, workspace=ws)
             if world > 1:
-                u = [Q.Solver.nccl_unique_id() if rank == 0 else None]
-                dist.broadcast_object_list(u, src=0)
-                s.attach_comm(u[0], rank, world)
+                qdist.attach(s, rank, world)
             s.run_linear(w.gamma_min, w.gamma_max, w.steps)
             r = s.round_evaluate(want_x=True, want_replicas=True)
             s.close()

@@ -1,0 +1,47 @@
+"""Multi-GPU plumbing around the C ABI (host logic only; the exchange itself is
+the library's per-step NCCL all-reduce of the 2n int64 replica-statistic sums).
+
+Replicas are sharded across ranks: rank r holds global replicas
+[r*S/G, (r+1)*S/G) of all variables. torch.distributed is used only to share
+the 128-byte NCCL unique id and for barriers / max-over-ranks timing.
+"""
+from __future__ import annotations
+
+
+def shard(S_total: int, world: int, rank: int) -> tuple[int, int]:
+    """(replica_offset, S_local) of ``rank``; the library requires equal shards."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    if S_total % world:
+        raise ValueError(f"S_total={S_total} is not divisible by {world} ranks")
+    S_local = S_total // world
+    return rank * S_local, S_local
+
+
+def share_unique_id(make_id, rank: int, group=None) -> bytes:
+    """Rank 0 calls ``make_id()`` (e.g. Solver.nccl_unique_id); every rank returns its bytes."""
+    import torch.distributed as dist
+
+    box = [make_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    uid = box[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise RuntimeError("unique id must be 128 bytes")
+    return bytes(uid)
+
+
+def attach(solver, rank: int, world: int, group=None) -> None:
+    """Collective: give ``solver`` its NCCL communicator over ``world`` ranks."""
+    uid = share_unique_id(solver.nccl_unique_id, rank, group)
+    solver.attach_comm(uid, rank, world)
+
+
+def max_over_ranks(x: float, device=None, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
