@@ -44,7 +44,12 @@ class OcCfg(ctypes.Structure):
                 ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
                 ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("init_lo", ctypes.c_float), ("init_hi", ctypes.c_float),
-                ("seed", ctypes.c_uint64), ("S", ctypes.c_int32), ("threads", ctypes.c_int32)]
+                ("seed", ctypes.c_uint64), ("S", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("map", ctypes.c_int32), ("temperature", ctypes.c_float)]
+
+
+MAP_SIGMOID, MAP_CLAMP = 0, 1
+MAPS = {"sigmoid": MAP_SIGMOID, "clamp": MAP_CLAMP}
 
 
 def _L():
@@ -63,6 +68,15 @@ def _L():
         lib.oc_sigmoid_array.argtypes = [ctypes.c_int64, f32, f32]
         lib.oc_exp_neg.restype = ctypes.c_float
         lib.oc_exp_neg.argtypes = [ctypes.c_float]
+        for name in ("oc_clamp01", "oc_ln", "oc_cos2pi"):
+            getattr(lib, name).restype = ctypes.c_float
+            getattr(lib, name).argtypes = [ctypes.c_float]
+        lib.oc_gauss_from_hash.restype = ctypes.c_float
+        lib.oc_gauss_from_hash.argtypes = [ctypes.c_uint64]
+        lib.oc_noise_array.restype = None
+        lib.oc_noise_array.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, f32]
+        lib.oc_noise_scale.restype = ctypes.c_float
+        lib.oc_noise_scale.argtypes = [cfgp]
         lib.oc_step_scalars.restype = None
         lib.oc_step_scalars.argtypes = [cfgp, ctypes.c_int64, ctypes.c_float, f32]
         lib.oc_schedule.restype = None
@@ -80,7 +94,7 @@ def _L():
                                      f32, f32, f32, f32, f32, i64, i64]
         lib.oc_eval.restype = None
         lib.oc_eval.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
-                                f32, i64, f64, ctypes.POINTER(ctypes.c_int32)]
+                                f32, ctypes.c_float, i64, f64, ctypes.POINTER(ctypes.c_int32)]
         lib.oc_complement.restype = ctypes.c_int64
         lib.oc_complement.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_void_p, ctypes.c_void_p]
         _lib = lib
@@ -88,10 +102,19 @@ def _L():
 
 
 def make_cfg(problem="mis", S=16, seed=1, threads=1, alpha=2, penalty=2.0, comm=0.1, lr=1.0,
-             beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, init_lo=-0.01, init_hi=0.01) -> OcCfg:
+             beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, init_lo=-0.01, init_hi=0.01,
+             map="sigmoid", temperature=0.0) -> OcCfg:
     pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
+    mid = MAPS[map] if isinstance(map, str) else int(map)
     return OcCfg(pid, int(alpha), penalty, comm, lr, beta1, beta2, eps, weight_decay,
-                 init_lo, init_hi, seed & 0xFFFFFFFFFFFFFFFF, int(S), int(threads))
+                 init_lo, init_hi, seed & 0xFFFFFFFFFFFFFFFF, int(S), int(threads), mid, float(temperature))
+
+
+def threshold(map="sigmoid") -> float:
+    """Rounding x = Theta(p - 1/2) on the stored parameter: theta >= 0 for
+    the sigmoid map, p >= 1/2 for clamp (where theta holds p)."""
+    mid = MAPS[map] if isinstance(map, str) else int(map)
+    return 0.5 if mid == MAP_CLAMP else 0.0
 
 
 @dataclasses.dataclass
@@ -121,6 +144,33 @@ def sigmoid(theta) -> np.ndarray:
 
 def exp_neg(a: float) -> float:
     return float(_L().oc_exp_neg(float(a)))
+
+
+def clamp01(w: float) -> float:
+    return float(_L().oc_clamp01(float(w)))
+
+
+def ln(u: float) -> float:
+    return float(_L().oc_ln(float(u)))
+
+
+def cos2pi(x: float) -> float:
+    return float(_L().oc_cos2pi(float(x)))
+
+
+def gauss_from_hash(h: int) -> float:
+    return float(_L().oc_gauss_from_hash(ctypes.c_uint64(h & 0xFFFFFFFFFFFFFFFF)))
+
+
+def noise(seed: int, t: int, n: int, S: int) -> np.ndarray:
+    """xi [n][S] of Adam step t (the contract's counter-based Box-Muller)."""
+    out = np.empty((n, S), np.float32)
+    _L().oc_noise_array(ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), t, n, S, out)
+    return out
+
+
+def noise_scale(cfg: OcCfg) -> float:
+    return float(_L().oc_noise_scale(ctypes.byref(cfg)))
 
 
 def schedule(gmin: float, gmax: float, T: int) -> np.ndarray:
@@ -197,8 +247,9 @@ def step_rows(g, cfg: OcCfg, gamma: float, t: int, p, c, sumD, sumD2, theta_rows
     return out
 
 
-def evaluate(g, problem, penalty: float, theta: np.ndarray, csr=None):
-    """Round (theta >= 0), count, energies, best replica. Returns (counts[S][3], energy[S], best)."""
+def evaluate(g, problem, penalty: float, theta: np.ndarray, csr=None, map="sigmoid"):
+    """Round (theta >= thr, see threshold()), count, energies, best replica.
+    Returns (counts[S][3], energy[S], best)."""
     pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
     if csr is None:
         csr = complement(g) if pid == MAXCLIQUE else (g.rowptr, g.colidx)
@@ -209,5 +260,5 @@ def evaluate(g, problem, penalty: float, theta: np.ndarray, csr=None):
     energy = np.zeros(S, np.float64)
     best = ctypes.c_int32(0)
     _L().oc_eval(g.n, np.ascontiguousarray(rp, np.int64), np.ascontiguousarray(ci, np.int32),
-                 pid, penalty, S, th, counts, energy, ctypes.byref(best))
+                 pid, penalty, S, th, threshold(map), counts, energy, ctypes.byref(best))
     return counts, energy, int(best.value)

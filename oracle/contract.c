@@ -20,6 +20,12 @@
  *   dR/dtheta = dR/dp * p (1 - p)
  *   AdamW, decoupled weight decay
  *   x = Theta(p - 1/2) evaluated as theta >= 0
+ *   map = CLAMP (sensitive transition, NEXT-1): AdamW on p itself with
+ *     dR/dp (no chain factor), then p = Clamp(p') into [0, 1]         Eq. 11
+ *     x = Theta(p - 1/2) evaluated as p >= 1/2
+ *   Langevin noise (NEXT-2): + sqrt(2 lr T) xi after the optimizer
+ *     step, before the map; xi ~ N(0,1) by Box-Muller from a counter
+ *     hash keyed (seed, t, i, s)                                     Eq. 9/11
  *   energies from integer counts
  *
  * THE fp32 CONTRACT: every element follows one fixed sequence
@@ -51,7 +57,11 @@ typedef struct {
     uint64_t seed;
     int32_t S;           /* replicas (the oracle always holds all of them) */
     int32_t threads;     /* OpenMP threads for the row loop (<=1: serial) */
+    int32_t map;         /* 0 sigmoid (theta is the parameter), 1 clamp (p is the parameter) */
+    float temperature;   /* Langevin T; 0 = no noise */
 } oc_cfg;
+
+enum { OC_MAP_SIGMOID = 0, OC_MAP_CLAMP = 1 };
 
 /* ------------------------------------------------------------ sigmoid ---- */
 /* E = exp(-a) for 0 <= a <= 87, in fp32: a = k ln2 + r, exp(r) by Taylor. */
@@ -83,6 +93,69 @@ float oc_sigmoid(float theta) {
 
 void oc_sigmoid_array(int64_t n, const float* in, float* out) {
     for (int64_t k = 0; k < n; ++k) out[k] = oc_sigmoid(in[k]);
+}
+
+/* Clamp(w) into [0, 1]; NaN and -0 map to +0 (NaN is flagged before). */
+float oc_clamp01(float w) {
+    return (w > 0.0f) ? ((w < 1.0f) ? w : 1.0f) : 0.0f;
+}
+
+/* ------------------------------------------------------ Gaussian noise ---- */
+/* ln(u), u in (0, 1], fp32: u = 2^e m, m in [sqrt(1/2), sqrt(2)), f = m - 1
+ * (exact), s = f/(2+f), ln m = 2 atanh(s) = 2 s (1 + s^2/3 + s^4/5 + s^6/7 + s^8/9),
+ * ln u = (e ln2_hi + ln m) + e ln2_lo. */
+float oc_ln(float u) {
+    union { float f; uint32_t u; } b;
+    b.f = u;
+    int e = (int)((b.u >> 23) & 0xffu) - 127;
+    b.u = (b.u & 0x007fffffu) | 0x3f800000u;                   /* m in [1, 2) */
+    float m = b.f;
+    if (m > 1.41421356f) { m = m * 0.5f; e = e + 1; }
+    const float f = m - 1.0f;
+    const float s = f / (2.0f + f);
+    const float z = s * s;
+    float P = 1.0f / 9.0f;
+    P = P * z + 1.0f / 7.0f;
+    P = P * z + 1.0f / 5.0f;
+    P = P * z + 1.0f / 3.0f;
+    P = P * z + 1.0f;
+    const float lnm = 2.0f * (s * P);
+    const float ef = (float)e;
+    return (ef * 0.693145751953125f + lnm) + ef * 1.428606765330187e-6f;
+}
+
+/* cos(2 pi x), x in [0, 1): y = 4x (exact), k = rint(y), r = y - k in [-1/2, 1/2]
+ * (exact), a = r pi/2 in [-pi/4, pi/4]; cos(k pi/2 + a) from the Taylor
+ * polynomials of cos a (to a^8) and sin a (to a^9) by quadrant k mod 4. */
+float oc_cos2pi(float x) {
+    const float y = 4.0f * x;
+    const float k = rintf(y);
+    const float r = y - k;
+    const float a = r * 1.57079632679489662f;
+    const float a2 = a * a;
+    float C = 1.0f / 40320.0f;
+    C = C * a2 - 1.0f / 720.0f;
+    C = C * a2 + 1.0f / 24.0f;
+    C = C * a2 - 0.5f;
+    C = C * a2 + 1.0f;
+    float Sn = 1.0f / 362880.0f;
+    Sn = Sn * a2 - 1.0f / 5040.0f;
+    Sn = Sn * a2 + 1.0f / 120.0f;
+    Sn = Sn * a2 - 1.0f / 6.0f;
+    Sn = Sn * a2 + 1.0f;
+    Sn = Sn * a;
+    const int q = ((int)k) & 3;
+    return (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
+}
+
+/* xi ~ N(0, 1) from one 64-bit hash h by Box-Muller:
+ * u1 = (top 24 bits + 1) 2^-24 in (0, 1], u2 = (bits 16..39) 2^-24 in [0, 1),
+ * xi = sqrt(-2 ln u1) cos(2 pi u2). */
+float oc_gauss_from_hash(uint64_t h) {
+    const float u1 = (float)((h >> 40) + 1u) * 0x1p-24f;
+    const float u2 = (float)((h >> 16) & 0xFFFFFFu) * 0x1p-24f;
+    const float r = sqrtf(-2.0f * oc_ln(u1));
+    return r * oc_cos2pi(u2);
 }
 
 /* ------------------------------------------------------ step scalars ---- */
@@ -134,8 +207,30 @@ static uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+/* Noise of (Adam step t, variable i, global replica s):
+ * xi = gauss(mix64(mix64(seed ^ 0x6A09E667F3BCC909) + (t n + i) S_total + s)). */
+uint64_t oc_noise_base(uint64_t seed) { return mix64(seed ^ 0x6A09E667F3BCC909ULL); }
+
+float oc_noise(uint64_t base, int64_t t, int32_t n, int32_t i, int32_t S_total, int32_t s) {
+    const uint64_t key = base + ((uint64_t)t * (uint64_t)n + (uint64_t)i) * (uint64_t)S_total + (uint64_t)s;
+    return oc_gauss_from_hash(mix64(key));
+}
+
+void oc_noise_array(uint64_t seed, int64_t t, int32_t n, int32_t S, float* out) {
+    const uint64_t base = oc_noise_base(seed);
+    for (int32_t i = 0; i < n; ++i)
+        for (int32_t s = 0; s < S; ++s) out[(size_t)i * S + s] = oc_noise(base, t, n, i, S, s);
+}
+
+/* sqrt(2 lr T), the Langevin noise scale (Eq. 9, eta = lr), host double -> fp32 */
+float oc_noise_scale(const oc_cfg* c) {
+    return (float)sqrt(2.0 * (double)c->lr * (double)c->temperature);
+}
+
 /* theta_0 ~ U(lo, hi) by a counter hash keyed (seed, i, s); m = v = 0; p = sigmoid(theta);
- * c = 1/2; sums of p with shift 1/2. Arrays are [n][S] row-major. */
+ * c = 1/2; sums of p with shift 1/2. Arrays are [n][S] row-major.
+ * map = CLAMP: the parameter is p itself, p_0 = 1/2 + U(lo, hi) (the same hash,
+ * the sum formed in double and rounded once); theta holds p. */
 void oc_init(int32_t n, const oc_cfg* cf, float* theta, float* m, float* v, float* p,
              float* c, int64_t* sumD, int64_t* sumD2) {
     const int32_t S = cf->S;
@@ -146,10 +241,15 @@ void oc_init(int32_t n, const oc_cfg* cf, float* theta, float* m, float* v, floa
             const uint64_t key = base + (uint64_t)i * (uint64_t)S + (uint64_t)s;
             const uint64_t k = mix64(key) >> 40;
             const size_t at = (size_t)i * S + s;
-            theta[at] = (float)(lo + (hi - lo) * (double)k * 0x1p-24);
+            if (cf->map == OC_MAP_CLAMP) {
+                theta[at] = (float)(0.5 + (lo + (hi - lo) * (double)k * 0x1p-24));
+                p[at] = theta[at];
+            } else {
+                theta[at] = (float)(lo + (hi - lo) * (double)k * 0x1p-24);
+                p[at] = oc_sigmoid(theta[at]);
+            }
             m[at] = 0.0f;
             v[at] = 0.0f;
-            p[at] = oc_sigmoid(theta[at]);
         }
         c[i] = 0.5f;
         row_sums(p + (size_t)i * S, S, 0.5f, &sumD[i], &sumD2[i]);
@@ -160,8 +260,8 @@ void oc_init(int32_t n, const oc_cfg* cf, float* theta, float* m, float* v, floa
 /* Update row i. Reads p (old values, all rows) and the row's stats (c_i, sums);
  * updates th/mm/vv (row i, length S) in place; writes p_new (row i) and the
  * row's new stats (shift = this step's mean). */
-static void update_row(int32_t i, const int64_t* rowptr, const int32_t* colidx, const oc_cfg* cf,
-                       const float* sc, const float* p, float* th, float* mm, float* vv,
+static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, const int32_t* colidx,
+                       const oc_cfg* cf, const float* sc, const float* p, float* th, float* mm, float* vv,
                        float c_i, int64_t sD_i, int64_t sD2_i,
                        float* p_new, float* c_new, int64_t* sD_new, int64_t* sD2_new, float* q) {
     const int32_t S = cf->S;
@@ -169,9 +269,13 @@ static void update_row(int32_t i, const int64_t* rowptr, const int32_t* colidx, 
     const float b1 = cf->beta1, b2 = cf->beta2, eps = cf->eps;
     const float c1 = (float)(1.0 - (double)cf->beta1), c2 = (float)(1.0 - (double)cf->beta2);
     const float lam = cf->penalty, ac = cf->comm;
+    const int clamp = cf->map == OC_MAP_CLAMP;
+    const float ns = oc_noise_scale(cf);
+    const uint64_t nbase = oc_noise_base(cf->seed);
     const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
     const float degf = (float)(e1 - e0);
     const float* pown = p + (size_t)i * S;
+    int nonfinite_flag = 0;
 
     float mu, sd;
     finalize_stats(c_i, sD_i, sD2_i, S, &mu, &sd);
@@ -193,23 +297,28 @@ static void update_row(int32_t i, const int64_t* rowptr, const int32_t* colidx, 
         const float obj = (cf->problem == OC_MAXCUT) ? (2.0f * q[s] - degf) : (lam * q[s] - 1.0f);
         const float com = (sd >= 1e-6f) ? (-ac) * ((pi - mu) / sd) : 0.0f;
         const float gp = (obj + ent) + com;
-        const float g = gp * (pi * (1.0f - pi));
+        /* sigmoid: chain rule dR/dtheta = dR/dp p (1-p); clamp: the parameter is p */
+        const float g = clamp ? gp : gp * (pi * (1.0f - pi));
         /* AdamW */
         float t1 = th[s] * at;
         const float m1 = b1 * mm[s] + c1 * g;
         const float v1 = b2 * vv[s] + (c2 * g) * g;
         const float den = sqrtf(v1) * rt + eps;
         t1 = t1 - st * (m1 / den);
+        if (cf->temperature > 0.0f)                       /* Langevin noise, Eq. 9 / 11 */
+            t1 = t1 + ns * oc_noise(nbase, t, n, i, S, s);
+        if (!isfinite(t1)) nonfinite_flag = 1;            /* SPEC.md:396 abort, before the map */
+        if (clamp) {
+            t1 = oc_clamp01(t1);                          /* p^{t+1} = Clamp(p'), Eq. 11 */
+            p_new[s] = t1;
+        } else {
+            p_new[s] = oc_sigmoid(t1);
+        }
         th[s] = t1; mm[s] = m1; vv[s] = v1;
-        p_new[s] = oc_sigmoid(t1);
     }
     *c_new = mu;
     row_sums(p_new, S, mu, sD_new, sD2_new);
-}
-
-static int nonfinite_row(const float* x, int32_t S) {
-    for (int32_t s = 0; s < S; ++s) if (!isfinite(x[s])) return 1;
-    return 0;
+    return nonfinite_flag;
 }
 
 /* Run n_steps annealing steps. gamma[k] is gamma for step k; Adam index t = t0 + k + 1.
@@ -229,15 +338,16 @@ int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg
         float sc[4];
         oc_step_scalars(cf, t0 + k + 1, gamma[k], sc);
         const int thr = cf->threads > 1 ? cf->threads : 1;
+        const int64_t t = t0 + k + 1;
         (void)thr;
-#pragma omp parallel num_threads(thr)
+#pragma omp parallel num_threads(thr) reduction(| : bad)
         {
             float* q = (float*)malloc(sizeof(float) * (S ? S : 1));
 #pragma omp for schedule(static)
             for (int32_t i = 0; i < n; ++i) {
                 const size_t r = (size_t)i * S;
-                update_row(i, rowptr, colidx, cf, sc, p, theta + r, m + r, v + r,
-                           c[i], sumD[i], sumD2[i], p2 + r, &c2[i], &d2a[i], &d2b[i], q);
+                bad |= update_row(i, n, t, rowptr, colidx, cf, sc, p, theta + r, m + r, v + r,
+                                  c[i], sumD[i], sumD2[i], p2 + r, &c2[i], &d2a[i], &d2b[i], q);
             }
             free(q);
         }
@@ -245,7 +355,6 @@ int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg
         memcpy(c, c2, sizeof(float) * n);
         memcpy(sumD, d2a, sizeof(int64_t) * n);
         memcpy(sumD2, d2b, sizeof(int64_t) * n);
-        for (int32_t i = 0; i < n && !bad; ++i) bad = nonfinite_row(theta + (size_t)i * S, S);
     }
     free(p2); free(c2); free(d2a); free(d2b);
     return bad ? 5 : 0;
@@ -262,7 +371,6 @@ void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const
                   float* theta_out, float* m_out, float* v_out, float* p_out,
                   float* c_out, int64_t* sD_out, int64_t* sD2_out) {
     const int32_t S = cf->S;
-    (void)n;
     float sc[4];
     oc_step_scalars(cf, t, gamma_t, sc);
     float* q = (float*)malloc(sizeof(float) * (S ? S : 1));
@@ -272,28 +380,29 @@ void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const
         memcpy(theta_out + r, theta_rows + r, sizeof(float) * S);
         memcpy(m_out + r, m_rows + r, sizeof(float) * S);
         memcpy(v_out + r, v_rows + r, sizeof(float) * S);
-        update_row(i, rowptr, colidx, cf, sc, p, theta_out + r, m_out + r, v_out + r,
+        (void)update_row(i, n, t, rowptr, colidx, cf, sc, p, theta_out + r, m_out + r, v_out + r,
                    c[i], sumD[i], sumD2[i], p_out + r, &c_out[k], &sD_out[k], &sD2_out[k], q);
     }
     free(q);
 }
 
 /* ------------------------------------------------------- evaluation ---- */
-/* x = [theta >= 0]; counts[s][3] = (size, violations, cut) with each
+/* x = [theta >= thr] (thr = 0 for the sigmoid map, 1/2 for clamp where theta
+ * holds p); counts[s][3] = (size, violations, cut) with each
  * undirected edge counted once (j > i); energy[s] = -size + lam*viol
  * (MIS / clique on the complement) or -cut (Max-Cut); *best = argmin energy,
  * lowest index on ties. */
 void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t problem, float lam,
-             int32_t S, const float* theta, int64_t* counts, double* energy, int32_t* best) {
+             int32_t S, const float* theta, float thr, int64_t* counts, double* energy, int32_t* best) {
     memset(counts, 0, sizeof(int64_t) * 3 * (size_t)S);
     for (int32_t i = 0; i < n; ++i) {
         for (int32_t s = 0; s < S; ++s) {
-            const int xi = theta[(size_t)i * S + s] >= 0.0f;
+            const int xi = theta[(size_t)i * S + s] >= thr;
             counts[3 * s + 0] += xi;
             for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
                 const int32_t j = colidx[e];
                 if (j <= i) continue;
-                const int xj = theta[(size_t)j * S + s] >= 0.0f;
+                const int xj = theta[(size_t)j * S + s] >= thr;
                 counts[3 * s + 1] += xi & xj;
                 counts[3 * s + 2] += xi ^ xj;
             }

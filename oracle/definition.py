@@ -13,6 +13,8 @@ Plain fp64 numpy, written equation by equation from PAPER.md (cited as P:<line>)
   * QQA objective r = l(p) + gamma s(p)                                       (Eq. 6)
   * ensemble objective R = sum_s r_s - S alpha_c sum_i STD_i, population STD  (Eq. 10)
   * p = sigmoid(theta)                                                        (BASELINE.json north_star)
+  * or the sensitive transition with Clamp: AdamW on p, p <- Clamp(p')        (Eq. 11)
+  * Langevin noise + sqrt(2 eta T) xi, eta = lr, after the optimizer step     (Eq. 9 / 11)
   * AdamW (decoupled weight decay)
   * gamma linear from gamma_min to gamma_max over the steps
   * rounding x = Theta(p - 1/2)  (evaluated as theta >= 0, Theta(0) = 1)
@@ -205,22 +207,68 @@ def init_theta(n: int, S_total: int, seed: int, lo: float = -0.01, hi: float = 0
     return lo64 + (hi64 - lo64) * k * 2.0 ** -24
 
 
+def init_p_clamp(n: int, S_total: int, seed: int, lo: float = -0.01, hi: float = 0.01) -> np.ndarray:
+    """Clamp map (NEXT-1): the parameter is p itself, p_0 = 1/2 + U(lo, hi) from the same
+    counter hash as init_theta (reading R23: the paper's init for Clamp is not printed)."""
+    return 0.5 + init_theta(n, S_total, seed, lo, hi)
+
+
+def clamp01(w):
+    """Clamp(w) into [0, 1] (P:248)."""
+    return np.clip(w, 0.0, 1.0)
+
+
+# ------------------------------------------------------------ Langevin noise
+NOISE_SALT = 0x6A09E667F3BCC909
+
+
+def gauss_noise(seed: int, t: int, n: int, S_total: int) -> np.ndarray:
+    """xi ~ N(0, 1) [n][S_total] for Adam step t by Box-Muller in fp64 from a counter hash:
+    h = splitmix64(splitmix64(seed ^ salt) + (t n + i) S_total + s);
+    u1 = (h >> 40 + 1) 2^-24 in (0, 1]; u2 = ((h >> 16) & (2^24 - 1)) 2^-24 in [0, 1);
+    xi = sqrt(-2 ln u1) cos(2 pi u2)."""
+    base = _splitmix64(np.array([(seed ^ NOISE_SALT) & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64))[0]
+    i = np.arange(n, dtype=np.uint64)[:, None]
+    s = np.arange(S_total, dtype=np.uint64)[None, :]
+    with np.errstate(over="ignore"):
+        key = base + (np.uint64(t) * np.uint64(n) + i) * np.uint64(S_total) + s
+    h = _splitmix64(key)
+    u1 = ((h >> np.uint64(40)) + np.uint64(1)).astype(np.float64) * 2.0 ** -24
+    u2 = ((h >> np.uint64(16)) & np.uint64(0xFFFFFF)).astype(np.float64) * 2.0 ** -24
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+
+
 # --------------------------------------------------------------- the loop
 def run(problem, A, theta0, gammas, alpha=2, lam=2.0, comm=0.1, lr=1.0, beta1=0.9,
-        beta2=0.999, eps=1e-8, wd=0.01, m0=None, v0=None, t0=0):
-    """PQQA with AdamW on theta, fp64. Returns (theta, m, v)."""
+        beta2=0.999, eps=1e-8, wd=0.01, m0=None, v0=None, t0=0, map="sigmoid", temperature=0.0, seed=0):
+    """PQQA with AdamW (P:220-222), fp64. Returns (theta, m, v).
+
+    map="sigmoid": theta is the parameter, p = sigmoid(theta), gradient by the chain rule.
+    map="clamp" (sensitive transition, Eq. 11): ``theta0`` is p_0; AdamW is applied to p with
+    dR/dp, then p <- Clamp(p'); the returned "theta" is p.
+    temperature > 0: + sqrt(2 lr T) xi after the optimizer step, before the map (Eq. 9 / 11)."""
     theta = np.array(theta0, dtype=np.float64)
     m = np.zeros_like(theta) if m0 is None else np.array(m0, dtype=np.float64)
     v = np.zeros_like(theta) if v0 is None else np.array(v0, dtype=np.float64)
+    n, S = theta.shape
     for k, gamma in enumerate(gammas):
-        g = grad_theta(problem, A, theta, float(gamma), alpha, lam, comm)
-        theta, m, v = adamw_step(theta, m, v, g, t0 + k + 1, lr, beta1, beta2, eps, wd)
+        t = t0 + k + 1
+        if map == "clamp":
+            g = grad_p(problem, A, theta, float(gamma), alpha, lam, comm)
+        else:
+            g = grad_theta(problem, A, theta, float(gamma), alpha, lam, comm)
+        theta, m, v = adamw_step(theta, m, v, g, t, lr, beta1, beta2, eps, wd)
+        if temperature > 0.0:
+            theta = theta + np.sqrt(2.0 * lr * temperature) * gauss_noise(seed, t, n, S)
+        if map == "clamp":
+            theta = clamp01(theta)
     return theta, m, v
 
 
-def round_x(theta: np.ndarray) -> np.ndarray:
-    """x = Theta(sigmoid(theta) - 1/2) with Theta(0)=1, i.e. theta >= 0 (reading R12)."""
-    return (theta >= 0).astype(np.int64)
+def round_x(theta: np.ndarray, map="sigmoid") -> np.ndarray:
+    """x = Theta(p - 1/2) with Theta(0)=1 (reading R12): theta >= 0 for the sigmoid
+    map, p >= 1/2 for clamp (theta holds p)."""
+    return (theta >= (0.5 if map == "clamp" else 0.0)).astype(np.int64)
 
 
 def counts(problem, A: np.ndarray, X: np.ndarray) -> np.ndarray:
