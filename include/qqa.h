@@ -12,8 +12,14 @@
  *            Max-Cut:                        dl/dp = -deg + 2 q
  *            ds/dp = -2 alpha (2p - 1)^(alpha - 1)                     (Eq. 7)
  *   theta  <- AdamW(theta, dR/dp * p (1 - p))
+ *            (+ sqrt(2 lr T) xi when temperature T > 0)        Eq. 9
  *   gamma  linear from gamma_min to gamma_max
  *   x      = Theta(p - 1/2)  (theta >= 0, Theta(0) = 1)
+ *
+ * With map = QQA_MAP_CLAMP (the paper's experimental setting, "sensitive
+ * transitions", Eq. 11) the parameter is p itself:
+ *   p' = AdamW(p, dR/dp) (+ sqrt(2 lr T) xi);  p = Clamp(p') into [0, 1];
+ *   x = Theta(p - 1/2) evaluated as p >= 1/2; p_0 = 1/2 + U(init_lo, init_hi).
  *   energy = -size + lambda * violations  |  -cut
  *   best   = argmin energy (lowest global replica on ties)
  *
@@ -44,7 +50,7 @@
 extern "C" {
 #endif
 
-#define QQA_ABI_VERSION 1
+#define QQA_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define QQA_API __attribute__((visibility("default")))
@@ -62,6 +68,11 @@ typedef enum {
   QQA_ERR_UNSUPPORTED = 6,   /* valid input outside what this build implements         */
   QQA_ERR_WORKSPACE = 7      /* workspace null, misaligned or too small                */
 } qqa_status;
+
+typedef enum {
+  QQA_MAP_SIGMOID = 0,  /* p = sigmoid(theta), AdamW on theta (north_star)              */
+  QQA_MAP_CLAMP = 1     /* AdamW on p, then Clamp into [0, 1] (Eq. 11)        */
+} qqa_map;
 
 typedef enum {
   QQA_MIS = 0,        /* maximum independent set, l = -1^T x + lambda x^T A x / 2       */
@@ -83,6 +94,10 @@ typedef struct {
   int32_t S_total;        /* replicas over all ranks (S of Eq. 10), 1..2^20                */
   int32_t replica_offset; /* first global replica held here                                */
   int32_t S_local;        /* replicas held here, 1..1024                                   */
+  int32_t map;            /* qqa_map                                                        */
+  float temperature;      /* Langevin T >= 0 (0.001); 0 = no noise. xi ~ N(0,1) is a
+                             counter-based Box-Muller draw keyed (seed, Adam step, variable,
+                             global replica): identical for every sharding               */
 } qqa_config;
 
 /* Undirected simple graph as symmetric CSR, host memory, copied at create.

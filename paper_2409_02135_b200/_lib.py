@@ -17,6 +17,7 @@ QQA_OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "BAD_GRAPH", 3: "CUDA", 4: "COMM", 5: "NONFINITE",
           6: "UNSUPPORTED", 7: "WORKSPACE"}
 PROBLEMS = {"mis": 0, "maxcut": 1, "maxclique": 2}
+MAPS = {"sigmoid": 0, "clamp": 1}
 
 
 class QQAError(RuntimeError):
@@ -32,7 +33,8 @@ class Config(ctypes.Structure):
                 ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("init_lo", ctypes.c_float), ("init_hi", ctypes.c_float),
                 ("seed", ctypes.c_uint64),
-                ("S_total", ctypes.c_int32), ("replica_offset", ctypes.c_int32), ("S_local", ctypes.c_int32)]
+                ("S_total", ctypes.c_int32), ("replica_offset", ctypes.c_int32), ("S_local", ctypes.c_int32),
+                ("map", ctypes.c_int32), ("temperature", ctypes.c_float)]
 
 
 class Graph(ctypes.Structure):

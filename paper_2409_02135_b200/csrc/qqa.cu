@@ -104,6 +104,10 @@ int check_config(const qqa_config* c) {
       !(c->beta1 >= 0.0f && c->beta1 < 1.0f) || !(c->beta2 >= 0.0f && c->beta2 < 1.0f) || !(c->eps >= 0.0f) ||
       !std::isfinite(c->weight_decay) || !std::isfinite(c->init_lo) || !std::isfinite(c->init_hi))
     return fail(QQA_ERR_INVALID_ARG, "hyper-parameter out of range (lr, penalty, comm>=0, 0<=beta<1, eps>=0 ...)");
+  if (c->map != QQA_MAP_SIGMOID && c->map != QQA_MAP_CLAMP)
+    return fail(QQA_ERR_INVALID_ARG, "map must be 0 (sigmoid) or 1 (clamp)");
+  if (!(c->temperature >= 0.0f) || !std::isfinite(c->temperature))
+    return fail(QQA_ERR_INVALID_ARG, "temperature must be finite and >= 0");
   return QQA_OK;
 }
 
@@ -226,10 +230,26 @@ namespace {
 using StepKernel = void (*)(const qqa::StepParams);
 using InitKernel = void (*)(const qqa::InitParams);
 
-bool pick_kernels(int lanes, int vpl, StepKernel& ks, InitKernel& ki) {
+// Step-kernel mode: bit 0 clamp map, bit 1 Langevin noise (template, so the
+// default sigmoid / no-noise kernel carries none of the optional code).
+int step_mode(const qqa_config& c) {
+  return (c.map == QQA_MAP_CLAMP ? qqa::kModeClamp : 0) | (c.temperature > 0.0f ? qqa::kModeNoise : 0);
+}
+
+template <int L, int V>
+StepKernel step_for_mode(int mode) {
+  switch (mode) {
+    case 0: return qqa::k_step<L, V, 0>;
+    case 1: return qqa::k_step<L, V, 1>;
+    case 2: return qqa::k_step<L, V, 2>;
+    default: return qqa::k_step<L, V, 3>;
+  }
+}
+
+bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki) {
 #define QQA_CASE(L, V)                                   \
   if (lanes == L && vpl == V) {                          \
-    ks = qqa::k_step<L, V>;                              \
+    ks = step_for_mode<L, V>(mode);                      \
     ki = qqa::k_init<L, V>;                              \
     return true;                                         \
   }
@@ -237,6 +257,13 @@ bool pick_kernels(int lanes, int vpl, StepKernel& ks, InitKernel& ki) {
   QQA_CASE(32, 1) QQA_CASE(32, 2) QQA_CASE(32, 4)
 #undef QQA_CASE
   return false;
+}
+
+uint64_t mix64_host(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
 }
 
 int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& grid) {
@@ -250,17 +277,14 @@ int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& gr
 int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   StepKernel ks;
   InitKernel ki;
-  pick_kernels(h->s.lanes, h->s.vpl, ks, ki);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki);
   qqa::InitParams P{};
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.p0 = h->p[0]; P.p1 = h->p[1];
   P.c = h->c[0]; P.sums = h->sums[0];
   P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = h->s.S_total;
   P.replica_offset = h->cfg.replica_offset;
-  // base = mix64(seed), computed on the host with the same mixer
-  uint64_t z = h->cfg.seed + 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  P.base = z ^ (z >> 31);
+  P.base = mix64_host(h->cfg.seed);  // base = mix64(seed), computed on the host with the same mixer
+  P.clamp = h->cfg.map == QQA_MAP_CLAMP ? 1 : 0;
   P.lo = (double)h->cfg.init_lo;
   P.hi = (double)h->cfg.init_hi;
   P.use_given = use_given ? 1 : 0;
@@ -287,7 +311,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (n_steps > 0 && !gamma) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
   StepKernel ks;
   InitKernel ki;
-  pick_kernels(h->s.lanes, h->s.vpl, ks, ki);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki);
   const qqa_config& c = h->cfg;
   qqa::StepParams P{};
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
@@ -298,8 +322,13 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
   P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
   P.eps = c.eps;
+  P.ns = (float)std::sqrt(2.0 * (double)c.lr * (double)c.temperature);   // Eq. 9: sqrt(2 eta T)
+  P.S_total_u = (unsigned long long)h->s.S_total;
+  const uint64_t nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);    // noise stream
   for (int64_t k = 0; k < n_steps; ++k) {
     const int64_t t = h->step + 1;  // Adam step index (reading R11)
+    // xi key of (t, i, global s) = nbase + (t n + i) S_total + s  (mod 2^64)
+    P.nkey = nbase + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total + (uint64_t)c.replica_offset;
     P.kt = (float)(-2.0 * (double)c.alpha * (double)gamma[k]);
     P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
     P.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
@@ -516,7 +545,8 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   }
   StepKernel ks;
   InitKernel ki;
-  if (!pick_kernels(s.lanes, s.vpl, ks, ki)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
+  if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki))
+    return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
   if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
   h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
   if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
@@ -597,7 +627,8 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
   // K3: round + pack
   if (s.n > 0) {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)s.n * s.W * 32 + 255) / 256, (int64_t)h->sm_count * 16));
-    qqa::k_pack<<<blocks, 256, 0, h->stream>>>(h->theta, h->X, s.n, s.SB, s.S_local, s.W);
+    const float thr = (h->cfg.map == QQA_MAP_CLAMP) ? 0.5f : 0.0f;   // x = Theta(p - 1/2)
+    qqa::k_pack<<<blocks, 256, 0, h->stream>>>(h->theta, h->X, s.n, s.SB, s.S_local, s.W, thr);
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }

@@ -35,6 +35,9 @@
 namespace qqa {
 
 enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2 };
+// Step-kernel mode (template): bit 0 = clamp map (Eq. 11),
+// bit 1 = Langevin noise (Eq. 9 / 11).
+enum : int { kModeClamp = 1, kModeNoise = 2 };
 
 #ifndef QQA_GATHER_U
 #define QQA_GATHER_U 4         // neighbour rows in flight per lane (multiple of 4)
@@ -75,6 +78,52 @@ __device__ __forceinline__ float sigmoid_c(float th) {
   return (th >= 0.0f) ? fdiv(1.0f, den) : fdiv(E, den);
 }
 
+// Clamp(w) into [0, 1]; NaN and -0 map to +0 (non-finite is flagged first).
+__device__ __forceinline__ float clamp01(float w) { return (w > 0.0f) ? ((w < 1.0f) ? w : 1.0f) : 0.0f; }
+
+// ln(u), u in (0, 1]: u = 2^e m, m in [sqrt(1/2), sqrt(2)), f = m - 1 (exact),
+// s = f/(2+f), ln m = 2 s (1 + s^2/3 + s^4/5 + s^6/7 + s^8/9), ln u = (e ln2_hi + ln m) + e ln2_lo.
+__device__ __forceinline__ float ln_c(float u) {
+  const uint32_t b = __float_as_uint(u);
+  int e = (int)((b >> 23) & 0xffu) - 127;
+  float m = __uint_as_float((b & 0x007fffffu) | 0x3f800000u);
+  if (m > 1.41421356f) { m = fmul(m, 0.5f); e = e + 1; }
+  const float f = fsub(m, 1.0f);
+  const float sv = fdiv(f, fadd(2.0f, f));
+  const float z = fmul(sv, sv);
+  float P = 1.0f / 9.0f;
+  P = fadd(fmul(P, z), 1.0f / 7.0f);
+  P = fadd(fmul(P, z), 1.0f / 5.0f);
+  P = fadd(fmul(P, z), 1.0f / 3.0f);
+  P = fadd(fmul(P, z), 1.0f);
+  const float lnm = fmul(2.0f, fmul(sv, P));
+  const float ef = (float)e;
+  return fadd(fadd(fmul(ef, 0.693145751953125f), lnm), fmul(ef, 1.428606765330187e-6f));
+}
+
+// cos(2 pi x), x in [0, 1): quadrant k = rint(4x), a = (4x - k) pi/2 in [-pi/4, pi/4],
+// Taylor cos a (to a^8) / sin a (to a^9).
+__device__ __forceinline__ float cos2pi_c(float x) {
+  const float y = fmul(4.0f, x);
+  const float k = rintf(y);
+  const float r = fsub(y, k);
+  const float a = fmul(r, 1.57079632679489662f);
+  const float a2 = fmul(a, a);
+  float C = 1.0f / 40320.0f;
+  C = fsub(fmul(C, a2), 1.0f / 720.0f);
+  C = fadd(fmul(C, a2), 1.0f / 24.0f);
+  C = fsub(fmul(C, a2), 0.5f);
+  C = fadd(fmul(C, a2), 1.0f);
+  float Sn = 1.0f / 362880.0f;
+  Sn = fsub(fmul(Sn, a2), 1.0f / 5040.0f);
+  Sn = fadd(fmul(Sn, a2), 1.0f / 120.0f);
+  Sn = fsub(fmul(Sn, a2), 1.0f / 6.0f);
+  Sn = fadd(fmul(Sn, a2), 1.0f);
+  Sn = fmul(Sn, a);
+  const int q = ((int)k) & 3;
+  return (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
+}
+
 // Replica mean / population STD of one variable from its fixed-point sums.
 __device__ __forceinline__ void finalize_stats(float c, long long sD, long long sD2, double S,
                                                float& mu, float& sd) {
@@ -97,6 +146,15 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
+}
+
+// xi ~ N(0,1) from one hash by Box-Muller: u1 = (h>>40 + 1) 2^-24 in (0,1],
+// u2 = ((h>>16) & 0xFFFFFF) 2^-24 in [0,1), xi = sqrt(-2 ln u1) cos(2 pi u2).
+__device__ __forceinline__ float gauss_c(uint64_t h) {
+  const float u1 = fmul(__ull2float_rn((h >> 40) + 1ull), 0x1p-24f);
+  const float u2 = fmul(__ull2float_rn((h >> 16) & 0xFFFFFFull), 0x1p-24f);
+  const float r = __fsqrt_rn(fmul(-2.0f, ln_c(u1)));
+  return fmul(r, cos2pi_c(u2));
 }
 
 // ------------------------------------------------------ 256-bit accesses
@@ -163,11 +221,19 @@ struct StepParams {
   int problem, alpha;
   float lam, comm, b1, c1, b2, c2, eps;
   float kt, at, st, rt;                 // per-step scalars (host double -> float)
+  float ns;                             // Langevin scale sqrt(2 lr T) (host double -> float)
+  unsigned long long nkey;              // noise key of (t, row 0, replica_offset): nbase + t n S_total + offset
+  unsigned long long S_total_u;         // key stride per row
 };
 
-// Gradient (Eq. 6/7/10 + App. D), AdamW and sigmoid for one element.
+// Gradient (Eq. 6/7/10 + App. D), AdamW, optional Langevin noise and
+// the map for one element. MODE bit 0: clamp (the parameter th is p itself, no
+// chain factor, p = Clamp(th)); otherwise p = sigmoid(th). Returns p_next; bad
+// is set when the pre-map parameter is non-finite.
+template <int MODE>
 __device__ __forceinline__ float update_element(const StepParams& P, float q, float degf, float pi,
-                                                float mu, float sd, float& th, float& mm, float& vv) {
+                                                float mu, float sd, float& th, float& mm, float& vv,
+                                                unsigned long long key, bool& bad) {
   const float e = fsub(fmul(2.0f, pi), 1.0f);
   float ep = e;
   for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);                 // (2p-1)^(alpha-1)
@@ -176,13 +242,21 @@ __device__ __forceinline__ float update_element(const StepParams& P, float q, fl
                                            : fsub(fmul(P.lam, q), 1.0f); // -1 + lambda q
   const float com = (sd >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, mu), sd)) : 0.0f;
   const float gp = fadd(fadd(obj, ent), com);
-  const float g = fmul(gp, fmul(pi, fsub(1.0f, pi)));                 // chain rule through sigmoid
+  const float g = (MODE & kModeClamp) ? gp                             // sensitive transition: d/dp
+                                      : fmul(gp, fmul(pi, fsub(1.0f, pi)));  // chain rule through sigmoid
   const float t1 = fmul(th, P.at);                                    // decoupled weight decay
   mm = fadd(fmul(P.b1, mm), fmul(P.c1, g));
   vv = fadd(fmul(P.b2, vv), fmul(fmul(P.c2, g), g));
   const float den = fadd(fmul(__fsqrt_rn(vv), P.rt), P.eps);
-  th = fsub(t1, fmul(P.st, fdiv(mm, den)));
-  return sigmoid_c(th);
+  float w = fsub(t1, fmul(P.st, fdiv(mm, den)));
+  if (MODE & kModeNoise) w = fadd(w, fmul(P.ns, gauss_c(mix64(key))));   // + sqrt(2 lr T) xi
+  bad |= !isfinite(w);
+  if (MODE & kModeClamp) {
+    th = clamp01(w);
+    return th;
+  }
+  th = w;
+  return sigmoid_c(w);
 }
 
 // Reduce the group's fixed-point partial sums and publish them for variable i.
@@ -230,7 +304,7 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
 // which equals 0 + row exactly since p >= +0), gradient + AdamW + sigmoid for
 // the block's replicas with (mu_i, STD_i) from k_finalize, then the fixed-point
 // sums of p_next (shuffles; atomics across blocks).
-template <int LANES, int VPL>
+template <int LANES, int VPL, int MODE>
 __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
   const int lane = threadIdx.x & (LANES - 1);
   const unsigned gmask = group_mask<LANES>();
@@ -290,8 +364,9 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
       const float mu = msi.x, sd = msi.y;
       const float degf = (P.problem == kMAXCUT) ? (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i)) : 0.0f;
 
-      // ---- gradient, AdamW, sigmoid, statistics of p_next
+      // ---- gradient, AdamW, (noise), map, statistics of p_next
       long long sD = 0, sD2 = 0;
+      const unsigned long long rkey = P.nkey + (unsigned long long)i * P.S_total_u;  // noise key of (t, i, offset)
 #pragma unroll
       for (int w = 0; w < VPL; ++w) {
         const int col8 = lane + w * LANES;
@@ -306,8 +381,8 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
         if (s0 + 8 <= P.S_local) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            pn.f[k] = update_element(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k]);
-            bad |= !isfinite(th.f[k]);
+            pn.f[k] = update_element<MODE>(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
+                                           rkey + (unsigned long long)(s0 + k), bad);
             long long D, D2;
             stat_terms(pn.f[k], mu, D, D2);
             sD += D; sD2 += D2;
@@ -316,8 +391,8 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (s0 + k < P.S_local) {
-              pn.f[k] = update_element(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k]);
-              bad |= !isfinite(th.f[k]);
+              pn.f[k] = update_element<MODE>(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
+                                             rkey + (unsigned long long)(s0 + k), bad);
               long long D, D2;
               stat_terms(pn.f[k], mu, D, D2);
               sD += D; sD2 += D2;
@@ -344,9 +419,11 @@ struct InitParams {
   double lo, hi;
   int use_given;                        // 1: keep theta/m/v (set_state), recompute p and stats
   const float* c_given;                 // shift per row (NULL -> 1/2)
+  int clamp;                            // map = clamp: the parameter is p, p_0 = 1/2 + U(lo, hi), p = theta
 };
 
-// theta_0 = lo + (hi - lo) k 2^-24, k = top 24 bits of mix64(mix64(seed) + i S_total + s_global).
+// theta_0 = lo + (hi - lo) k 2^-24, k = top 24 bits of mix64(mix64(seed) + i S_total + s_global);
+// clamp map: p_0 = theta_0 = 1/2 + (lo + (hi - lo) k 2^-24), the sum in double, rounded once.
 template <int LANES, int VPL>
 __global__ void __launch_bounds__(256) k_init(const InitParams P) {
   const int lane = threadIdx.x & (LANES - 1);
@@ -379,11 +456,11 @@ __global__ void __launch_bounds__(256) k_init(const InitParams P) {
               const uint64_t key = P.base + (uint64_t)i * (uint64_t)P.S_total + (uint64_t)(P.replica_offset + s);
               const uint64_t kk = mix64(key) >> 40;
               const double x = __dadd_rn(P.lo, __dmul_rn(__dmul_rn(__dsub_rn(P.hi, P.lo), (double)kk), 0x1p-24));
-              t = __double2float_rn(x);
+              t = __double2float_rn(P.clamp ? __dadd_rn(0.5, x) : x);
             }
           }
           th.f[k] = t;
-          pp.f[k] = sigmoid_c(t);
+          pp.f[k] = P.clamp ? t : sigmoid_c(t);
           if (s < P.S_local) {
             long long D, D2;
             stat_terms(pp.f[k], ci, D, D2);
@@ -441,10 +518,11 @@ __global__ void k_pad_csr(const int* __restrict__ rowptr, const int* __restrict_
 }
 
 // ---------------------------------------------------------------- K3/K4/K5
-// K3: X[i][w] bit l = (theta of local replica 32w+l >= 0) for 32w+l < S_local
-// (Theta(0)=1); theta is [B][n+1][SB].
+// K3: X[i][w] bit l = (theta of local replica 32w+l >= thr) for 32w+l < S_local
+// (Theta(0)=1; thr = 0 for the sigmoid map, 1/2 for clamp where theta
+// holds p); theta is [B][n+1][SB].
 __global__ void k_pack(const float* __restrict__ theta, uint32_t* __restrict__ X, int n, int SB,
-                       int S_local, int W) {
+                       int S_local, int W, float thr) {
   const int lane = threadIdx.x & 31;
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -454,7 +532,7 @@ __global__ void k_pack(const float* __restrict__ theta, uint32_t* __restrict__ X
     bool x = false;
     if (s < S_local) {
       const int b = s / SB, col = s - b * SB;
-      x = theta[((size_t)b * (n + 1) + i) * SB + col] >= 0.0f;
+      x = theta[((size_t)b * (n + 1) + i) * SB + col] >= thr;
     }
     const uint32_t word = __ballot_sync(0xffffffffu, x);
     if (lane == 0) X[it] = word;
