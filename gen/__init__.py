@@ -138,6 +138,25 @@ def random_bipartite(a: int, b: int, p: float, seed: int) -> Graph:
     return from_edges(a + b, u.astype(np.int32), (v + a).astype(np.int32))
 
 
+def disjoint_union(graphs) -> tuple[Graph, np.ndarray]:
+    """Block-diagonal union of instances (the paper's batch of instances {C_mu}):
+    instance k's rows are the contiguous range after instances 0..k-1. Returns the union
+    graph and group_of_row (int32 [n], instance of each row)."""
+    n = sum(g.n for g in graphs)
+    rowptr = np.zeros(n + 1, np.int64)
+    cols, groups = [], []
+    r0, e0 = 0, 0
+    for k, g in enumerate(graphs):
+        rowptr[r0 + 1:r0 + g.n + 1] = e0 + g.rowptr[1:]
+        cols.append(g.colidx.astype(np.int64) + r0)
+        groups.append(np.full(g.n, k, np.int32))
+        r0 += g.n
+        e0 += g.nnz
+    colidx = np.concatenate(cols).astype(np.int32) if cols else np.zeros(0, np.int32)
+    gor = np.concatenate(groups) if groups else np.zeros(0, np.int32)
+    return Graph(n, rowptr, colidx), gor
+
+
 # ------------------------------------------------------------------ configs
 PROBLEMS = {"mis": 0, "maxcut": 1, "maxclique": 2}
 

@@ -95,6 +95,9 @@ def _L():
         lib.oc_eval.restype = None
         lib.oc_eval.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
                                 f32, ctypes.c_float, i64, f64, ctypes.POINTER(ctypes.c_int32)]
+        lib.oc_eval_groups.restype = None
+        lib.oc_eval_groups.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
+                                       f32, ctypes.c_float, i32, ctypes.c_int32, i64, f64, i32]
         lib.oc_complement.restype = ctypes.c_int64
         lib.oc_complement.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_void_p, ctypes.c_void_p]
         _lib = lib
@@ -262,3 +265,47 @@ def evaluate(g, problem, penalty: float, theta: np.ndarray, csr=None, map="sigmo
     _L().oc_eval(g.n, np.ascontiguousarray(rp, np.int64), np.ascontiguousarray(ci, np.int32),
                  pid, penalty, S, th, threshold(map), counts, energy, ctypes.byref(best))
     return counts, energy, int(best.value)
+
+
+def evaluate_groups(g, problem, penalty: float, theta: np.ndarray, group_of_row, n_groups: int, map="sigmoid"):
+    """Per-instance evaluation of a block-diagonal batch (NEXT-3).
+    Returns (counts[G][S][3], energy[G][S], best[G])."""
+    pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
+    rp, ci = complement_groups(g, group_of_row) if pid == MAXCLIQUE else (g.rowptr, g.colidx)
+    th = np.ascontiguousarray(theta, np.float32)
+    S = th.shape[1]
+    counts = np.zeros((n_groups, S, 3), np.int64)
+    energy = np.zeros((n_groups, S), np.float64)
+    best = np.zeros(n_groups, np.int32)
+    _L().oc_eval_groups(g.n, np.ascontiguousarray(rp, np.int64), np.ascontiguousarray(ci, np.int32),
+                        pid, penalty, S, th, threshold(map), np.ascontiguousarray(group_of_row, np.int32),
+                        int(n_groups), counts, energy, best)
+    return counts, energy, best
+
+
+def instance_rows(group_of_row) -> list[tuple[int, int]]:
+    """Row range [a, b) of every instance (instances are contiguous, group_of_row non-decreasing)."""
+    gor = np.asarray(group_of_row)
+    G = int(gor.max()) + 1 if gor.size else 0
+    starts = np.searchsorted(gor, np.arange(G + 1))
+    return [(int(starts[k]), int(starts[k + 1])) for k in range(G)]
+
+
+def subgraph(g, a: int, b: int):
+    """Induced subgraph on rows [a, b) of a block-diagonal graph (no edge leaves the block)."""
+    rp = (g.rowptr[a:b + 1] - g.rowptr[a]).astype(np.int64)
+    ci = (g.colidx[g.rowptr[a]:g.rowptr[b]].astype(np.int64) - a).astype(np.int32)
+    return type(g)(b - a, rp, ci)
+
+
+def complement_groups(g, group_of_row):
+    """Max clique on a batch = MIS on the block-diagonal union of per-instance complements."""
+    rps, cis, r0, e0 = [np.zeros(1, np.int64)], [], 0, 0
+    for a, b in instance_rows(group_of_row):
+        rp, ci = complement(subgraph(g, a, b))
+        rps.append(rp[1:] + e0)
+        cis.append(ci.astype(np.int64) + a)
+        e0 += int(rp[-1])
+    rp = np.concatenate(rps)
+    ci = np.concatenate(cis).astype(np.int32) if cis else np.zeros(0, np.int32)
+    return rp, ci

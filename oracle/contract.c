@@ -417,6 +417,41 @@ void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t pr
     *best = b;
 }
 
+/* Multi-instance batch (NEXT-3): rows carry their instance in
+ * group_of_row[n] (0..G-1); counts[g][s][3] over the rows of group g and the
+ * edges (i < j) leaving them; energy[g][s] as in oc_eval; best[g] = argmin over s
+ * of energy[g][s], lowest index on ties. */
+void oc_eval_groups(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t problem, float lam,
+                    int32_t S, const float* theta, float thr, const int32_t* group_of_row, int32_t G,
+                    int64_t* counts, double* energy, int32_t* best) {
+    memset(counts, 0, sizeof(int64_t) * 3 * (size_t)S * (size_t)G);
+    for (int32_t i = 0; i < n; ++i) {
+        int64_t* cg = counts + (size_t)group_of_row[i] * 3 * (size_t)S;
+        for (int32_t s = 0; s < S; ++s) {
+            const int xi = theta[(size_t)i * S + s] >= thr;
+            cg[3 * s + 0] += xi;
+            for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                const int32_t j = colidx[e];
+                if (j <= i) continue;
+                const int xj = theta[(size_t)j * S + s] >= thr;
+                cg[3 * s + 1] += xi & xj;
+                cg[3 * s + 2] += xi ^ xj;
+            }
+        }
+    }
+    for (int32_t g = 0; g < G; ++g) {
+        const int64_t* cg = counts + (size_t)g * 3 * (size_t)S;
+        double* eg = energy + (size_t)g * S;
+        int32_t b = 0;
+        for (int32_t s = 0; s < S; ++s) {
+            eg[s] = (problem == OC_MAXCUT) ? -(double)cg[3 * s + 2]
+                                           : -(double)cg[3 * s + 0] + (double)lam * (double)cg[3 * s + 1];
+            if (eg[s] < eg[b]) b = s;
+        }
+        best[g] = b;
+    }
+}
+
 /* -------------------------------------------------------- complement --- */
 /* Complement of a simple graph (for max clique = MIS on the complement).
  * Pass colidx_out = NULL to get the nnz only. Returns nnz of the complement. */
