@@ -117,7 +117,7 @@ def cpu_info():
 def oracle_sample(w, n_steps: int, threads: int):
     """Time the fp32 contract oracle (as it stands) for n_steps annealing steps of w."""
     import oracle
-    g, seed = w.graphs[0], w.seeds[0]
+    (g, _), seed = w.batched(), w.seeds[0]
     hp = {k: v for k, v in w.hparams().items() if k != "problem"}
     cfg = oracle.make_cfg(w.problem, S=w.S, seed=seed, threads=threads, **hp)
     gam = oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:n_steps]
@@ -141,7 +141,7 @@ def run_reference(args, w):
         _, dt = oracle_sample(w, n_sample, cores)
         times.append(dt)
     t = sum(times)
-    g = w.graphs[0]
+    g, _ = w.batched()
     value = g.n * w.S * n_sample * args.steps / t
     sample = (f"{n_sample} of {w.steps} annealing steps of {w.name} per bench step at full size "
               f"(N={g.n}, nnz={g.nnz}, S={w.S}); oracle/contract.c, OpenMP over rows")
@@ -156,12 +156,14 @@ def run_reference(args, w):
 
 
 def workload_config(w, world):
-    g = w.graphs[0]
+    g, _ = w.batched()
     S_l = w.S // world
     state_bytes = 5 * g.n * ((S_l + 7) // 8 * 8) * 4
     return {"workload": w.name, "problem": w.problem, "recipe": w.recipe, "N": g.n, "nnz": g.nnz, "S": w.S,
             "S_local": S_l, "anneal_steps": w.steps, "instances": len(w.graphs),
-            "parallelism": f"replica-sharded x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"replica-sharded x{world}" if world > 1 else "single GPU")
+                           + (f", {len(w.graphs)} instances batched block-diagonally in one handle"
+                              if len(w.graphs) > 1 else ""),
             "l2": f"inputs larger than L2: {state_bytes / 1e9:.2f} GB of replica state per GPU"
                   if state_bytes > 132e6 else "state fits L2 (no flush)"}
 
@@ -181,7 +183,7 @@ def main():
     args = ap.parse_args()
 
     import gen
-    w = gen.workload(args.workload, n_instances=1 if args.workload == "c2" else None)
+    w = gen.workload(args.workload)
     if args.anneal_steps:
         w.steps = args.anneal_steps
     if args.impl == "reference":
@@ -202,7 +204,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     offset, S_l = qdist.shard(w.S, world, rank)
-    g, seed = w.graphs[0], w.seeds[0]
+    (g, gor), seed = w.batched(), w.seeds[0]
     hp = {k: v for k, v in w.hparams().items() if k != "problem"}
     cfg = Q.make_config(w.problem, S_total=w.S, seed=seed, replica_offset=offset, S_local=S_l, **hp)
     stream = torch.cuda.current_stream(dev)
@@ -215,14 +217,19 @@ def main():
     def max_over_ranks(x: float) -> float:
         return qdist.max_over_ranks(x, device=dev)
 
-    sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream)
+    sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
     if world > 1:
         qdist.attach(sol, rank, world)
+
+    def evaluate(s):
+        if gor is not None:   # batch: every instance's best replica (NEXT-3)
+            return s.round_evaluate_groups(want_x=True, want_counts=False)
+        return s.round_evaluate(want_x=True, want_replicas=False)
 
     def solve(s):
         s.reset()
         s.run_linear(w.gamma_min, w.gamma_max, w.steps)
-        return s.round_evaluate(want_x=True, want_replicas=False)
+        return evaluate(s)
 
     for _ in range(args.warmup):
         solve(sol)
@@ -265,12 +272,15 @@ def main():
         sol.close()
         del sol
 
+        gp = None if gor is None else torch.from_numpy(gor).pin_memory().numpy()
+
         def e2e_step():
-            s = Q.Solver(rp, ci, cfg, device=dev, stream=stream, workspace=ws)
+            s = Q.Solver(rp, ci, cfg, device=dev, stream=stream, workspace=ws, group_of_row=gp)
             if world > 1:
                 qdist.attach(s, rank, world)
             s.run_linear(w.gamma_min, w.gamma_max, w.steps)
-            r = s.round_evaluate(want_x=True, want_replicas=True)
+            r = (s.round_evaluate_groups(want_x=True, want_counts=True) if gp is not None
+                 else s.round_evaluate(want_x=True, want_replicas=True))
             s.close()
             return r
 
@@ -284,8 +294,9 @@ def main():
         barrier()
         te = max_over_ranks(e0.elapsed_time(e1))
         e2e = {"value": total_updates / (te / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(g.rowptr.nbytes + g.colidx.nbytes),
-               "d2h_bytes_per_step": int(S_l * 48 + g.n + 4 + 8 + 4),
+               "h2d_bytes_per_step": int(g.rowptr.nbytes + g.colidx.nbytes + (0 if gor is None else gor.nbytes)),
+               "d2h_bytes_per_step": int(S_l * 48 + g.n + 4 + 8 + 4) if gor is None
+                                     else int(len(w.graphs) * (S_l * 32 + 12) + g.n + 4),
                "ms_per_step": te / args.steps,
                "path": "qqa_create (pinned host CSR -> HBM) + qqa_run_linear + qqa_round_evaluate (results -> host)"}
 
@@ -309,7 +320,8 @@ def main():
                              "launches_timed": kern_launches, "peak_source": peak_src,
                              "step_kernel_share": kern_ms / t_ms},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": l1 - l0, "clocks": clocks,
-                "result": {"best_replica": res.best_replica, "best_energy": res.best_energy}}
+                "result": ({"best_replica": res.best_replica, "best_energy": res.best_energy} if gor is None else
+                           {"instances": len(w.graphs), "best_energy_per_instance": [float(x) for x in res.best_energy]})}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

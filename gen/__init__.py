@@ -184,6 +184,13 @@ class Workload:
     init_hi: float = 0.01
     recipe: str = ""
 
+    def batched(self):
+        """(graph, group_of_row): the block-diagonal union of the instances (one handle anneals
+        them together, NEXT-3), or (the graph, None) for a single instance."""
+        if len(self.graphs) == 1:
+            return self.graphs[0], None
+        return disjoint_union(self.graphs)
+
     def hparams(self) -> dict:
         return dict(problem=self.problem, alpha=self.alpha, penalty=self.penalty, comm=self.comm,
                     lr=self.lr, beta1=self.beta1, beta2=self.beta2, eps=self.eps,

@@ -102,12 +102,23 @@ typedef struct {
 
 /* Undirected simple graph as symmetric CSR, host memory, copied at create.
  * rowptr[n+1] (rowptr[0] = 0, non-decreasing, rowptr[n] = nnz), colidx[nnz]
- * strictly ascending within each row, no self-loops, (i,j) present iff (j,i). */
+ * strictly ascending within each row, no self-loops, (i,j) present iff (j,i).
+ *
+ * Batch of instances (NEXT-3; "batch parallel computation for multiple
+ * ... instances {C_mu}"): the graph is the block-diagonal union of the
+ * instances, group_of_row[i] = instance of row i, non-decreasing (each instance
+ * is a contiguous row range), in [0, n_groups); no edge may join two instances
+ * (QQA_ERR_BAD_GRAPH). The replicas of every instance anneal together in one
+ * step kernel; qqa_round_evaluate_groups reports every instance separately.
+ * Max clique takes the complement inside each instance. group_of_row = NULL:
+ * one instance (n_groups ignored). */
 typedef struct {
   int32_t n;
   int64_t nnz;            /* < 2^31 in this build                                          */
   const int64_t* rowptr;
   const int32_t* colidx;
+  const int32_t* group_of_row;  /* [n] or NULL                                             */
+  int32_t n_groups;             /* 1..2^24 when group_of_row is set                        */
 } qqa_graph;
 
 /* Evaluation of one rounded replica (integer counts: bit-exact, order-free). */
@@ -158,12 +169,27 @@ QQA_API int qqa_run(qqa_handle* h, const float* gamma_host, int64_t n_steps);
  * over total_steps = T; T = 1 gives gmin. Async. */
 QQA_API int qqa_run_linear(qqa_handle* h, float gmin, float gmax, int64_t total_steps, int64_t t0, int64_t t1);
 
-/* Round, evaluate every replica, pick the best over all ranks.
+/* Round, evaluate every replica, pick the best over all ranks. For a
+ * batch the counts and energies are summed over the instances (the energy of
+ * the union graph).
  * per_replica: host [S_local] or NULL; best_x: host uint8[n] (the best replica's
  * x on every rank) or NULL. Returns QQA_ERR_NONFINITE if any step produced a
  * non-finite theta. (sync) */
 QQA_API int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica,
                        int32_t* best_replica, double* best_energy, uint8_t* best_x);
+
+/* Per-instance evaluation of a batch (NEXT-3): round, count and pick,
+ * for every instance g, the best replica over all ranks (argmin of the
+ * instance's energy, lowest global replica on ties). Host outputs, NULL to skip:
+ * counts int64 [n_groups][S_local][3] (size, violations, cut of this rank's
+ * replicas), energy double [n_groups][S_local], best_replica int32 [n_groups]
+ * (global index), best_energy double [n_groups], best_x uint8 [n] (row i = x of
+ * its instance's best replica, on every rank). Without group_of_row this is the
+ * single-instance evaluation (n_groups = 1). (sync) */
+QQA_API int qqa_round_evaluate_groups(qqa_handle* h, int64_t* counts, double* energy, int32_t* best_replica,
+                                      double* best_energy, uint8_t* best_x);
+/* Number of instances of the handle's graph (1 without group_of_row). Host-only. */
+QQA_API int qqa_n_groups(qqa_handle* h, int32_t* n_groups);
 
 /* Checkpoint / inspection: host [n][S_local] float arrays, NULL to skip.
  * p = sigmoid(theta) as used by the next step; step = Adam steps taken. (sync) */

@@ -39,7 +39,8 @@ class Config(ctypes.Structure):
 
 class Graph(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("nnz", ctypes.c_int64),
-                ("rowptr", ctypes.c_void_p), ("colidx", ctypes.c_void_p)]
+                ("rowptr", ctypes.c_void_p), ("colidx", ctypes.c_void_p),
+                ("group_of_row", ctypes.c_void_p), ("n_groups", ctypes.c_int32)]
 
 
 class ReplicaResult(ctypes.Structure):
@@ -66,6 +67,8 @@ def _declare(lib):
         "qqa_run_linear": (ctypes.c_int, [H, ctypes.c_float, ctypes.c_float, i64, i64, i64]),
         "qqa_round_evaluate": (ctypes.c_int, [H, P, ctypes.POINTER(ctypes.c_int32),
                                               ctypes.POINTER(ctypes.c_double), P]),
+        "qqa_round_evaluate_groups": (ctypes.c_int, [H, P, P, P, P, P]),
+        "qqa_n_groups": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_int32)]),
         "qqa_get_state": (ctypes.c_int, [H, P, P, P, P, ctypes.POINTER(i64)]),
         "qqa_get_stats": (ctypes.c_int, [H, P, P, P]),
         "qqa_set_state": (ctypes.c_int, [H, P, P, P, P, i64]),

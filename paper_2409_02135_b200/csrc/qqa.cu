@@ -51,11 +51,12 @@ struct Shape {
   int SB = 0, B = 0, S_p = 0;  // replica blocks: S_p = B * SB local columns, layout [B][n+1][SB]
   int W = 0, lanes = 0, vpl = 0;
   int64_t nnz_pad = 0;         // row-padded CSR (rows rounded up to 4 entries)
+  int G = 1;                   // instances of a batch (NEXT-3); 1 without group_of_row
 };
 
 struct Layout {
-  size_t rowptr, colidx, rowptr_pad, colidx_pad, theta, m, v, p0, p1, c0, c1, ms, s0, s1, s2, flag, X, counts,
-      energy, best, beste, xbuf, total;
+  size_t rowptr, colidx, rowptr_pad, colidx_pad, gor, theta, m, v, p0, p1, c0, c1, ms, s0, s1, s2, flag, X,
+      counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, total;
 };
 
 Layout make_layout(const Shape& s) {
@@ -67,6 +68,7 @@ Layout make_layout(const Shape& s) {
   L.colidx = take((size_t)s.nnz * sizeof(int));
   L.rowptr_pad = take(((size_t)s.n + 1) * sizeof(int));
   L.colidx_pad = take((size_t)s.nnz_pad * sizeof(int));
+  L.gor = take((size_t)s.n * sizeof(int));
   L.theta = take(ns);
   L.m = take(ns);
   L.v = take(ns);
@@ -80,10 +82,14 @@ Layout make_layout(const Shape& s) {
   L.s2 = take(2 * (size_t)s.n * sizeof(long long));
   L.flag = take(4 * sizeof(int));
   L.X = take((size_t)s.n * s.W * sizeof(uint32_t));
-  L.counts = take(3 * (size_t)s.S_total * sizeof(long long));
+  L.counts = take(3 * (size_t)s.S_total * s.G * sizeof(long long));   // [S_total][G][3]
+  L.tot = take(3 * (size_t)s.S_total * sizeof(long long));            // [S_total][3] summed over instances
   L.energy = take((size_t)s.S_total * sizeof(double));
   L.best = take(sizeof(int));
   L.beste = take(sizeof(double));
+  L.genergy = take((size_t)s.S_total * s.G * sizeof(double));         // [G][S_total]
+  L.gbest = take((size_t)s.G * sizeof(int));
+  L.gbeste = take((size_t)s.G * sizeof(double));
   L.xbuf = take((size_t)s.n);
   L.total = o;
   return L;
@@ -121,12 +127,38 @@ int check_graph(const qqa_graph* g) {
   if (g->rowptr[0] != 0 || g->rowptr[g->n] != g->nnz) return fail(QQA_ERR_BAD_GRAPH, "rowptr[0] != 0 or rowptr[n] != nnz");
   for (int i = 0; i < g->n; ++i)
     if (g->rowptr[i + 1] < g->rowptr[i]) return fail(QQA_ERR_BAD_GRAPH, "rowptr is not non-decreasing");
+  if (g->group_of_row) {  // batch of instances (NEXT-3): contiguous row ranges 0..n_groups-1
+    if (g->n_groups < 1 || g->n_groups > (1 << 24)) return fail(QQA_ERR_INVALID_ARG, "n_groups must be in 1..2^24");
+    for (int i = 0; i < g->n; ++i) {
+      const int k = g->group_of_row[i];
+      if (k < 0 || k >= g->n_groups) return fail(QQA_ERR_BAD_GRAPH, "group_of_row out of [0, n_groups)");
+      if (i > 0 && k < g->group_of_row[i - 1])
+        return fail(QQA_ERR_BAD_GRAPH, "group_of_row must be non-decreasing (instances are contiguous row ranges)");
+    }
+  }
   return QQA_OK;
 }
 
+// Row range [a, b) of the instance holding row i (the whole graph without groups).
+void instance_range(const qqa_graph* g, int i, int& a, int& b) {
+  if (!g->group_of_row) { a = 0; b = g->n; return; }
+  const int k = g->group_of_row[i];
+  a = i; b = i + 1;
+  while (a > 0 && g->group_of_row[a - 1] == k) --a;
+  while (b < g->n && g->group_of_row[b] == k) ++b;
+}
+
 int64_t problem_nnz(const qqa_graph* g, int problem) {
-  if (problem == QQA_MAXCLIQUE) return (int64_t)g->n * (g->n - 1) - g->nnz;
-  return g->nnz;
+  if (problem != QQA_MAXCLIQUE) return g->nnz;
+  if (!g->group_of_row) return (int64_t)g->n * (g->n - 1) - g->nnz;
+  int64_t pairs = 0;  // sum over instances of n_k (n_k - 1)
+  for (int i = 0; i < g->n;) {
+    int a, b;
+    instance_range(g, i, a, b);
+    pairs += (int64_t)(b - a) * (b - a - 1);
+    i = b;
+  }
+  return pairs - g->nnz;
 }
 
 int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
@@ -139,6 +171,7 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   if (s.nnz >= (int64_t)INT32_MAX) return fail(QQA_ERR_UNSUPPORTED, "complement nnz >= 2^31");
   s.S_local = c->S_local;
   s.S_total = c->S_total;
+  s.G = g->group_of_row ? g->n_groups : 1;
   // Replica blocking: when one copy of p is larger than the L2
   // budget, split the replicas into blocks of SB (a power of two >= 8) so that
   // one block of p -- the gathered working set while the grid sweeps it -- fits.
@@ -162,7 +195,9 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   s.vpl = next_pow2((SB8 + s.lanes - 1) / s.lanes);
   s.nnz_pad = 0;
   for (int i = 0; i < s.n; ++i) {
-    const int64_t deg = (c->problem == QQA_MAXCLIQUE) ? (int64_t)(s.n - 1) - (g->rowptr[i + 1] - g->rowptr[i])
+    int a = 0, b = s.n;
+    if (c->problem == QQA_MAXCLIQUE) instance_range(g, i, a, b);
+    const int64_t deg = (c->problem == QQA_MAXCLIQUE) ? (int64_t)(b - a - 1) - (g->rowptr[i + 1] - g->rowptr[i])
                                                       : g->rowptr[i + 1] - g->rowptr[i];
     s.nnz_pad += (deg + 3) / 4 * 4;
   }
@@ -171,16 +206,19 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   return QQA_OK;
 }
 
-// Complement CSR (max clique = MIS on the complement graph).
+// Complement CSR (max clique = MIS on the complement graph); for a batch
+// the complement is taken inside each instance (block-diagonal union of complements).
 void build_complement(const qqa_graph* g, std::vector<int>& rp, std::vector<int>& ci) {
   const int n = g->n;
   rp.assign((size_t)n + 1, 0);
   ci.clear();
-  ci.reserve((size_t)((int64_t)n * (n - 1) - g->nnz));
+  ci.reserve((size_t)problem_nnz(g, QQA_MAXCLIQUE));
   std::vector<char> mark((size_t)n, 0);
   for (int i = 0; i < n; ++i) {
+    int a, b;
+    instance_range(g, i, a, b);
     for (int64_t e = g->rowptr[i]; e < g->rowptr[i + 1]; ++e) mark[g->colidx[e]] = 1;
-    for (int j = 0; j < n; ++j)
+    for (int j = a; j < b; ++j)
       if (j != i && !mark[j]) ci.push_back(j);
     for (int64_t e = g->rowptr[i]; e < g->rowptr[i + 1]; ++e) mark[g->colidx[e]] = 0;
     rp[i + 1] = (int)ci.size();
@@ -206,10 +244,15 @@ struct qqa_handle {
   float2* ms = nullptr;
   int* flag = nullptr;
   uint32_t* X = nullptr;
+  int* gor = nullptr;          // group_of_row on the device (NULL without a batch)
   unsigned long long* counts = nullptr;
+  long long* tot = nullptr;
   double* energy = nullptr;
   int* best = nullptr;
   double* beste = nullptr;
+  double* genergy = nullptr;
+  int* gbest = nullptr;
+  double* gbeste = nullptr;
   uint8_t* xbuf = nullptr;
   int cur = 0;   // p / c buffer of the current step (mod 2)
   int scur = 0;  // sums buffer of the current step (mod 3)
@@ -484,9 +527,14 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   h->flag = (int*)(ws + L.flag);
   h->X = (uint32_t*)(ws + L.X);
   h->counts = (unsigned long long*)(ws + L.counts);
+  h->tot = (long long*)(ws + L.tot);
   h->energy = (double*)(ws + L.energy);
   h->best = (int*)(ws + L.best);
   h->beste = (double*)(ws + L.beste);
+  h->genergy = (double*)(ws + L.genergy);
+  h->gbest = (int*)(ws + L.gbest);
+  h->gbeste = (double*)(ws + L.gbeste);
+  h->gor = g->group_of_row ? (int*)(ws + L.gor) : nullptr;
   h->xbuf = (uint8_t*)(ws + L.xbuf);
 
   // Graph -> device (int32 offsets). Max clique walks the complement graph.
@@ -508,14 +556,15 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   QQA_CUDA_C(cudaMemcpyAsync(h->rowptr, rp32.data(), rp32.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
   if (s.nnz > 0)
     QQA_CUDA_C(cudaMemcpyAsync(h->colidx, ci_src, (size_t)s.nnz * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  if (h->gor && s.n > 0)
+    QQA_CUDA_C(cudaMemcpyAsync(h->gor, g->group_of_row, (size_t)s.n * sizeof(int), cudaMemcpyHostToDevice, h->stream));
   QQA_CUDA_C(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
-  // theta/m/v padding and both p buffers start at zero / sigmoid(0)
   // theta/m/v padding and the zero row n of both p buffers
   for (float* buf : {h->theta, h->m, h->v, h->p[0], h->p[1]})
     QQA_CUDA_C(cudaMemsetAsync(buf, 0, ((size_t)s.n + 1) * s.S_p * sizeof(float), h->stream));
   if (cfg->problem != QQA_MAXCLIQUE && s.n > 0 && s.nnz > 0) {
     const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
-    qqa::k_validate<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, s.n, h->flag);
+    qqa::k_validate<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, s.n, h->gor, h->flag);
     QQA_CUDA_C(cudaGetLastError());
     h->launches++;
     int flag = 0;
@@ -527,6 +576,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
       if (flag & 4) why += " row not strictly ascending (unsorted or duplicate);";
       if (flag & 8) why += " self-loop;";
       if (flag & 16) why += " not symmetric;";
+      if (flag & 32) why += " edge between two instances of the batch;";
       return cleanup(fail(QQA_ERR_BAD_GRAPH, "graph rejected:" + why));
     }
   }
@@ -617,52 +667,101 @@ int qqa_run_linear(qqa_handle* h, float gmin, float gmax, int64_t total_steps, i
   return do_steps(h, gam.data(), t1 - t0);
 }
 
-int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* best_replica,
-                       double* best_energy, uint8_t* best_x) {
-  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
-  int st = set_device(h);
-  if (st) return st;
+}  // extern "C"
+
+namespace {
+
+// K3-K5 on the device: round + pack, per-(replica, instance) counts, all-gather of
+// the counts over ranks, energies + argmin of the totals and of every instance.
+int evaluate_core(qqa_handle* h) {
   const Shape& s = h->s;
   const int off = h->cfg.replica_offset;
-  // K3: round + pack
-  if (s.n > 0) {
+  if (s.n > 0) {  // K3: round + pack
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)s.n * s.W * 32 + 255) / 256, (int64_t)h->sm_count * 16));
     const float thr = (h->cfg.map == QQA_MAP_CLAMP) ? 0.5f : 0.0f;   // x = Theta(p - 1/2)
     qqa::k_pack<<<blocks, 256, 0, h->stream>>>(h->theta, h->X, s.n, s.SB, s.S_local, s.W, thr);
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }
-  // K4: counts of the local replicas, placed at their global slots
-  QQA_CUDA(cudaMemsetAsync(h->counts, 0, 3 * (size_t)s.S_total * sizeof(long long), h->stream));
+  // K4: counts of the local replicas at their global slots, [S_total][G][3]
+  QQA_CUDA(cudaMemsetAsync(h->counts, 0, 3 * (size_t)s.S_total * s.G * sizeof(long long), h->stream));
   if (s.n > 0) {
     const int R = (int)std::max<int64_t>(1, std::min<int64_t>(s.n, (int64_t)h->sm_count * 64 / s.W));
+    const int CH = (s.n + R - 1) / R;
     const int64_t warps = (int64_t)s.W * R;
     const int blocks = (int)((warps + 7) / 8);
-    qqa::k_eval<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, h->X, s.n, s.W, R, s.S_local,
-                                               h->counts + 3 * (size_t)off);
+    qqa::k_eval<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, h->X, h->gor, s.n, s.W, R, CH, s.S_local, s.G,
+                                               h->counts + 3 * (size_t)off * s.G);
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }
   if (h->comm && h->nranks > 1) {
-    QQA_NCCL(ncclAllGather(h->counts + 3 * (size_t)off, h->counts, 3 * (size_t)s.S_local, ncclInt64, h->comm, h->stream));
+    QQA_NCCL(ncclAllGather(h->counts + 3 * (size_t)off * s.G, h->counts, 3 * (size_t)s.S_local * s.G, ncclInt64,
+                           h->comm, h->stream));
   }
-  // K5: energies + argmin over all replicas
-  qqa::k_argmin<<<1, 1024, 0, h->stream>>>((const long long*)h->counts, s.S_total,
-                                            h->cfg.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS,
-                                            (double)h->cfg.penalty, h->energy, h->best, h->beste);
+  const int prob = h->cfg.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;
+  const long long* tot = (const long long*)h->counts;
+  if (s.G > 1) {  // totals over instances = the energy of the union graph
+    qqa::k_sum_groups<<<std::max(1, std::min((3 * s.S_total + 255) / 256, h->sm_count * 4)), 256, 0, h->stream>>>(
+        (const long long*)h->counts, s.S_total, s.G, h->tot);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+    tot = h->tot;
+    qqa::k_argmin<<<s.G, 1024, 0, h->stream>>>((const long long*)h->counts, 3 * s.G, s.S_total, prob,
+                                                (double)h->cfg.penalty, h->genergy, h->gbest, h->gbeste);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  // K5: energies + argmin over all replicas (of the totals)
+  qqa::k_argmin<<<1, 1024, 0, h->stream>>>(tot, 3, s.S_total, prob, (double)h->cfg.penalty, h->energy, h->best,
+                                           h->beste);
   QQA_CUDA(cudaGetLastError());
   h->launches++;
-  int best = 0, flag = 0;
+  if (s.G == 1) {  // the single instance is the whole graph
+    QQA_CUDA(cudaMemcpyAsync(h->genergy, h->energy, (size_t)s.S_total * sizeof(double), cudaMemcpyDeviceToDevice,
+                             h->stream));
+    QQA_CUDA(cudaMemcpyAsync(h->gbest, h->best, sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+    QQA_CUDA(cudaMemcpyAsync(h->gbeste, h->beste, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  }
+  return QQA_OK;
+}
+
+int finish_eval(qqa_handle* h) {
+  int flag = 0;
+  QQA_CUDA(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  if (h->comm) {
+    ncclResult_t async_err = ncclSuccess;
+    ncclCommGetAsyncError(h->comm, &async_err);
+    if (async_err != ncclSuccess) return fail(QQA_ERR_COMM, ncclGetErrorString(async_err));
+  }
+  if (flag & 1) return fail(QQA_ERR_NONFINITE, "a non-finite theta appeared during the run");
+  return QQA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* best_replica,
+                       double* best_energy, uint8_t* best_x) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  if ((st = evaluate_core(h))) return st;
+  const Shape& s = h->s;
+  const int off = h->cfg.replica_offset;
+  const long long* tot = (s.G > 1) ? h->tot : (const long long*)h->counts;
+  int best = 0;
   double be = 0.0;
   QQA_CUDA(cudaMemcpyAsync(&best, h->best, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   QQA_CUDA(cudaMemcpyAsync(&be, h->beste, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  QQA_CUDA(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   std::vector<long long> cnt;
   std::vector<double> en;
   if (per_replica) {
     cnt.resize(3 * (size_t)s.S_local);
     en.resize((size_t)s.S_local);
-    QQA_CUDA(cudaMemcpyAsync(cnt.data(), h->counts + 3 * (size_t)off, cnt.size() * sizeof(long long),
+    QQA_CUDA(cudaMemcpyAsync(cnt.data(), tot + 3 * (size_t)off, cnt.size() * sizeof(long long),
                              cudaMemcpyDeviceToHost, h->stream));
     QQA_CUDA(cudaMemcpyAsync(en.data(), h->energy + off, en.size() * sizeof(double), cudaMemcpyDeviceToHost,
                              h->stream));
@@ -680,13 +779,8 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
       QQA_NCCL(ncclBroadcast(h->xbuf, h->xbuf, (size_t)s.n, ncclUint8, owner, h->comm, h->stream));
     }
     QQA_CUDA(cudaMemcpyAsync(best_x, h->xbuf, (size_t)s.n, cudaMemcpyDeviceToHost, h->stream));
-    QQA_CUDA(cudaStreamSynchronize(h->stream));
   }
-  if (h->comm) {
-    ncclResult_t async_err = ncclSuccess;
-    ncclCommGetAsyncError(h->comm, &async_err);
-    if (async_err != ncclSuccess) return fail(QQA_ERR_COMM, ncclGetErrorString(async_err));
-  }
+  if ((st = finish_eval(h))) return st;
   if (per_replica) {
     for (int k = 0; k < s.S_local; ++k) {
       qqa_replica_result& r = per_replica[k];
@@ -700,7 +794,66 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
   }
   if (best_replica) *best_replica = best;
   if (best_energy) *best_energy = be;
-  if (flag & 1) return fail(QQA_ERR_NONFINITE, "a non-finite theta appeared during the run");
+  return QQA_OK;
+}
+
+int qqa_n_groups(qqa_handle* h, int32_t* n_groups) {
+  if (!h || !n_groups) return fail(QQA_ERR_INVALID_ARG, "handle or n_groups is NULL");
+  *n_groups = h->s.G;
+  return QQA_OK;
+}
+
+int qqa_round_evaluate_groups(qqa_handle* h, int64_t* counts, double* energy, int32_t* best_replica,
+                              double* best_energy, uint8_t* best_x) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  int st = set_device(h);
+  if (st) return st;
+  if ((st = evaluate_core(h))) return st;
+  const Shape& s = h->s;
+  const int off = h->cfg.replica_offset;
+  if (best_replica) QQA_CUDA(cudaMemcpyAsync(best_replica, h->gbest, (size_t)s.G * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  if (best_energy) QQA_CUDA(cudaMemcpyAsync(best_energy, h->gbeste, (size_t)s.G * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (energy)  // [G][S_local]: this rank's replicas of every instance
+    QQA_CUDA(cudaMemcpy2DAsync(energy, (size_t)s.S_local * sizeof(double), h->genergy + off,
+                               (size_t)s.S_total * sizeof(double), (size_t)s.S_local * sizeof(double), (size_t)s.G,
+                               cudaMemcpyDeviceToHost, h->stream));
+  std::vector<long long> cnt;
+  if (counts) {  // device [S_total][G][3] -> host [G][S_local][3]
+    cnt.resize(3 * (size_t)s.S_local * s.G);
+    QQA_CUDA(cudaMemcpyAsync(cnt.data(), h->counts + 3 * (size_t)off * s.G, cnt.size() * sizeof(long long),
+                             cudaMemcpyDeviceToHost, h->stream));
+  }
+  if (best_x && s.n > 0) {
+    if (h->gor) {
+      qqa::k_extract_groups<<<std::max(1, std::min((s.n + 255) / 256, h->sm_count * 4)), 256, 0, h->stream>>>(
+          h->X, h->gor, h->gbest, s.n, s.W, off, s.S_local, h->xbuf);
+      QQA_CUDA(cudaGetLastError());
+      h->launches++;
+      if (h->comm && h->nranks > 1)  // exactly one rank holds each row's best replica: sum = that value
+        QQA_NCCL(ncclAllReduce(h->xbuf, h->xbuf, (size_t)s.n, ncclUint8, ncclSum, h->comm, h->stream));
+      QQA_CUDA(cudaMemcpyAsync(best_x, h->xbuf, (size_t)s.n, cudaMemcpyDeviceToHost, h->stream));
+    } else {
+      int best = 0;
+      QQA_CUDA(cudaMemcpyAsync(&best, h->best, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      QQA_CUDA(cudaStreamSynchronize(h->stream));
+      const int owner = best / s.S_local;
+      if (!h->comm || h->nranks == 1 || owner == h->rank) {
+        qqa::k_extract<<<std::max(1, std::min((s.n + 255) / 256, h->sm_count * 4)), 256, 0, h->stream>>>(
+            h->X, s.n, s.W, best - off, h->xbuf);
+        QQA_CUDA(cudaGetLastError());
+        h->launches++;
+      }
+      if (h->comm && h->nranks > 1)
+        QQA_NCCL(ncclBroadcast(h->xbuf, h->xbuf, (size_t)s.n, ncclUint8, owner, h->comm, h->stream));
+      QQA_CUDA(cudaMemcpyAsync(best_x, h->xbuf, (size_t)s.n, cudaMemcpyDeviceToHost, h->stream));
+    }
+  }
+  if ((st = finish_eval(h))) return st;
+  if (counts)
+    for (int k = 0; k < s.S_local; ++k)
+      for (int g = 0; g < s.G; ++g)
+        for (int c = 0; c < 3; ++c)
+          counts[((size_t)g * s.S_local + k) * 3 + c] = cnt[((size_t)k * s.G + g) * 3 + c];
   return QQA_OK;
 }
 

@@ -484,8 +484,9 @@ __global__ void __launch_bounds__(256) k_init(const InitParams P) {
 // --------------------------------------------------------- graph checks
 // Original CSR: bit 1: column out of range, bit 2: row not strictly ascending
 // (unsorted / duplicate), bit 3: self-loop, bit 4: asymmetric (j's row lacks i).
+// bit 5: edge between two instances of a batch (group_of_row[i] != group_of_row[j]).
 __global__ void k_validate(const int* __restrict__ rowptr, const int* __restrict__ colidx, int n,
-                           int* __restrict__ flag) {
+                           const int* __restrict__ gor, int* __restrict__ flag) {
   int bad = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int e0 = rowptr[i], e1 = rowptr[i + 1];
@@ -495,6 +496,7 @@ __global__ void k_validate(const int* __restrict__ rowptr, const int* __restrict
       if (j < 0 || j >= n) { bad |= 2; continue; }
       if (j <= prev) bad |= 4;
       if (j == i) bad |= 8;
+      if (gor && gor[j] != gor[i]) bad |= 32;
       prev = j;
       int lo = rowptr[j], hi = rowptr[j + 1];
       while (lo < hi) {
@@ -539,18 +541,37 @@ __global__ void k_pack(const float* __restrict__ theta, uint32_t* __restrict__ X
   }
 }
 
-// K4: per-replica integer counts; lane = replica bit of word w; each undirected
-// edge once (j > i). Warps 0..W*R-1: warp k takes word k % W and rows k / W, +R, ...
-// counts[s][3] = (size, violations, cut), unsigned 64-bit atomics (exact, order-free).
+// K4: per-(instance, replica) integer counts; lane = replica bit of word w; each
+// undirected edge once (j > i). Warp k takes word k % W and the contiguous row
+// chunk [c CH, (c+1) CH), c = k / W; its partial counts are flushed (u64 atomics:
+// exact, order-free) whenever the instance of the row changes (rows of one
+// instance are contiguous) and at the end.
+// counts[s][g][3] = (size, violations, cut), s local (the caller offsets the pointer).
 __global__ void k_eval(const int* __restrict__ rowptr, const int* __restrict__ colidx,
-                       const uint32_t* __restrict__ X, int n, int W, int R, int S_local,
-                       unsigned long long* __restrict__ counts) {
+                       const uint32_t* __restrict__ X, const int* __restrict__ gor, int n, int W, int R, int CH,
+                       int S_local, int G, unsigned long long* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= W * R) return;
   const int w = warp % W;
+  const int s = w * 32 + lane;
+  const int i0 = (warp / W) * CH, i1 = min(n, i0 + CH);
   unsigned long long size = 0, viol = 0, cut = 0;
-  for (int i = warp / W; i < n; i += R) {
+  int cur = (gor && i0 < n) ? gor[i0] : 0;
+  auto flush = [&](int g) {
+    if (s < S_local && (size | viol | cut)) {
+      unsigned long long* c = counts + ((size_t)s * G + g) * 3;
+      atomicAdd(c + 0, size);
+      atomicAdd(c + 1, viol);
+      atomicAdd(c + 2, cut);
+    }
+    size = viol = cut = 0;
+  };
+  for (int i = i0; i < i1; ++i) {
+    if (gor) {
+      const int g = gor[i];
+      if (g != cur) { flush(cur); cur = g; }
+    }
     const uint32_t bi = (X[(size_t)i * W + w] >> lane) & 1u;
     size += bi;
     const int e1 = rowptr[i + 1];
@@ -562,25 +583,37 @@ __global__ void k_eval(const int* __restrict__ rowptr, const int* __restrict__ c
       cut += bi ^ bj;
     }
   }
-  const int s = w * 32 + lane;
-  if (s < S_local && (size | viol | cut)) {
-    atomicAdd(counts + 3 * s + 0, size);
-    atomicAdd(counts + 3 * s + 1, viol);
-    atomicAdd(counts + 3 * s + 2, cut);
+  flush(cur);
+}
+
+// Totals over instances: tot[s][c] = sum_g counts[s][g][c] (the energy of the union graph).
+__global__ void k_sum_groups(const long long* __restrict__ counts, int S_total, int G, long long* __restrict__ tot) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < 3 * S_total; k += gridDim.x * blockDim.x) {
+    const int s = k / 3, c = k - 3 * s;
+    long long a = 0;
+    for (int g = 0; g < G; ++g) a += counts[((size_t)s * G + g) * 3 + c];
+    tot[k] = a;
   }
 }
 
-// K5: energies of all S_total replicas and argmin (lowest index on ties). One CTA.
-__global__ void k_argmin(const long long* __restrict__ counts, int S_total, int problem, double lam,
+// K5: energies of all S_total replicas and argmin (lowest index on ties). One CTA
+// per instance g = blockIdx.x: counts of replica s at counts[s stride + 3 g],
+// energy[g][S_total], best[g], best_e[g] (stride = 3 G; G = 1 for the totals).
+__global__ void k_argmin(const long long* __restrict__ counts, int stride, int S_total, int problem, double lam,
                          double* __restrict__ energy, int* __restrict__ best, double* __restrict__ best_e) {
   __shared__ double se[32];
   __shared__ int si[32];
+  counts += 3 * (size_t)blockIdx.x;
+  energy += (size_t)blockIdx.x * S_total;
+  best += blockIdx.x;
+  best_e += blockIdx.x;
   double be = 0.0;
   int bi = -1;
   for (int s = threadIdx.x; s < S_total; s += blockDim.x) {
+    const long long* c = counts + (size_t)s * stride;
     const double e = (problem == kMAXCUT)
-                         ? -(double)counts[3 * s + 2]
-                         : __dadd_rn(-(double)counts[3 * s + 0], __dmul_rn(lam, (double)counts[3 * s + 1]));
+                         ? -(double)c[2]
+                         : __dadd_rn(-(double)c[0], __dmul_rn(lam, (double)c[1]));
     energy[s] = e;
     if (bi < 0 || e < be) { be = e; bi = s; }
   }
@@ -609,6 +642,17 @@ __global__ void k_argmin(const long long* __restrict__ counts, int S_total, int 
 __global__ void k_extract(const uint32_t* __restrict__ X, int n, int W, int s_local, uint8_t* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = (uint8_t)((X[(size_t)i * W + (s_local >> 5)] >> (s_local & 31)) & 1u);
+}
+
+// Batch: row i gets x of its instance's best replica best[gor[i]] if this rank
+// holds it ([off, off + S_local)), else 0 (ranks are then summed: one owner per row).
+__global__ void k_extract_groups(const uint32_t* __restrict__ X, const int* __restrict__ gor,
+                                 const int* __restrict__ best, int n, int W, int off, int S_local,
+                                 uint8_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = best[gor[i]] - off;
+    out[i] = (s >= 0 && s < S_local) ? (uint8_t)((X[(size_t)i * W + (s >> 5)] >> (s & 31)) & 1u) : (uint8_t)0;
+  }
 }
 
 }  // namespace qqa

@@ -29,15 +29,20 @@ def make_config(problem="mis", S_total=16, seed=1, replica_offset=0, S_local=Non
                   mid, float(kw["temperature"]))
 
 
-def _as_graph(rowptr: np.ndarray, colidx: np.ndarray) -> Graph:
+def _as_graph(rowptr: np.ndarray, colidx: np.ndarray, group_of_row: np.ndarray | None = None,
+              n_groups: int | None = None) -> Graph:
     n = len(rowptr) - 1
-    return Graph(n, int(rowptr[-1]) if n >= 0 else 0, rowptr.ctypes.data, colidx.ctypes.data)
+    if group_of_row is None:
+        return Graph(n, int(rowptr[-1]) if n >= 0 else 0, rowptr.ctypes.data, colidx.ctypes.data, None, 1)
+    G = int(n_groups) if n_groups is not None else (int(group_of_row.max()) + 1 if group_of_row.size else 1)
+    return Graph(n, int(rowptr[-1]), rowptr.ctypes.data, colidx.ctypes.data, group_of_row.ctypes.data, G)
 
 
-def workspace_bytes(rowptr, colidx, cfg: Config) -> int:
+def workspace_bytes(rowptr, colidx, cfg: Config, group_of_row=None, n_groups=None) -> int:
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     colidx = np.ascontiguousarray(colidx, np.int32)
-    g = _as_graph(rowptr, colidx)
+    gor = None if group_of_row is None else np.ascontiguousarray(group_of_row, np.int32)
+    g = _as_graph(rowptr, colidx, gor, n_groups)
     out = ctypes.c_size_t(0)
     check(lib.qqa_workspace_bytes(ctypes.byref(g), ctypes.byref(cfg), ctypes.byref(out)))
     return int(out.value)
@@ -51,10 +56,24 @@ class Result:
     per_replica: np.ndarray | None  # structured: size, violations, cut, energy, feasible, replica
 
 
-class Solver:
-    """One GPU's shard of the PQQA replica ensemble behind the C ABI."""
+@dataclass
+class GroupResult:
+    """Per-instance evaluation of a batch (NEXT-3)."""
+    best_replica: np.ndarray   # int32 [G], global replica index
+    best_energy: np.ndarray    # float64 [G]
+    best_x: np.ndarray | None  # uint8 [n]: row i = x of its instance's best replica
+    counts: np.ndarray | None  # int64 [G][S_local][3]
+    energy: np.ndarray | None  # float64 [G][S_local]
 
-    def __init__(self, rowptr, colidx, cfg: Config, device=None, stream=None, workspace=None):
+
+class Solver:
+    """One GPU's shard of the PQQA replica ensemble behind the C ABI.
+
+    ``group_of_row`` (optional) makes the graph a batch of instances (block-diagonal
+    union, contiguous row ranges; NEXT-3)."""
+
+    def __init__(self, rowptr, colidx, cfg: Config, device=None, stream=None, workspace=None,
+                 group_of_row=None, n_groups=None):
         import torch
 
         self._torch = torch
@@ -64,7 +83,8 @@ class Solver:
         self.colidx = np.ascontiguousarray(colidx, np.int32)
         self.n = len(self.rowptr) - 1
         self.S_local = cfg.S_local
-        g = _as_graph(self.rowptr, self.colidx)
+        self.group_of_row = None if group_of_row is None else np.ascontiguousarray(group_of_row, np.int32)
+        g = _as_graph(self.rowptr, self.colidx, self.group_of_row, n_groups)
         nbytes = ctypes.c_size_t(0)
         check(lib.qqa_workspace_bytes(ctypes.byref(g), ctypes.byref(cfg), ctypes.byref(nbytes)))
         self.workspace_bytes = int(nbytes.value)
@@ -102,6 +122,24 @@ class Solver:
         if per is not None:
             arr = np.ctypeslib.as_array(per).copy()
         return Result(int(best.value), float(be.value), x, arr)
+
+    @property
+    def n_groups(self) -> int:
+        k = ctypes.c_int32(0)
+        check(lib.qqa_n_groups(self._h, ctypes.byref(k)))
+        return int(k.value)
+
+    def round_evaluate_groups(self, want_x=True, want_counts=True) -> GroupResult:
+        G = self.n_groups
+        best = np.zeros(G, np.int32)
+        be = np.zeros(G, np.float64)
+        cnt = np.zeros((G, self.S_local, 3), np.int64) if want_counts else None
+        en = np.zeros((G, self.S_local), np.float64) if want_counts else None
+        x = np.zeros(self.n, np.uint8) if want_x else None
+        check(lib.qqa_round_evaluate_groups(self._h, cnt.ctypes.data if cnt is not None else None,
+                                            en.ctypes.data if en is not None else None, best.ctypes.data,
+                                            be.ctypes.data, x.ctypes.data if x is not None else None))
+        return GroupResult(best, be, x, cnt, en)
 
     # --------------------------------------------------------------- state
     def get_state(self):
