@@ -138,6 +138,30 @@ def random_bipartite(a: int, b: int, p: float, seed: int) -> Graph:
     return from_edges(a + b, u.astype(np.int32), (v + a).astype(np.int32))
 
 
+def queens(r: int, c: int) -> Graph:
+    """Queens graph of an r x c board: squares adjacent iff they share a row, a column
+    or a diagonal. queen5-5: 25 nodes, 160 edges (Table 13)."""
+    a = np.arange(r * c) // c
+    b = np.arange(r * c) % c
+    u, v = np.triu_indices(r * c, 1)
+    keep = (a[u] == a[v]) | (b[u] == b[v]) | (np.abs(a[u] - a[v]) == np.abs(b[u] - b[v]))
+    return from_edges(r * c, u[keep].astype(np.int32), v[keep].astype(np.int32))
+
+
+def mycielski(k: int) -> Graph:
+    """myciel_k of the COLOR set: k-1 Mycielski transformations of K2
+    (mu(G): copies u_i of every vertex v_i, u_i ~ N(v_i), and a hub w ~ every u_i).
+    myciel5: 47 nodes, 236 edges; myciel6: 95, 755 (Table 13)."""
+    n, eu, ev = 2, [0], [1]
+    for _ in range(k - 1):
+        u0 = list(eu) + [n + a for a in eu] + [n + b for b in ev] + [n + i for i in range(n)]
+        v0 = list(ev) + list(ev) + list(eu) + [2 * n] * n
+        n, eu, ev = 2 * n + 1, u0, v0
+    lo = np.minimum(eu, ev).astype(np.int32)
+    hi = np.maximum(eu, ev).astype(np.int32)
+    return from_edges(n, lo, hi)
+
+
 def disjoint_union(graphs) -> tuple[Graph, np.ndarray]:
     """Block-diagonal union of instances (the paper's batch of instances {C_mu}):
     instance k's rows are the contiguous range after instances 0..k-1. Returns the union

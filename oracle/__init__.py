@@ -98,6 +98,19 @@ def _L():
         lib.oc_eval_groups.restype = None
         lib.oc_eval_groups.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
                                        f32, ctypes.c_float, i32, ctypes.c_int32, i64, f64, i32]
+        u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        lib.oc_kt_K.restype = ctypes.c_float
+        lib.oc_kt_K.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_float]
+        lib.oc_normalize_K.restype = None
+        lib.oc_normalize_K.argtypes = [f32, ctypes.c_int32, f32]
+        lib.oc_init_K.restype = None
+        lib.oc_init_K.argtypes = [ctypes.c_int32, cfgp, ctypes.c_int32, f32, f32, f32, f32, i64, i64]
+        lib.oc_run_K.restype = ctypes.c_int
+        lib.oc_run_K.argtypes = [ctypes.c_int32, i64, i32, cfgp, ctypes.c_int32, f32, ctypes.c_int64,
+                                 ctypes.c_int64, f32, f32, f32, f32, i64, i64]
+        lib.oc_eval_K.restype = None
+        lib.oc_eval_K.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_int32, f32, u8, i64, f64,
+                                  ctypes.POINTER(ctypes.c_int32)]
         lib.oc_complement.restype = ctypes.c_int64
         lib.oc_complement.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_void_p, ctypes.c_void_p]
         _lib = lib
@@ -309,3 +322,65 @@ def complement_groups(g, group_of_row):
     rp = np.concatenate(rps)
     ci = np.concatenate(cis).astype(np.int32) if cis else np.zeros(0, np.int32)
     return rp, ci
+
+
+# ------------------------------------------------------- K-ary (NEXT-4)
+@dataclasses.dataclass
+class StateK:
+    """K-ary ensemble state: P (the parameter, row-stochastic), m, v [N][S][K]; stats [N][K]."""
+    P: np.ndarray
+    m: np.ndarray
+    v: np.ndarray
+    c: np.ndarray
+    sumD: np.ndarray
+    sumD2: np.ndarray
+    t: int = 0
+
+    def copy(self) -> "StateK":
+        return StateK(self.P.copy(), self.m.copy(), self.v.copy(), self.c.copy(), self.sumD.copy(),
+                      self.sumD2.copy(), self.t)
+
+
+def kt_K(K: int, alpha: int, gamma: float) -> float:
+    return float(_L().oc_kt_K(K, alpha, gamma))
+
+
+def normalize_K(w) -> np.ndarray:
+    w = np.ascontiguousarray(w, np.float32)
+    out = np.empty_like(w)
+    _L().oc_normalize_K(w, w.size, out)
+    return out
+
+
+def init_K(g, cfg: OcCfg, K: int) -> StateK:
+    n, S = g.n, cfg.S
+    st = StateK(*(np.zeros((n, S, K), np.float32) for _ in range(3)), np.zeros((n, K), np.float32),
+                np.zeros((n, K), np.int64), np.zeros((n, K), np.int64), 0)
+    _L().oc_init_K(n, ctypes.byref(cfg), K, st.P, st.m, st.v, st.c, st.sumD, st.sumD2)
+    return st
+
+
+def run_K(g, cfg: OcCfg, K: int, gammas, state: StateK | None = None) -> StateK:
+    """Advance a K-ary (graph colouring) ensemble by len(gammas) steps, in place."""
+    st = init_K(g, cfg, K) if state is None else state
+    gam = np.ascontiguousarray(gammas, dtype=np.float32)
+    rc = _L().oc_run_K(g.n, np.ascontiguousarray(g.rowptr, np.int64), np.ascontiguousarray(g.colidx, np.int32),
+                       ctypes.byref(cfg), K, gam, len(gam), st.t, st.P, st.m, st.v, st.c, st.sumD, st.sumD2)
+    st.t += len(gam)
+    if rc != 0:
+        raise FloatingPointError("oracle: non-finite parameter (SPEC.md:396 abort)")
+    return st
+
+
+def evaluate_K(g, P: np.ndarray):
+    """Colour x = argmax_k P (lowest k on ties), conflicts per replica.
+    Returns (counts[S][3] = (0, conflicts, |E| - conflicts), energy[S] = conflicts, best, X[N][S])."""
+    P = np.ascontiguousarray(P, np.float32)
+    n, S, K = P.shape
+    X = np.zeros((n, S), np.uint8)
+    counts = np.zeros((S, 3), np.int64)
+    energy = np.zeros(S, np.float64)
+    best = ctypes.c_int32(0)
+    _L().oc_eval_K(n, np.ascontiguousarray(g.rowptr, np.int64), np.ascontiguousarray(g.colidx, np.int32), S, K,
+                   P, X, counts, energy, ctypes.byref(best))
+    return counts, energy, int(best.value), X

@@ -473,3 +473,206 @@ int64_t oc_complement(int32_t n, const int64_t* rowptr, const int32_t* colidx,
     free(mark);
     return nnz;
 }
+
+/* ================================================== K-ary (NEXT-4) ====== */
+/* Graph colouring with K colours (App. B, map P:672-676, energy
+ * P:745-750). Arrays are [n][S][K]; the parameter is P itself (row-stochastic
+ * per (i, s)): AdamW on P with dR/dP, (+ noise), then P = Clamp(P') / sum_k
+ * Clamp(P'_k) (uniform 1/K if every clamp is 0). Statistics per (i, k) over the
+ * replicas, with the binary path's fixed-point contract (shift = previous mean).
+ *   dR/dp_isk = q_isk + k_t (K p - 1)^(alpha-1) - a_c (p - mu_ik)/STD_ik,
+ *   q_isk = sum_{j in N(i)} p_jsk (CSR order), k_t = -gamma_t c_K alpha K,
+ *   c_K = 1/((K-1)((K-1)^(alpha-1) + 1)).
+ * fp32 contract for the K-ary parts:
+ *   - the entropy factor e = fl(fl(K p) - 1), e^(alpha-1) left to right;
+ *   - the normaliser Z = ((c_0 + c_1) + c_2) + ..., p_k = c_k / Z;
+ *   - noise key of (t, i, k, s) = base + ((t n + i) K + k) S_total + s. */
+
+/* k_t for the K-ary entropy, host double -> fp32 */
+float oc_kt_K(int32_t K, int32_t alpha, float gamma_t) {
+    const double cK = 1.0 / ((double)(K - 1) * (pow((double)(K - 1), (double)(alpha - 1)) + 1.0));
+    return (float)(-(double)gamma_t * cK * (double)alpha * (double)K);
+}
+
+static void normalize_K(const float* w, int32_t K, float* p) {
+    float Z = 0.0f;
+    for (int32_t k = 0; k < K; ++k) Z = Z + oc_clamp01(w[k]);
+    if (Z > 0.0f) {
+        for (int32_t k = 0; k < K; ++k) p[k] = oc_clamp01(w[k]) / Z;
+    } else {
+        const float u = (float)(1.0 / (double)K);
+        for (int32_t k = 0; k < K; ++k) p[k] = u;
+    }
+}
+
+void oc_normalize_K(const float* w, int32_t K, float* p) { normalize_K(w, K, p); }
+
+/* W_0 = 1/K + U(lo, hi) keyed (seed, i K + k, s) (the sum in double, rounded once), P_0 = normalise(W_0);
+ * the first statistics shift is c = 1/K (the centre of the simplex); sums of P_0. */
+void oc_init_K(int32_t n, const oc_cfg* cf, int32_t K, float* P, float* m, float* v,
+               float* c, int64_t* sumD, int64_t* sumD2) {
+    const int32_t S = cf->S;
+    const uint64_t base = mix64(cf->seed);
+    const double lo = (double)cf->init_lo, hi = (double)cf->init_hi;
+    float* w = (float*)malloc(sizeof(float) * (size_t)K);
+    const float c0 = (float)(1.0 / (double)K);
+    for (int32_t i = 0; i < n; ++i) {
+        for (int32_t s = 0; s < S; ++s) {
+            for (int32_t k = 0; k < K; ++k) {
+                const uint64_t key = base + ((uint64_t)i * (uint64_t)K + (uint64_t)k) * (uint64_t)S + (uint64_t)s;
+                const uint64_t kk = mix64(key) >> 40;
+                w[k] = (float)(1.0 / (double)K + (lo + (hi - lo) * (double)kk * 0x1p-24));
+            }
+            const size_t at = ((size_t)i * S + s) * K;
+            normalize_K(w, K, P + at);
+            for (int32_t k = 0; k < K; ++k) { m[at + k] = 0.0f; v[at + k] = 0.0f; }
+        }
+        for (int32_t k = 0; k < K; ++k) {
+            int64_t a = 0, b = 0;
+            for (int32_t s = 0; s < S; ++s) {
+                const float d = P[((size_t)i * S + s) * K + k] - c0;
+                a += llrintf(d * 0x1p40f);
+                const float dd = d * d;
+                b += llrintf(dd * 0x1p40f);
+            }
+            c[(size_t)i * K + k] = c0;
+            sumD[(size_t)i * K + k] = a;
+            sumD2[(size_t)i * K + k] = b;
+        }
+    }
+    free(w);
+}
+
+static int update_row_K(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, const int32_t* colidx,
+                        const oc_cfg* cf, int32_t K, float kt, const float* sc, const float* P,
+                        float* pp, float* mm, float* vv, const float* c_i, const int64_t* sD_i,
+                        const int64_t* sD2_i, float* p_new, float* c_new, int64_t* sD_new, int64_t* sD2_new,
+                        float* q, float* w, float* mu, float* sd) {
+    const int32_t S = cf->S;
+    const float at = sc[1], st = sc[2], rt = sc[3];
+    const float b1 = cf->beta1, b2 = cf->beta2, eps = cf->eps;
+    const float c1 = (float)(1.0 - (double)cf->beta1), c2 = (float)(1.0 - (double)cf->beta2);
+    const float ac = cf->comm, Kf = (float)K;
+    const float ns = oc_noise_scale(cf);
+    const uint64_t nbase = oc_noise_base(cf->seed);
+    int bad = 0;
+    for (int32_t k = 0; k < K; ++k) finalize_stats(c_i[k], sD_i[k], sD2_i[k], S, &mu[k], &sd[k]);
+    for (int32_t s = 0; s < S; ++s) {
+        for (int32_t k = 0; k < K; ++k) q[k] = 0.0f;
+        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+            const float* pj = P + ((size_t)colidx[e] * S + s) * K;
+            for (int32_t k = 0; k < K; ++k) q[k] = q[k] + pj[k];
+        }
+        const size_t at_s = (size_t)s * K;        /* offset of (s, 0) inside row i */
+        for (int32_t k = 0; k < K; ++k) {
+            const float pi = pp[at_s + k];
+            const float e = Kf * pi - 1.0f;
+            float ep = e;
+            for (int32_t a = 2; a < cf->alpha; ++a) ep = ep * e;       /* (K p - 1)^(alpha-1) */
+            const float ent = kt * ep;
+            const float com = (sd[k] >= 1e-6f) ? (-ac) * ((pi - mu[k]) / sd[k]) : 0.0f;
+            const float g = (q[k] + ent) + com;
+            float t1 = pi * at;
+            const float m1 = b1 * mm[at_s + k] + c1 * g;
+            const float v1 = b2 * vv[at_s + k] + (c2 * g) * g;
+            const float den = sqrtf(v1) * rt + eps;
+            t1 = t1 - st * (m1 / den);
+            if (cf->temperature > 0.0f) {
+                const uint64_t key = nbase + (((uint64_t)t * (uint64_t)n + (uint64_t)i) * (uint64_t)K + (uint64_t)k)
+                                                 * (uint64_t)S + (uint64_t)s;
+                t1 = t1 + ns * oc_gauss_from_hash(mix64(key));
+            }
+            if (!isfinite(t1)) bad = 1;
+            w[k] = t1;
+            mm[at_s + k] = m1;
+            vv[at_s + k] = v1;
+        }
+        normalize_K(w, K, p_new + at_s);
+    }
+    for (int32_t k = 0; k < K; ++k) {
+        int64_t a = 0, b = 0;
+        for (int32_t s = 0; s < S; ++s) {
+            const float d = p_new[(size_t)s * K + k] - mu[k];
+            a += llrintf(d * 0x1p40f);
+            const float dd = d * d;
+            b += llrintf(dd * 0x1p40f);
+        }
+        c_new[k] = mu[k];
+        sD_new[k] = a;
+        sD2_new[k] = b;
+    }
+    return bad;
+}
+
+/* n_steps K-ary annealing steps; P/m/v [n][S][K], c/sums [n][K] in place. Returns 0 or 5 (non-finite). */
+int oc_run_K(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg* cf, int32_t K,
+             const float* gamma, int64_t n_steps, int64_t t0, float* P, float* m, float* v,
+             float* c, int64_t* sumD, int64_t* sumD2) {
+    const int32_t S = cf->S;
+    const size_t NSK = (size_t)n * S * K, NK = (size_t)n * K;
+    float* P2 = (float*)malloc(sizeof(float) * (NSK ? NSK : 1));
+    float* cc = (float*)malloc(sizeof(float) * (NK ? NK : 1));
+    int64_t* da = (int64_t*)malloc(sizeof(int64_t) * (NK ? NK : 1));
+    int64_t* db = (int64_t*)malloc(sizeof(int64_t) * (NK ? NK : 1));
+    int bad = 0;
+    for (int64_t k = 0; k < n_steps && !bad; ++k) {
+        float sc[4];
+        const int64_t t = t0 + k + 1;
+        oc_step_scalars(cf, t, gamma[k], sc);
+        const float kt = oc_kt_K(K, cf->alpha, gamma[k]);
+        const int thr = cf->threads > 1 ? cf->threads : 1;
+        (void)thr;
+#pragma omp parallel num_threads(thr) reduction(| : bad)
+        {
+            float* q = (float*)malloc(sizeof(float) * (size_t)K * 4);
+            float* w = q + K;
+            float* mu = q + 2 * K;
+            float* sd = q + 3 * K;
+#pragma omp for schedule(static)
+            for (int32_t i = 0; i < n; ++i) {
+                const size_t r = (size_t)i * S * K, rk = (size_t)i * K;
+                bad |= update_row_K(i, n, t, rowptr, colidx, cf, K, kt, sc, P, P + r, m + r, v + r,
+                                    c + rk, sumD + rk, sumD2 + rk, P2 + r, cc + rk, da + rk, db + rk, q, w, mu, sd);
+            }
+            free(q);
+        }
+        memcpy(P, P2, sizeof(float) * NSK);
+        memcpy(c, cc, sizeof(float) * NK);
+        memcpy(sumD, da, sizeof(int64_t) * NK);
+        memcpy(sumD2, db, sizeof(int64_t) * NK);
+    }
+    free(P2); free(cc); free(da); free(db);
+    return bad ? 5 : 0;
+}
+
+/* x_is = argmax_k P (lowest k on ties); counts[s][3] = (0, conflicts, |E| - conflicts) with
+ * conflicts = #{(i<j) in E : x_i = x_j}; energy[s] = conflicts; *best = argmin, lowest s on ties;
+ * X (optional, [n][S] uint8) receives the colours. */
+void oc_eval_K(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t S, int32_t K,
+               const float* P, uint8_t* X, int64_t* counts, double* energy, int32_t* best) {
+    uint8_t* x = X ? X : (uint8_t*)malloc((size_t)n * S + 1);
+    for (int32_t i = 0; i < n; ++i)
+        for (int32_t s = 0; s < S; ++s) {
+            const float* pr = P + ((size_t)i * S + s) * K;
+            int32_t b = 0;
+            for (int32_t k = 1; k < K; ++k) if (pr[k] > pr[b]) b = k;
+            x[(size_t)i * S + s] = (uint8_t)b;
+        }
+    memset(counts, 0, sizeof(int64_t) * 3 * (size_t)S);
+    int64_t edges = 0;
+    for (int32_t i = 0; i < n; ++i)
+        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+            const int32_t j = colidx[e];
+            if (j <= i) continue;
+            ++edges;
+            for (int32_t s = 0; s < S; ++s) counts[3 * s + 1] += x[(size_t)i * S + s] == x[(size_t)j * S + s];
+        }
+    int32_t b = 0;
+    for (int32_t s = 0; s < S; ++s) {
+        counts[3 * s + 2] = edges - counts[3 * s + 1];
+        energy[s] = (double)counts[3 * s + 1];
+        if (energy[s] < energy[b]) b = s;
+    }
+    *best = b;
+    if (!X) free(x);
+}

@@ -18,6 +18,8 @@ Plain fp64 numpy, written equation by equation from PAPER.md (cited as P:<line>)
   * AdamW (decoupled weight decay)
   * gamma linear from gamma_min to gamma_max over the steps
   * rounding x = Theta(p - 1/2)  (evaluated as theta >= 0, Theta(0) = 1)
+  * K-ary / graph colouring (NEXT-4): s_K entropy, Clamp-normalise map, AdamW on P (App. B, P:613-647;
+    P:672-676; colouring energy P:745-750)
 
 Every function here is pinned by ``tests/test_oracle_definition.py`` against
 things other than itself: SPEC.md worked values, central finite differences,
@@ -319,3 +321,121 @@ def brute_force(problem, A: np.ndarray, lam: float = 2.0):
     best = E.min()
     arg = [X[:, k].astype(np.int64) for k in np.flatnonzero(np.isclose(E, best, atol=1e-9))]
     return float(best), arg
+
+
+# ======================================================= K-ary (NEXT-4)
+# Generalisation to discrete variables x_i in {0..K-1} (Appendix B): each
+# variable is relaxed to a row of K probabilities P[i, s, :] (one-hot encoding), the
+# entropy becomes s_K (Eq. after), the map is Clamp-then-normalise,
+# and the sensitive transition (Eq. 11) applies AdamW to P itself. Graph colouring
+# (P:745-750): conflicts = #{(i<j) in E : x_i = x_j}, relaxed as
+# sum_{(i<j) in E} sum_k p_ik p_jk (exact at one-hot P). Arrays are [N][S][K].
+def c_K(K: int, alpha: int) -> float:
+    """Normaliser of s_K: 1 / ((K-1) ((K-1)^(alpha-1) + 1))."""
+    return 1.0 / ((K - 1) * ((K - 1) ** (alpha - 1) + 1))
+
+
+def entropy_K(P: np.ndarray, alpha: int) -> np.ndarray:
+    """s_K per replica: sum_i 1 - c_K sum_k (K p_ik - 1)^alpha."""
+    K = P.shape[2]
+    return (1.0 - c_K(K, alpha) * ((K * P - 1.0) ** alpha).sum(axis=2)).sum(axis=0)
+
+
+def coloring_objective(A: np.ndarray, P: np.ndarray) -> np.ndarray:
+    """Relaxed conflicts per replica: sum_{(i<j) in E} sum_k p_ik p_jk = (1/2) sum_ij A_ij <p_i, p_j>."""
+    return 0.5 * np.einsum("isk,ij,jsk->s", P, A, P)
+
+
+def std_rows_K(P: np.ndarray) -> np.ndarray:
+    """Population STD over replicas of every (i, k) (Eq. 10 applied per colour column)."""
+    S = P.shape[1]
+    mu = P.sum(axis=1) / S
+    return np.sqrt(((P - mu[:, None, :]) ** 2).sum(axis=1) / S)
+
+
+def R_hat_K(A, P, gamma, alpha, comm) -> float:
+    """sum_s [l(P_s) + gamma s_K(P_s)] - S alpha_c sum_{i,k} STD_ik."""
+    return float((coloring_objective(A, P) + gamma * entropy_K(P, alpha)).sum()
+                 - P.shape[1] * comm * std_rows_K(P).sum())
+
+
+def grad_K(A, P, gamma, alpha, comm) -> np.ndarray:
+    """dR/dP [N][S][K]: (A P)_isk - gamma c_K alpha K (K p - 1)^(alpha-1) - alpha_c (p - mu_ik)/STD_ik."""
+    K, S = P.shape[2], P.shape[1]
+    obj = np.einsum("ij,jsk->isk", A, P)
+    ent = -c_K(K, alpha) * alpha * K * (K * P - 1.0) ** (alpha - 1)
+    mu = P.sum(axis=1) / S
+    sd = std_rows_K(P)
+    com = np.zeros_like(P)
+    ok = sd >= STD_FLOOR
+    d = P - mu[:, None, :]
+    com[:, :, :] = np.where(ok[:, None, :], -comm * d / np.where(ok, sd, 1.0)[:, None, :], 0.0)
+    return obj + gamma * ent + com
+
+
+def clamp_normalize(W: np.ndarray) -> np.ndarray:
+    """sigma(W_ik) = Clamp(W_ik) / sum_k' Clamp(W_ik'); a row whose clamps are all 0 maps
+    to the uniform 1/K (reading R27: the paper leaves 0/0 undefined)."""
+    K = W.shape[-1]
+    C = np.clip(W, 0.0, 1.0)
+    Z = C.sum(axis=-1, keepdims=True)
+    return np.where(Z > 0, C / np.where(Z > 0, Z, 1.0), 1.0 / K)
+
+
+def init_W_K(n: int, S_total: int, K: int, seed: int, lo: float = -0.01, hi: float = 0.01) -> np.ndarray:
+    """W_0[i][s][k] = 1/K + U(lo, hi), U from the counter hash keyed (seed, i K + k, s):
+    key = splitmix64(seed) + (i K + k) S_total + s; k24 = top 24 bits; u = lo + (hi - lo) k24 2^-24."""
+    base = _splitmix64(np.array([seed], dtype=np.uint64))[0]
+    i = np.arange(n, dtype=np.uint64)[:, None, None]
+    s = np.arange(S_total, dtype=np.uint64)[None, :, None]
+    k = np.arange(K, dtype=np.uint64)[None, None, :]
+    with np.errstate(over="ignore"):
+        key = base + (i * np.uint64(K) + k) * np.uint64(S_total) + s
+    k24 = (_splitmix64(key) >> np.uint64(40)).astype(np.float64)
+    lo64, hi64 = float(np.float32(lo)), float(np.float32(hi))
+    return 1.0 / K + (lo64 + (hi64 - lo64) * k24 * 2.0 ** -24)
+
+
+def gauss_noise_K(seed: int, t: int, n: int, S_total: int, K: int) -> np.ndarray:
+    """xi [n][S][K]: the Box-Muller draw of gauss_noise with row index i K + k of n K rows."""
+    z = gauss_noise(seed, t, n * K, S_total)          # [(i K + k)][s]
+    return z.reshape(n, K, S_total).transpose(0, 2, 1)
+
+
+def run_K(A, P0, gammas, alpha=2, comm=0.1, lr=1.0, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.01,
+          m0=None, v0=None, t0=0, temperature=0.0, seed=0):
+    """K-ary PQQA, fp64: AdamW on P with dR/dP, (+ noise), then P <- clamp_normalize(P') (Eq. 11 with
+    the K-ary map of P:672-676). P0 is the (already normalised) starting point. Returns (P, m, v)."""
+    P = np.array(P0, dtype=np.float64)
+    m = np.zeros_like(P) if m0 is None else np.array(m0, dtype=np.float64)
+    v = np.zeros_like(P) if v0 is None else np.array(v0, dtype=np.float64)
+    n, S, K = P.shape
+    for k, gamma in enumerate(gammas):
+        t = t0 + k + 1
+        g = grad_K(A, P, float(gamma), alpha, comm)
+        P, m, v = adamw_step(P, m, v, g, t, lr, beta1, beta2, eps, wd)
+        if temperature > 0.0:
+            P = P + np.sqrt(2.0 * lr * temperature) * gauss_noise_K(seed, t, n, S, K)
+        P = clamp_normalize(P)
+    return P, m, v
+
+
+def round_K(P: np.ndarray) -> np.ndarray:
+    """x_is = argmax_k p_isk, lowest k on ties."""
+    return np.argmax(P, axis=2).astype(np.int64)
+
+
+def conflicts(A: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """Per replica: #{(i<j) in E : x_i = x_j} (the colouring cost, read as minimised)."""
+    iu, ju = np.nonzero(np.triu(A, 1))
+    return (X[iu] == X[ju]).sum(axis=0).astype(np.int64)
+
+
+def brute_force_coloring(A: np.ndarray, K: int) -> int:
+    """Minimum conflicts over all K^N colourings (K^N <= 2e6)."""
+    n = A.shape[0]
+    if K ** n > 2_000_000:
+        raise ValueError("brute force too large")
+    iu, ju = np.nonzero(np.triu(A, 1))
+    X = np.array(list(itertools.product(range(K), repeat=n)), dtype=np.int64).T  # [N][K^N]
+    return int((X[iu] == X[ju]).sum(axis=0).min())
