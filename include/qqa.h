@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define QQA_ABI_VERSION 2
+#define QQA_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define QQA_API __attribute__((visibility("default")))
@@ -77,8 +77,13 @@ typedef enum {
 typedef enum {
   QQA_MIS = 0,        /* maximum independent set, l = -1^T x + lambda x^T A x / 2       */
   QQA_MAXCUT = 1,     /* max cut, l = -sum_{(i,j) in E} (1 - (2x_i-1)(2x_j-1))/2       */
-  QQA_MAXCLIQUE = 2   /* max clique, solved as MIS on the complement graph (the library
+  QQA_MAXCLIQUE = 2,  /* max clique, solved as MIS on the complement graph (the library
                          builds the complement on the host at create; n <= 65536)                */
+  QQA_COLORING = 3    /* graph colouring with K = n_colors colours (NEXT-4, App. B):
+                         every variable is a row of K probabilities, s_K entropy, map
+                         Clamp-then-normalise, AdamW on the probabilities,
+                         x = argmax_k, energy = #{(i<j) in E : x_i = x_j}. The
+                         map field is ignored; state arrays are [n][S_local][K]; no batches */
 } qqa_problem;
 
 /* Hyper-parameters and the replica shard of this process. Copied at create. */
@@ -98,6 +103,7 @@ typedef struct {
   float temperature;      /* Langevin T >= 0 (0.001); 0 = no noise. xi ~ N(0,1) is a
                              counter-based Box-Muller draw keyed (seed, Adam step, variable,
                              global replica): identical for every sharding               */
+  int32_t n_colors;       /* K, 2..16, for QQA_COLORING (ignored otherwise)                 */
 } qqa_config;
 
 /* Undirected simple graph as symmetric CSR, host memory, copied at create.
@@ -121,7 +127,9 @@ typedef struct {
   int32_t n_groups;             /* 1..2^24 when group_of_row is set                        */
 } qqa_graph;
 
-/* Evaluation of one rounded replica (integer counts: bit-exact, order-free). */
+/* Evaluation of one rounded replica (integer counts: bit-exact, order-free).
+ * QQA_COLORING: size = 0, violations = conflicts #{(i<j) in E : x_i = x_j},
+ * cut = |E| - conflicts, energy = conflicts, feasible = (conflicts == 0). */
 typedef struct {
   int64_t size;           /* sum_i x_i                                                     */
   int64_t violations;     /* #{(i<j) in E' : x_i = x_j = 1}, E' = E (complement for clique) */
@@ -192,14 +200,16 @@ QQA_API int qqa_round_evaluate_groups(qqa_handle* h, int64_t* counts, double* en
 QQA_API int qqa_n_groups(qqa_handle* h, int32_t* n_groups);
 
 /* Checkpoint / inspection: host [n][S_local] float arrays, NULL to skip.
- * p = sigmoid(theta) as used by the next step; step = Adam steps taken. (sync) */
+ * p = sigmoid(theta) as used by the next step; step = Adam steps taken. (sync)
+ * QQA_COLORING: arrays are [n][S_local][K]; theta and p both receive P. */
 QQA_API int qqa_get_state(qqa_handle* h, float* theta, float* m, float* v, float* p, int64_t* step);
 /* Replica statistics of the current p: c (shift, float[n]) and the int64 sums
- * (sumD, sumD2: int64[n], already reduced over ranks). (sync) */
+ * (sumD, sumD2: int64[n], already reduced over ranks). (sync)
+ * QQA_COLORING: per (variable, colour), arrays [n][K]. */
 QQA_API int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2);
 /* Resume from a checkpoint: theta/m/v host [n][S_local]; c = shift of the
  * statistics (float[n], NULL = 1/2); step = Adam steps taken. Collective with a
- * communicator. (sync) */
+ * communicator. (sync) QQA_COLORING: theta = P, [n][S_local][K]; c [n][K] (NULL = 1/K). */
 QQA_API int qqa_set_state(qqa_handle* h, const float* theta, const float* m, const float* v,
                   const float* c, int64_t step);
 

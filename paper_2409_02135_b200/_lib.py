@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "qqa.h")
 QQA_OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "BAD_GRAPH", 3: "CUDA", 4: "COMM", 5: "NONFINITE",
           6: "UNSUPPORTED", 7: "WORKSPACE"}
-PROBLEMS = {"mis": 0, "maxcut": 1, "maxclique": 2}
+PROBLEMS = {"mis": 0, "maxcut": 1, "maxclique": 2, "coloring": 3}
 MAPS = {"sigmoid": 0, "clamp": 1}
 
 
@@ -34,7 +34,7 @@ class Config(ctypes.Structure):
                 ("init_lo", ctypes.c_float), ("init_hi", ctypes.c_float),
                 ("seed", ctypes.c_uint64),
                 ("S_total", ctypes.c_int32), ("replica_offset", ctypes.c_int32), ("S_local", ctypes.c_int32),
-                ("map", ctypes.c_int32), ("temperature", ctypes.c_float)]
+                ("map", ctypes.c_int32), ("temperature", ctypes.c_float), ("n_colors", ctypes.c_int32)]
 
 
 class Graph(ctypes.Structure):

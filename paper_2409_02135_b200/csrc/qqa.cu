@@ -52,6 +52,8 @@ struct Shape {
   int W = 0, lanes = 0, vpl = 0;
   int64_t nnz_pad = 0;         // row-padded CSR (rows rounded up to 4 entries)
   int G = 1;                   // instances of a batch (NEXT-3); 1 without group_of_row
+  bool kary = false;           // graph colouring (NEXT-4): layout [n][S_local][KP]
+  int K = 0, KP = 0, LK = 0;   // colours, padded to a multiple of 4, lanes per variable
 };
 
 struct Layout {
@@ -63,25 +65,27 @@ Layout make_layout(const Shape& s) {
   Layout L{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = up(o + std::max<size_t>(bytes, 1), kAlign); return at; };
-  const size_t ns = ((size_t)s.n + 1) * s.S_p * sizeof(float);
+  const size_t ns = s.kary ? (size_t)s.n * s.S_local * s.KP * sizeof(float)
+                           : ((size_t)s.n + 1) * s.S_p * sizeof(float);
+  const size_t nk = (size_t)s.n * (s.kary ? s.K : 1);   // statistics entries: per (variable[, colour])
   L.rowptr = take(((size_t)s.n + 1) * sizeof(int));
   L.colidx = take((size_t)s.nnz * sizeof(int));
   L.rowptr_pad = take(((size_t)s.n + 1) * sizeof(int));
   L.colidx_pad = take((size_t)s.nnz_pad * sizeof(int));
   L.gor = take((size_t)s.n * sizeof(int));
-  L.theta = take(ns);
+  L.theta = take(s.kary ? 0 : ns);   // K-ary: the parameter is P itself (p0 / p1)
   L.m = take(ns);
   L.v = take(ns);
   L.p0 = take(ns);
   L.p1 = take(ns);
-  L.c0 = take((size_t)s.n * sizeof(float));
-  L.c1 = take((size_t)s.n * sizeof(float));
-  L.ms = take((size_t)s.n * sizeof(float2));
-  L.s0 = take(2 * (size_t)s.n * sizeof(long long));
-  L.s1 = take(2 * (size_t)s.n * sizeof(long long));
-  L.s2 = take(2 * (size_t)s.n * sizeof(long long));
+  L.c0 = take(nk * sizeof(float));
+  L.c1 = take(nk * sizeof(float));
+  L.ms = take(nk * sizeof(float2));
+  L.s0 = take(2 * nk * sizeof(long long));
+  L.s1 = take(2 * nk * sizeof(long long));
+  L.s2 = take(2 * nk * sizeof(long long));
   L.flag = take(4 * sizeof(int));
-  L.X = take((size_t)s.n * s.W * sizeof(uint32_t));
+  L.X = take(s.kary ? (size_t)s.n * s.S_local : (size_t)s.n * s.W * sizeof(uint32_t));   // K-ary: uint8 colours
   L.counts = take(3 * (size_t)s.S_total * s.G * sizeof(long long));   // [S_total][G][3]
   L.tot = take(3 * (size_t)s.S_total * sizeof(long long));            // [S_total][3] summed over instances
   L.energy = take((size_t)s.S_total * sizeof(double));
@@ -99,7 +103,10 @@ int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
 
 int check_config(const qqa_config* c) {
   if (!c) return fail(QQA_ERR_INVALID_ARG, "config is NULL");
-  if (c->problem < 0 || c->problem > 2) return fail(QQA_ERR_INVALID_ARG, "problem must be 0 (MIS), 1 (Max-Cut) or 2 (max clique)");
+  if (c->problem < 0 || c->problem > 3)
+    return fail(QQA_ERR_INVALID_ARG, "problem must be 0 (MIS), 1 (Max-Cut), 2 (max clique) or 3 (colouring)");
+  if (c->problem == QQA_COLORING && (c->n_colors < 2 || c->n_colors > 16))
+    return fail(QQA_ERR_INVALID_ARG, "n_colors must be in 2..16 for QQA_COLORING");
   if (c->alpha < 2 || c->alpha > 16 || (c->alpha & 1)) return fail(QQA_ERR_INVALID_ARG, "alpha must be even, 2..16 (Eq. 7)");
   if (c->S_total < 1 || c->S_total > (1 << 20)) return fail(QQA_ERR_INVALID_ARG, "S_total must be in 1..2^20");
   if (c->S_local < 1) return fail(QQA_ERR_INVALID_ARG, "S_local must be >= 1");
@@ -172,6 +179,13 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   s.S_local = c->S_local;
   s.S_total = c->S_total;
   s.G = g->group_of_row ? g->n_groups : 1;
+  if (c->problem == QQA_COLORING) {
+    if (g->group_of_row) return fail(QQA_ERR_UNSUPPORTED, "batches (group_of_row) are not supported for colouring");
+    s.kary = true;
+    s.K = c->n_colors;
+    s.KP = (s.K + 3) / 4 * 4;
+    s.LK = std::max(4, std::min(32, next_pow2(c->S_local)));
+  }
   // Replica blocking: when one copy of p is larger than the L2
   // budget, split the replicas into blocks of SB (a power of two >= 8) so that
   // one block of p -- the gathered working set while the grid sweeps it -- fits.
@@ -179,7 +193,9 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   const double p_bytes = (double)s.n * S8 * sizeof(float);
   int SB = S8;
   const char* env = std::getenv("QQA_BLOCK_REPLICAS");
-  if (env && std::atoi(env) > 0) {
+  if (s.kary) {
+    SB = S8;  // no replica blocking in the K-ary layout
+  } else if (env && std::atoi(env) > 0) {
     SB = std::max(8, next_pow2(std::atoi(env)));
   } else if (p_bytes > kL2BlockBudget && s.n > 0) {
     SB = 8;
@@ -309,6 +325,31 @@ uint64_t mix64_host(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// ------------------------------------------------------------- K-ary kernels
+using StepKKernel = void (*)(const qqa::StepKParams);
+using InitKKernel = void (*)(const qqa::InitKParams);
+using PackKKernel = void (*)(const float*, uint8_t*, int, int, int);
+
+bool pick_kary(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp) {
+  const bool noise = (mode & qqa::kModeNoise) != 0;
+#define QQA_KCASE(KPV)                                                          \
+  if (KP == KPV) {                                                              \
+    ks = noise ? qqa::k_step_K<KPV, qqa::kModeNoise> : qqa::k_step_K<KPV, 0>;   \
+    ki = qqa::k_init_K<KPV>;                                                    \
+    kp = qqa::k_pack_K<KPV>;                                                    \
+    return true;                                                                \
+  }
+  QQA_KCASE(4) QQA_KCASE(8) QQA_KCASE(12) QQA_KCASE(16)
+#undef QQA_KCASE
+  return false;
+}
+
+// k_t of the K-ary entropy: -gamma c_K alpha K, c_K = 1/((K-1)((K-1)^(alpha-1) + 1)) (host double -> fp32)
+float kt_kary(int K, int alpha, float gamma) {
+  const double cK = 1.0 / ((double)(K - 1) * (std::pow((double)(K - 1), (double)(alpha - 1)) + 1.0));
+  return (float)(-(double)gamma * cK * (double)alpha * (double)K);
+}
+
 int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& grid) {
   int per_sm = 0;
   QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
@@ -317,7 +358,38 @@ int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& gr
   return QQA_OK;
 }
 
+int launch_init_kary(qqa_handle* h, bool use_given, const float* c_given) {
+  const Shape& s = h->s;
+  StepKKernel ks;
+  InitKKernel ki;
+  PackKKernel kp;
+  pick_kary(s.KP, step_mode(h->cfg), ks, ki, kp);
+  qqa::InitKParams P{};
+  P.p0 = h->p[0]; P.p1 = h->p[1]; P.m = h->m; P.v = h->v;
+  P.c = h->c[0]; P.sums = h->sums[0];
+  P.n = s.n; P.S = s.S_local; P.K = s.K; P.S_total = s.S_total; P.replica_offset = h->cfg.replica_offset;
+  P.base = mix64_host(h->cfg.seed);
+  P.lo = (double)h->cfg.init_lo;
+  P.hi = (double)h->cfg.init_hi;
+  P.unif = (float)(1.0 / (double)s.K);
+  P.use_given = use_given ? 1 : 0;
+  P.c_given = c_given;
+  const size_t nk = (size_t)s.n * s.K;
+  for (int b = 0; b < 3; ++b) QQA_CUDA(cudaMemsetAsync(h->sums[b], 0, 2 * nk * sizeof(long long), h->stream));
+  if (s.n > 0 && s.S_local > 0) {
+    ki<<<h->grid_init, 256, 0, h->stream>>>(P);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  if (h->comm) QQA_NCCL(ncclAllReduce(h->sums[0], h->sums[0], 2 * nk, ncclInt64, ncclSum, h->comm, h->stream));
+  h->cur = 0;
+  h->scur = 0;
+  QQA_CUDA(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
+  return QQA_OK;
+}
+
 int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
+  if (h->s.kary) return launch_init_kary(h, use_given, c_given);
   StepKernel ks;
   InitKernel ki;
   pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki);
@@ -349,9 +421,84 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   return QQA_OK;
 }
 
+int record_start(qqa_handle* h) {
+  if (!h->profiling) return QQA_OK;
+  if (h->ev_used + 2 > h->ev.size()) {
+    for (int e = 0; e < 256; ++e) {
+      cudaEvent_t x;
+      QQA_CUDA(cudaEventCreate(&x));
+      h->ev.push_back(x);
+    }
+  }
+  QQA_CUDA(cudaEventRecord(h->ev[h->ev_used], h->stream));
+  return QQA_OK;
+}
+
+int record_end(qqa_handle* h) {
+  if (!h->profiling) return QQA_OK;
+  QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
+  h->ev_used += 2;
+  h->prof_launches++;
+  return QQA_OK;
+}
+
+// K-ary step loop: k_finalize over the n K (variable, colour) statistics, then k_step_K.
+int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
+  const Shape& s = h->s;
+  const qqa_config& c = h->cfg;
+  StepKKernel ks;
+  InitKKernel ki;
+  PackKKernel kp;
+  pick_kary(s.KP, step_mode(c), ks, ki, kp);
+  const size_t nk = (size_t)s.n * s.K;
+  qqa::StepKParams P{};
+  P.rowptr = h->rowptr; P.colidx = h->colidx; P.m = h->m; P.v = h->v; P.flag = h->flag;
+  P.n = s.n; P.S = s.S_local; P.K = s.K; P.L = s.LK;
+  P.Kf = (float)s.K; P.comm = c.comm; P.alpha = c.alpha;
+  P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
+  P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
+  P.eps = c.eps;
+  P.unif = (float)(1.0 / (double)s.K);
+  P.ns = (float)std::sqrt(2.0 * (double)c.lr * (double)c.temperature);
+  P.S_total_u = (unsigned long long)s.S_total;
+  const uint64_t nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);
+  for (int64_t k = 0; k < n_steps; ++k) {
+    const int64_t t = h->step + 1;
+    // xi key of (t, i, k, global s) = nbase + ((t n + i) K + k) S_total + s
+    P.nkey = nbase + (uint64_t)t * (uint64_t)s.n * (uint64_t)s.K * (uint64_t)s.S_total + (uint64_t)c.replica_offset;
+    P.kt = kt_kary(s.K, c.alpha, gamma[k]);
+    P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
+    P.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
+    P.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
+    const int a = h->cur, b = h->cur ^ 1;
+    const int sa = h->scur, sb = (h->scur + 1) % 3;
+    P.p_cur = h->p[a]; P.p_next = h->p[b];
+    P.ms = h->ms;
+    P.sums_next = h->sums[sb];
+    if (s.n > 0) {
+      qqa::k_finalize<<<h->grid_fin, 256, 0, h->stream>>>(h->c[a], h->sums[sa], (int)nk, (double)s.S_total, h->ms,
+                                                           h->c[b]);
+      QQA_CUDA(cudaGetLastError());
+      h->launches++;
+      int st;
+      if ((st = record_start(h))) return st;
+      ks<<<h->grid_step, 256, 0, h->stream>>>(P);
+      QQA_CUDA(cudaGetLastError());
+      h->launches++;
+      if ((st = record_end(h))) return st;
+    }
+    if (h->comm) QQA_NCCL(ncclAllReduce(h->sums[sb], h->sums[sb], 2 * nk, ncclInt64, ncclSum, h->comm, h->stream));
+    h->cur = b;
+    h->scur = sb;
+    h->step = t;
+  }
+  return QQA_OK;
+}
+
 int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (n_steps < 0) return fail(QQA_ERR_INVALID_ARG, "n_steps < 0");
   if (n_steps > 0 && !gamma) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
+  if (h->s.kary) return do_steps_kary(h, gamma, n_steps);
   StepKernel ks;
   InitKernel ki;
   pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki);
@@ -388,24 +535,12 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
                                                            h->ms, h->c[b]);
       QQA_CUDA(cudaGetLastError());
       h->launches++;
-      if (h->profiling) {
-        if (h->ev_used + 2 > h->ev.size()) {
-          for (int e = 0; e < 256; ++e) {
-            cudaEvent_t x;
-            QQA_CUDA(cudaEventCreate(&x));
-            h->ev.push_back(x);
-          }
-        }
-        QQA_CUDA(cudaEventRecord(h->ev[h->ev_used], h->stream));
-      }
+      int st;
+      if ((st = record_start(h))) return st;
       ks<<<h->grid_step, 256, 0, h->stream>>>(P);
       QQA_CUDA(cudaGetLastError());
       h->launches++;
-      if (h->profiling) {
-        QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
-        h->ev_used += 2;
-        h->prof_launches++;
-      }
+      if ((st = record_end(h))) return st;
     }
     if (h->comm) {
       QQA_NCCL(ncclAllReduce(h->sums[sb], h->sums[sb], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
@@ -418,9 +553,18 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
 }
 
 // Host [n][S_local] <-> device [B][n][SB], one 2-D copy per replica block.
+// K-ary: host [n][S_local][K] <-> device [n][S_local][KP], one 2-D copy.
 int copy_blocked(qqa_handle* h, float* host, float* dev, cudaMemcpyKind dir) {
   const Shape& s = h->s;
   if (s.n == 0) return QQA_OK;
+  if (s.kary) {
+    const size_t rows = (size_t)s.n * s.S_local, hp = (size_t)s.K * sizeof(float), dp = (size_t)s.KP * sizeof(float);
+    if (dir == cudaMemcpyDeviceToHost)
+      QQA_CUDA(cudaMemcpy2DAsync(host, hp, dev, dp, hp, rows, dir, h->stream));
+    else
+      QQA_CUDA(cudaMemcpy2DAsync(dev, dp, host, hp, hp, rows, dir, h->stream));
+    return QQA_OK;
+  }
   for (int b = 0; b < s.B; ++b) {
     const int cols = std::min(s.SB, s.S_local - b * s.SB);
     if (cols <= 0) break;
@@ -559,9 +703,15 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   if (h->gor && s.n > 0)
     QQA_CUDA_C(cudaMemcpyAsync(h->gor, g->group_of_row, (size_t)s.n * sizeof(int), cudaMemcpyHostToDevice, h->stream));
   QQA_CUDA_C(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
-  // theta/m/v padding and the zero row n of both p buffers
-  for (float* buf : {h->theta, h->m, h->v, h->p[0], h->p[1]})
-    QQA_CUDA_C(cudaMemsetAsync(buf, 0, ((size_t)s.n + 1) * s.S_p * sizeof(float), h->stream));
+  // theta/m/v padding and the zero row n of both p buffers (K-ary: the colour padding)
+  if (s.kary) {
+    h->theta = nullptr;
+    for (float* buf : {h->m, h->v, h->p[0], h->p[1]})
+      QQA_CUDA_C(cudaMemsetAsync(buf, 0, (size_t)s.n * s.S_local * s.KP * sizeof(float), h->stream));
+  } else {
+    for (float* buf : {h->theta, h->m, h->v, h->p[0], h->p[1]})
+      QQA_CUDA_C(cudaMemsetAsync(buf, 0, ((size_t)s.n + 1) * s.S_p * sizeof(float), h->stream));
+  }
   if (cfg->problem != QQA_MAXCLIQUE && s.n > 0 && s.nnz > 0) {
     const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
     qqa::k_validate<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, s.n, h->gor, h->flag);
@@ -593,13 +743,24 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     }
     QQA_CUDA_C(cudaStreamSynchronize(h->stream));  // rp_pad is pageable host memory
   }
-  StepKernel ks;
-  InitKernel ki;
-  if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki))
-    return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
-  if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
-  h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
-  if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
+  if (s.kary) {
+    StepKKernel ks;
+    InitKKernel ki;
+    PackKKernel kp;
+    if (!pick_kary(s.KP, step_mode(*cfg), ks, ki, kp)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no K-ary kernel"));
+    if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.LK, h->grid_step))) return cleanup(st);
+    if ((st = grid_for((const void*)ki, h->sm_count, (int64_t)s.n * s.S_local, 1, h->grid_init))) return cleanup(st);
+    const int64_t nk = (int64_t)s.n * s.K;
+    h->grid_fin = (int)std::max<int64_t>(1, std::min<int64_t>((nk + 255) / 256, (int64_t)h->sm_count * 8));
+  } else {
+    StepKernel ks;
+    InitKernel ki;
+    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki))
+      return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
+    if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
+    h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
+    if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
+  }
   if ((st = launch_init(h, false, nullptr))) return cleanup(st);
   QQA_CUDA_C(cudaStreamSynchronize(h->stream));
 #undef QQA_CUDA_C
@@ -673,7 +834,64 @@ namespace {
 
 // K3-K5 on the device: round + pack, per-(replica, instance) counts, all-gather of
 // the counts over ranks, energies + argmin of the totals and of every instance.
+int evaluate_core_kary(qqa_handle* h) {
+  const Shape& s = h->s;
+  const int off = h->cfg.replica_offset;
+  StepKKernel ks;
+  InitKKernel ki;
+  PackKKernel kp;
+  pick_kary(s.KP, step_mode(h->cfg), ks, ki, kp);
+  uint8_t* X8 = (uint8_t*)h->X;
+  const int64_t ns = (int64_t)s.n * s.S_local;
+  if (ns > 0) {  // K3: x = argmax_k P
+    kp<<<(int)std::max<int64_t>(1, std::min<int64_t>((ns + 255) / 256, (int64_t)h->sm_count * 16)), 256, 0,
+         h->stream>>>(h->p[h->cur], X8, s.n, s.S_local, s.K);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  QQA_CUDA(cudaMemsetAsync(h->counts, 0, 3 * (size_t)s.S_total * sizeof(long long), h->stream));
+  unsigned long long* mine = h->counts + 3 * (size_t)off;
+  if (s.n > 0) {  // K4: conflicts per replica
+    const int W = (s.S_local + 31) / 32;
+    const int R = (int)std::max<int64_t>(1, std::min<int64_t>(s.n, (int64_t)h->sm_count * 64 / W));
+    const int CH = (s.n + R - 1) / R;
+    const int64_t warps = (int64_t)W * R;
+    qqa::k_eval_K<<<(int)((warps + 7) / 8), 256, 0, h->stream>>>(h->rowptr, h->colidx, X8, s.n, s.S_local, W, R,
+                                                                  CH, mine);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  qqa::k_conflicts_finish<<<1, 256, 0, h->stream>>>((long long*)mine, s.S_local, (long long)(s.nnz / 2));
+  QQA_CUDA(cudaGetLastError());
+  h->launches++;
+  if (h->comm && h->nranks > 1)
+    QQA_NCCL(ncclAllGather(mine, h->counts, 3 * (size_t)s.S_local, ncclInt64, h->comm, h->stream));
+  qqa::k_argmin<<<1, 1024, 0, h->stream>>>((const long long*)h->counts, 3, s.S_total, qqa::kCOLORING, 0.0,
+                                           h->energy, h->best, h->beste);
+  QQA_CUDA(cudaGetLastError());
+  h->launches++;
+  QQA_CUDA(cudaMemcpyAsync(h->genergy, h->energy, (size_t)s.S_total * sizeof(double), cudaMemcpyDeviceToDevice,
+                           h->stream));
+  QQA_CUDA(cudaMemcpyAsync(h->gbest, h->best, sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+  QQA_CUDA(cudaMemcpyAsync(h->gbeste, h->beste, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  return QQA_OK;
+}
+
+// Best replica's x as bytes into xbuf (K-ary: its colours), on the owner rank.
+int extract_x(qqa_handle* h, int s_local) {
+  const Shape& s = h->s;
+  const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 4));
+  if (s.kary)
+    qqa::k_extract_K<<<blocks, 256, 0, h->stream>>>((const uint8_t*)h->X, s.n, s.S_local, s_local, h->xbuf);
+  else
+    qqa::k_extract<<<blocks, 256, 0, h->stream>>>(h->X, s.n, s.W, s_local, h->xbuf);
+  QQA_CUDA(cudaGetLastError());
+  h->launches++;
+  return QQA_OK;
+}
+
 int evaluate_core(qqa_handle* h) {
+  if (h->s.kary) return evaluate_core_kary(h);
   const Shape& s = h->s;
   const int off = h->cfg.replica_offset;
   if (s.n > 0) {  // K3: round + pack
@@ -770,10 +988,7 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
   if (best_x && s.n > 0) {
     const int owner = best / s.S_local;
     if (!h->comm || h->nranks == 1 || owner == h->rank) {
-      qqa::k_extract<<<std::max(1, std::min((s.n + 255) / 256, h->sm_count * 4)), 256, 0, h->stream>>>(
-          h->X, s.n, s.W, best - off, h->xbuf);
-      QQA_CUDA(cudaGetLastError());
-      h->launches++;
+      if ((st = extract_x(h, best - off))) return st;
     }
     if (h->comm && h->nranks > 1) {
       QQA_NCCL(ncclBroadcast(h->xbuf, h->xbuf, (size_t)s.n, ncclUint8, owner, h->comm, h->stream));
@@ -788,7 +1003,7 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
       r.violations = cnt[3 * k + 1];
       r.cut = cnt[3 * k + 2];
       r.energy = en[k];
-      r.feasible = (h->cfg.problem == QQA_MAXCUT) ? 1 : (r.violations == 0);
+      r.feasible = (h->cfg.problem == QQA_MAXCUT) ? 1 : (r.violations == 0);   // colouring: proper
       r.replica = off + k;
     }
   }
@@ -838,10 +1053,7 @@ int qqa_round_evaluate_groups(qqa_handle* h, int64_t* counts, double* energy, in
       QQA_CUDA(cudaStreamSynchronize(h->stream));
       const int owner = best / s.S_local;
       if (!h->comm || h->nranks == 1 || owner == h->rank) {
-        qqa::k_extract<<<std::max(1, std::min((s.n + 255) / 256, h->sm_count * 4)), 256, 0, h->stream>>>(
-            h->X, s.n, s.W, best - off, h->xbuf);
-        QQA_CUDA(cudaGetLastError());
-        h->launches++;
+        if ((st = extract_x(h, best - off))) return st;
       }
       if (h->comm && h->nranks > 1)
         QQA_NCCL(ncclBroadcast(h->xbuf, h->xbuf, (size_t)s.n, ncclUint8, owner, h->comm, h->stream));
@@ -861,7 +1073,8 @@ int qqa_get_state(qqa_handle* h, float* theta, float* m, float* v, float* p, int
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   int st = set_device(h);
   if (st) return st;
-  const float* src[4] = {h->theta, h->m, h->v, h->p[h->cur]};
+  // K-ary: the parameter is P itself, so theta and p both receive P
+  const float* src[4] = {h->s.kary ? h->p[h->cur] : h->theta, h->m, h->v, h->p[h->cur]};
   float* dst[4] = {theta, m, v, p};
   for (int k = 0; k < 4; ++k)
     if (dst[k] && (st = copy_blocked(h, dst[k], const_cast<float*>(src[k]), cudaMemcpyDeviceToHost))) return st;
@@ -874,7 +1087,7 @@ int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2) {
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   int st = set_device(h);
   if (st) return st;
-  const size_t n = (size_t)h->s.n;
+  const size_t n = (size_t)h->s.n * (h->s.kary ? h->s.K : 1);   // statistics entries
   if (c && n) QQA_CUDA(cudaMemcpyAsync(c, h->c[h->cur], n * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
   if (sumD && n)
     QQA_CUDA(cudaMemcpyAsync(sumD, h->sums[h->scur], n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
@@ -890,15 +1103,18 @@ int qqa_set_state(qqa_handle* h, const float* theta, const float* m, const float
   int st = set_device(h);
   if (st) return st;
   const Shape& s = h->s;
-  for (float* buf : {h->theta, h->m, h->v})
-    QQA_CUDA(cudaMemsetAsync(buf, 0, ((size_t)s.n + 1) * s.S_p * sizeof(float), h->stream));
+  float* param = s.kary ? h->p[0] : h->theta;   // K-ary: the parameter is P (launch_init copies it to p[1])
+  const size_t bytes = s.kary ? (size_t)s.n * s.S_local * s.KP * sizeof(float)
+                              : ((size_t)s.n + 1) * s.S_p * sizeof(float);
+  for (float* buf : {param, h->m, h->v}) QQA_CUDA(cudaMemsetAsync(buf, 0, bytes, h->stream));
   const float* src[3] = {theta, m, v};
-  float* dst[3] = {h->theta, h->m, h->v};
+  float* dst[3] = {param, h->m, h->v};
   for (int k = 0; k < 3; ++k)
     if ((st = copy_blocked(h, const_cast<float*>(src[k]), dst[k], cudaMemcpyHostToDevice))) return st;
   const float* cdev = nullptr;
+  const size_t nk = (size_t)s.n * (s.kary ? s.K : 1);
   if (c && s.n > 0) {
-    QQA_CUDA(cudaMemcpyAsync(h->c[1], c, (size_t)s.n * sizeof(float), cudaMemcpyHostToDevice, h->stream));
+    QQA_CUDA(cudaMemcpyAsync(h->c[1], c, nk * sizeof(float), cudaMemcpyHostToDevice, h->stream));
     cdev = h->c[1];
   }
   if ((st = launch_init(h, true, cdev))) return st;

@@ -34,7 +34,7 @@
 
 namespace qqa {
 
-enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2 };
+enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2, kCOLORING = 3 };
 // Step-kernel mode (template): bit 0 = clamp map (Eq. 11),
 // bit 1 = Langevin noise (Eq. 9 / 11).
 enum : int { kModeClamp = 1, kModeNoise = 2 };
@@ -611,9 +611,9 @@ __global__ void k_argmin(const long long* __restrict__ counts, int stride, int S
   int bi = -1;
   for (int s = threadIdx.x; s < S_total; s += blockDim.x) {
     const long long* c = counts + (size_t)s * stride;
-    const double e = (problem == kMAXCUT)
-                         ? -(double)c[2]
-                         : __dadd_rn(-(double)c[0], __dmul_rn(lam, (double)c[1]));
+    const double e = (problem == kMAXCUT)     ? -(double)c[2]
+                     : (problem == kCOLORING) ? (double)c[1]                  // conflicts
+                                              : __dadd_rn(-(double)c[0], __dmul_rn(lam, (double)c[1]));
     energy[s] = e;
     if (bi < 0 || e < be) { be = e; bi = s; }
   }
@@ -653,6 +653,245 @@ __global__ void k_extract_groups(const uint32_t* __restrict__ X, const int* __re
     const int s = best[gor[i]] - off;
     out[i] = (s >= 0 && s < S_local) ? (uint8_t)((X[(size_t)i * W + (s >> 5)] >> (s & 31)) & 1u) : (uint8_t)0;
   }
+}
+
+// ======================================================== K-ary (NEXT-4)
+// Graph colouring with K <= KP colours (App. B, map P:672-676, energy
+// P:745-750). Layout: P[2] (ping-pong), m, v float [n][S][KP] -- replica s of
+// variable i is KP contiguous floats (the K colour probabilities, padding = 0);
+// statistics per (i, k): c / ms [n][K], sums int64 [2][n K]. One thread owns a
+// (variable, replica) pair with all its colours in registers; a group of L lanes
+// (L = min(32, pow2 >= S)) covers the replicas of one variable (replica r =
+// lane + L v). The parameter is P itself: AdamW with dR/dP, (+ noise), then
+// P = Clamp(P') / sum_k Clamp(P'_k) (uniform 1/K if every clamp is 0).
+struct StepKParams {
+  const int* __restrict__ rowptr;
+  const int* __restrict__ colidx;
+  const float* __restrict__ p_cur;      // [n][S][KP]
+  float* __restrict__ p_next;
+  float* __restrict__ m;
+  float* __restrict__ v;
+  const float2* __restrict__ ms;        // [n][K] (mu, STD) of the current P
+  long long* __restrict__ sums_next;    // [2][n K]
+  int* __restrict__ flag;
+  int n, S, K, L;
+  float Kf, comm, b1, c1, b2, c2, eps, unif;   // unif = (float)(1/K)
+  int alpha;
+  float kt, at, st, rt, ns;
+  unsigned long long nkey;              // nbase + t n K S_total + replica_offset
+  unsigned long long S_total_u;
+};
+
+template <int KP>
+__device__ __forceinline__ void ld_colours(const float* ptr, float (&x)[KP]) {
+#pragma unroll
+  for (int k = 0; k < KP; k += 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(ptr + k));
+    x[k] = t.x; x[k + 1] = t.y; x[k + 2] = t.z; x[k + 3] = t.w;
+  }
+}
+template <int KP>
+__device__ __forceinline__ void st_colours(float* ptr, const float (&x)[KP]) {
+#pragma unroll
+  for (int k = 0; k < KP; k += 4) *reinterpret_cast<float4*>(ptr + k) = make_float4(x[k], x[k + 1], x[k + 2], x[k + 3]);
+}
+
+// P = Clamp(w) / Z, Z = ((c_0 + c_1) + c_2) + ... (K colours; padding stays 0).
+template <int KP>
+__device__ __forceinline__ void normalize_colours(float (&w)[KP], int K, float unif) {
+  float Z = 0.0f;
+#pragma unroll
+  for (int k = 0; k < KP; ++k)
+    if (k < K) Z = fadd(Z, clamp01(w[k]));
+#pragma unroll
+  for (int k = 0; k < KP; ++k) w[k] = (k < K) ? ((Z > 0.0f) ? fdiv(clamp01(w[k]), Z) : unif) : 0.0f;
+}
+
+template <int KP, int MODE>
+__global__ void __launch_bounds__(256) k_step_K(const StepKParams P) {
+  __shared__ unsigned long long red[256 / 4][2][KP];   // per group (L >= 4 lanes) and colour: sum D, sum D2
+  const int L = P.L;                                   // power of two in [4, 32]: a group lies in one warp
+  const int lane = threadIdx.x & (L - 1);
+  const int gl = threadIdx.x / L;                      // group within the CTA
+  const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
+  const int groups_cta = blockDim.x / L;
+  const int vpl = (P.S + L - 1) / L;
+  bool bad = false;
+  for (int i = blockIdx.x * groups_cta + gl; i < P.n; i += gridDim.x * groups_cta) {
+    for (int k = lane; k < KP; k += L) { red[gl][0][k] = 0ull; red[gl][1][k] = 0ull; }
+    __syncwarp(gmask);
+    const int e0 = __ldg(P.rowptr + i), e1 = __ldg(P.rowptr + i + 1);
+    const unsigned long long rkey = P.nkey + (unsigned long long)i * (unsigned long long)P.K * P.S_total_u;
+    for (int vv = 0; vv < vpl; ++vv) {
+      const int r = lane + vv * L;
+      if (r >= P.S) break;
+      // q_k = sum_{j in N(i)} p_j[r][k], CSR order
+      float q[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) q[k] = 0.0f;
+      for (int e = e0; e < e1; ++e) {
+        const int j = __ldg(P.colidx + e);
+        float pj[KP];
+        ld_colours<KP>(P.p_cur + ((size_t)j * P.S + r) * KP, pj);
+#pragma unroll
+        for (int k = 0; k < KP; ++k) q[k] = fadd(q[k], pj[k]);
+      }
+      const size_t at = ((size_t)i * P.S + r) * KP;
+      float w[KP], mm[KP], vv2[KP];
+      ld_colours<KP>(P.p_cur + at, w);
+      ld_colours<KP>(P.m + at, mm);
+      ld_colours<KP>(P.v + at, vv2);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        if (k >= P.K) continue;
+        const float pi = w[k];
+        const float2 st = P.ms[(size_t)i * P.K + k];
+        const float e = fsub(fmul(P.Kf, pi), 1.0f);
+        float ep = e;
+        for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);            // (K p - 1)^(alpha-1)
+        const float ent = fmul(P.kt, ep);
+        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
+        const float g = fadd(fadd(q[k], ent), com);
+        const float t1 = fmul(pi, P.at);
+        mm[k] = fadd(fmul(P.b1, mm[k]), fmul(P.c1, g));
+        vv2[k] = fadd(fmul(P.b2, vv2[k]), fmul(fmul(P.c2, g), g));
+        const float den = fadd(fmul(__fsqrt_rn(vv2[k]), P.rt), P.eps);
+        float x = fsub(t1, fmul(P.st, fdiv(mm[k], den)));
+        if (MODE & kModeNoise)
+          x = fadd(x, fmul(P.ns, gauss_c(mix64(rkey + (unsigned long long)k * P.S_total_u + (unsigned long long)r))));
+        bad |= !isfinite(x);
+        w[k] = x;
+      }
+      normalize_colours<KP>(w, P.K, P.unif);
+      st_colours<KP>(P.m + at, mm);
+      st_colours<KP>(P.v + at, vv2);
+      st_colours<KP>(P.p_next + at, w);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        if (k >= P.K) continue;
+        long long D, D2;
+        stat_terms(w[k], P.ms[(size_t)i * P.K + k].x, D, D2);
+        atomicAdd(&red[gl][0][k], (unsigned long long)D);
+        atomicAdd(&red[gl][1][k], (unsigned long long)D2);
+      }
+    }
+    __syncwarp(gmask);
+    for (int k = lane; k < P.K; k += L) {
+      const size_t ik = (size_t)i * P.K + k;
+      P.sums_next[ik] = (long long)red[gl][0][k];
+      P.sums_next[(size_t)P.n * P.K + ik] = (long long)red[gl][1][k];
+    }
+    __syncwarp(gmask);
+  }
+  if (bad) atomicOr(P.flag, 1);
+}
+
+// K1 for K-ary: W_0 = 1/K + U(lo, hi) keyed (seed, i K + k, global s), P_0 = normalise(W_0),
+// m = v = 0; or (use_given) P_0 as given. Sums of P_0 with shift c (1/K or c_given), u64 atomics.
+struct InitKParams {
+  float* p0; float* p1; float* m; float* v;
+  float* c; long long* sums;            // c[n K], sums[2][n K] (zero on entry)
+  int n, S, K, S_total, replica_offset;
+  uint64_t base;
+  double lo, hi;
+  float unif;
+  int use_given;
+  const float* c_given;
+};
+
+template <int KP>
+__global__ void __launch_bounds__(256) k_init_K(const InitKParams P) {
+  const long long total = (long long)P.n * P.S;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < total;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(it / P.S), r = (int)(it % P.S);
+    const size_t at = (size_t)it * KP;
+    float w[KP];
+    if (P.use_given) {
+      ld_colours<KP>(P.p0 + at, w);
+    } else {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        w[k] = 0.0f;
+        if (k < P.K) {
+          const uint64_t key = P.base + ((uint64_t)i * (uint64_t)P.K + (uint64_t)k) * (uint64_t)P.S_total +
+                               (uint64_t)(P.replica_offset + r);
+          const uint64_t kk = mix64(key) >> 40;
+          const double u = __dadd_rn(P.lo, __dmul_rn(__dmul_rn(__dsub_rn(P.hi, P.lo), (double)kk), 0x1p-24));
+          w[k] = __double2float_rn(__dadd_rn(__ddiv_rn(1.0, (double)P.K), u));
+        }
+      }
+      normalize_colours<KP>(w, P.K, P.unif);
+      float z[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) z[k] = 0.0f;
+      st_colours<KP>(P.p0 + at, w);
+      st_colours<KP>(P.m + at, z);
+      st_colours<KP>(P.v + at, z);
+    }
+    st_colours<KP>(P.p1 + at, w);
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      if (k >= P.K) continue;
+      const size_t ik = (size_t)i * P.K + k;
+      const float ci = P.c_given ? P.c_given[ik] : P.unif;
+      long long D, D2;
+      stat_terms(w[k], ci, D, D2);
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.sums + ik), (unsigned long long)D);
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.sums + (size_t)P.n * P.K + ik), (unsigned long long)D2);
+      if (r == 0) P.c[ik] = ci;
+    }
+  }
+}
+
+// K3 for K-ary: X8[i][s] = argmax_k P[i][s][k] (lowest k on ties).
+template <int KP>
+__global__ void k_pack_K(const float* __restrict__ Pm, uint8_t* __restrict__ X8, int n, int S, int K) {
+  const long long total = (long long)n * S;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < total;
+       it += (long long)gridDim.x * blockDim.x) {
+    float w[KP];
+    ld_colours<KP>(Pm + (size_t)it * KP, w);
+    int b = 0;
+#pragma unroll
+    for (int k = 1; k < KP; ++k)
+      if (k < K && w[k] > w[b]) b = k;
+    X8[it] = (uint8_t)b;
+  }
+}
+
+// K4 for K-ary: conflicts per replica; lane = replica 32 w + lane, warp k takes word k % W and the
+// row chunk [c CH, (c+1) CH), c = k / W. counts[s][3] = (0, conflicts, |E| - conflicts) (the last
+// term is added by the host-known |E| in k_conflicts_finish).
+__global__ void k_eval_K(const int* __restrict__ rowptr, const int* __restrict__ colidx,
+                         const uint8_t* __restrict__ X8, int n, int S, int W, int R, int CH,
+                         unsigned long long* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= W * R) return;
+  const int s = (warp % W) * 32 + lane;
+  if (s >= S) return;
+  const int i0 = (warp / W) * CH, i1 = min(n, i0 + CH);
+  unsigned long long conf = 0;
+  for (int i = i0; i < i1; ++i) {
+    const uint8_t xi = X8[(size_t)i * S + s];
+    const int e1 = rowptr[i + 1];
+    for (int e = rowptr[i]; e < e1; ++e) {
+      const int j = colidx[e];
+      if (j > i) conf += (X8[(size_t)j * S + s] == xi);
+    }
+  }
+  if (conf) atomicAdd(counts + 3 * (size_t)s + 1, conf);
+}
+
+__global__ void k_conflicts_finish(long long* __restrict__ counts, int S, long long n_edges) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
+    counts[3 * s + 2] = n_edges - counts[3 * s + 1];
+}
+
+__global__ void k_extract_K(const uint8_t* __restrict__ X8, int n, int S, int s_local, uint8_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = X8[(size_t)i * S + s_local];
 }
 
 }  // namespace qqa

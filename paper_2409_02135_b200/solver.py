@@ -15,7 +15,8 @@ from . import _lib
 from ._lib import Config, Graph, ReplicaResult, check, lib
 
 DEFAULTS = dict(alpha=2, penalty=2.0, comm=0.1, lr=1.0, beta1=0.9, beta2=0.999, eps=1e-8,
-                weight_decay=0.01, init_lo=-0.01, init_hi=0.01, map="sigmoid", temperature=0.0)
+                weight_decay=0.01, init_lo=-0.01, init_hi=0.01, map="sigmoid", temperature=0.0,
+                n_colors=0)
 
 
 def make_config(problem="mis", S_total=16, seed=1, replica_offset=0, S_local=None, **hp) -> Config:
@@ -26,7 +27,7 @@ def make_config(problem="mis", S_total=16, seed=1, replica_offset=0, S_local=Non
     return Config(pid, int(kw["alpha"]), kw["penalty"], kw["comm"], kw["lr"], kw["beta1"], kw["beta2"],
                   kw["eps"], kw["weight_decay"], kw["init_lo"], kw["init_hi"], seed & 0xFFFFFFFFFFFFFFFF,
                   int(S_total), int(replica_offset), int(S_total if S_local is None else S_local),
-                  mid, float(kw["temperature"]))
+                  mid, float(kw["temperature"]), int(kw["n_colors"]))
 
 
 def _as_graph(rowptr: np.ndarray, colidx: np.ndarray, group_of_row: np.ndarray | None = None,
@@ -83,6 +84,7 @@ class Solver:
         self.colidx = np.ascontiguousarray(colidx, np.int32)
         self.n = len(self.rowptr) - 1
         self.S_local = cfg.S_local
+        self.K = int(cfg.n_colors) if cfg.problem == _lib.PROBLEMS["coloring"] else 0   # NEXT-4
         self.group_of_row = None if group_of_row is None else np.ascontiguousarray(group_of_row, np.int32)
         g = _as_graph(self.rowptr, self.colidx, self.group_of_row, n_groups)
         nbytes = ctypes.c_size_t(0)
@@ -142,8 +144,15 @@ class Solver:
         return GroupResult(best, be, x, cnt, en)
 
     # --------------------------------------------------------------- state
+    def _shape(self):
+        return (self.n, self.S_local, self.K) if self.K else (self.n, self.S_local)
+
+    def _stat_shape(self):
+        return (self.n, self.K) if self.K else (self.n,)
+
     def get_state(self):
-        shp = (self.n, self.S_local)
+        """theta / m / v / p as host arrays [n][S_local] (colouring: [n][S_local][K], theta = p = P)."""
+        shp = self._shape()
         th, m, v, p = (np.empty(shp, np.float32) for _ in range(4))
         step = ctypes.c_int64(0)
         check(lib.qqa_get_state(self._h, th.ctypes.data, m.ctypes.data, v.ctypes.data, p.ctypes.data,
@@ -151,9 +160,9 @@ class Solver:
         return dict(theta=th, m=m, v=v, p=p, step=int(step.value))
 
     def get_stats(self):
-        c = np.empty(self.n, np.float32)
-        a = np.empty(self.n, np.int64)
-        b = np.empty(self.n, np.int64)
+        c = np.empty(self._stat_shape(), np.float32)
+        a = np.empty(self._stat_shape(), np.int64)
+        b = np.empty(self._stat_shape(), np.int64)
         check(lib.qqa_get_stats(self._h, c.ctypes.data, a.ctypes.data, b.ctypes.data))
         return dict(c=c, sumD=a, sumD2=b)
 

@@ -1,0 +1,128 @@
+"""GPU parity for NEXT-4 (K-ary PQQA / graph colouring, App. B, map P:672-676,
+energy P:745-750) through the C ABI, against the fp32 contract oracle: P, m, v and the
+per-(variable, colour) statistics bit-identical; colours, conflicts, energies and the
+best replica bit-exact."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def Q():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2409_02135_b200 as Q
+    return Q
+
+
+def gpu(Q, g, K, S, seed, S_total=None, offset=0, **hp):
+    cfg = Q.make_config("coloring", S_total=S if S_total is None else S_total, seed=seed, replica_offset=offset,
+                        S_local=S, n_colors=K, **hp)
+    return Q.Solver(g.rowptr, g.colidx, cfg)
+
+
+def ocfg(S, seed, **hp):
+    return oracle.make_cfg("mis", S=S, seed=seed, threads=8, **hp)
+
+
+def assert_equal_K(sol, st):
+    gs = sol.get_state()
+    for f, ref in (("p", st.P), ("theta", st.P), ("m", st.m), ("v", st.v)):
+        bad = np.count_nonzero(gs[f].view(np.uint32) != ref.view(np.uint32))
+        assert bad == 0, f"{f}: {bad} of {ref.size} differ (max |d| = {np.abs(gs[f] - ref).max()})"
+    ss = sol.get_stats()
+    assert np.array_equal(ss["c"].view(np.uint32), st.c.view(np.uint32))
+    assert np.array_equal(ss["sumD"], st.sumD) and np.array_equal(ss["sumD2"], st.sumD2)
+
+
+@pytest.mark.parametrize("K", [2, 3, 5, 9, 13, 16])
+@pytest.mark.parametrize("S", [1, 7, 32, 100])
+def test_init_parity(Q, K, S):
+    g = gen.queens(5, 5)
+    sol = gpu(Q, g, K, S, 17)
+    assert_equal_K(sol, oracle.init_K(g, ocfg(S, 17), K))
+
+
+CASES = [
+    # (graph, K, S, hyper-parameters)
+    (lambda: gen.queens(5, 5), 5, 16, dict(lr=0.1)),
+    (lambda: gen.mycielski(5), 6, 100, dict(lr=0.1)),
+    (lambda: gen.erdos_renyi(300, 0.03, 6), 3, 64, dict(lr=0.1, temperature=0.001, comm=0.3)),
+    (lambda: gen.queens(8, 8), 9, 33, dict(lr=0.1, comm=0.3, alpha=4)),
+    (lambda: gen.random_regular(500, 8, 2), 16, 8, dict(lr=0.03)),
+    (lambda: gen.grid(10, 12), 2, 40, dict(lr=0.1, temperature=0.01)),
+    (lambda: gen.erdos_renyi(200, 0.05, 9), 4, 1, dict(lr=0.1)),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_fifty_steps_parity(Q, case):
+    mk, K, S, hp = CASES[case]
+    g = mk()
+    gam = oracle.schedule(-2.0, 0.1, 1000)[:50]
+    sol = gpu(Q, g, K, S, 11, **hp)
+    sol.run(gam)
+    st = oracle.run_K(g, ocfg(S, 11, **hp), K, gam)
+    assert_equal_K(sol, st)
+
+
+@pytest.mark.parametrize("name,K", [("queen5-5", 5), ("myciel5", 6)])
+def test_full_schedule_with_evaluation(Q, name, K):
+    """3000 steps at S=100 (the oracle finds a proper colouring for both, Table 4 reports 0 conflicts):
+    state, colours, conflicts and the best replica bit-exact; best replica conflict-free."""
+    g = gen.queens(5, 5) if name == "queen5-5" else gen.mycielski(5)
+    sol = gpu(Q, g, K, 100, 1, lr=0.1)
+    sol.run_linear(-2.0, 0.1, 3000)
+    st = oracle.run_K(g, ocfg(100, 1, lr=0.1), K, oracle.schedule(-2.0, 0.1, 3000))
+    assert_equal_K(sol, st)
+    counts, energy, best, X = oracle.evaluate_K(g, st.P)
+    res = sol.round_evaluate()
+    pr = res.per_replica
+    assert np.array_equal(pr["violations"], counts[:, 1]) and np.array_equal(pr["cut"], counts[:, 2])
+    assert np.array_equal(pr["energy"], energy) and res.best_replica == best
+    assert np.array_equal(res.best_x, X[:, best]) and res.best_energy == 0
+    assert pr["feasible"][best] == 1
+
+
+def test_checkpoint_resume(Q):
+    g = gen.queens(6, 6)
+    gam = oracle.schedule(-2.0, 0.1, 200)
+    a = gpu(Q, g, 7, 24, 5, lr=0.1, temperature=0.001)
+    a.run(gam[:30])
+    ck, cs = a.get_state(), a.get_stats()
+    a.run(gam[30:60])
+    b = gpu(Q, g, 7, 24, 5, lr=0.1, temperature=0.001)   # same seed: the noise stream is keyed by it
+    b.set_state(ck["theta"], ck["m"], ck["v"], ck["step"], c=cs["c"])
+    assert np.array_equal(b.get_stats()["sumD"], cs["sumD"])
+    b.run(gam[30:60])
+    for f in ("p", "m", "v"):
+        assert np.array_equal(a.get_state()[f], b.get_state()[f])
+
+
+def test_shard_is_column_slice_without_comm(Q):
+    g = gen.queens(5, 5)
+    gam = oracle.schedule(-2.0, 0.1, 100)[:40]
+    full = gpu(Q, g, 5, 64, 3, comm=0.0, lr=0.1, temperature=0.01)
+    full.run(gam)
+    fs = full.get_state()
+    for off, S in [(0, 32), (32, 32), (8, 8)]:
+        sh = gpu(Q, g, 5, S, 3, S_total=64, offset=off, comm=0.0, lr=0.1, temperature=0.01)
+        sh.run(gam)
+        assert np.array_equal(sh.get_state()["p"], fs["p"][:, off:off + S])
+
+
+def test_invalid_colouring_configs(Q):
+    g = gen.queens(4, 4)
+    for K in (0, 1, 17):
+        with pytest.raises(Q.QQAError) as e:
+            gpu(Q, g, K, 8, 1)
+        assert e.value.status == 1
+    U, gor = gen.disjoint_union([g, g])
+    with pytest.raises(Q.QQAError) as e:
+        Q.Solver(U.rowptr, U.colidx, Q.make_config("coloring", S_total=8, n_colors=4), group_of_row=gor)
+    assert e.value.status == 6
