@@ -38,10 +38,11 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
-def algorithmic_bytes(n: int, nnz: int, S_local: int) -> int:
+def algorithmic_bytes(n: int, nnz: int, S_local: int, K: int = 1) -> int:
     """BASELINE.json north_star byte model per step and GPU:
-    CSR indices (4 nnz + 4 (n+1)) + gathered neighbour values (4 nnz S_l) + theta/m/v read+write (24 n S_l)."""
-    return 4 * nnz + 4 * (n + 1) + 4 * nnz * S_local + 24 * n * S_local
+    CSR indices (4 nnz + 4 (n+1)) + gathered neighbour values (4 nnz S_l) + theta/m/v read+write (24 n S_l).
+    K-ary (NEXT-4): every replica-variable carries K colour columns, so S_l -> S_l K."""
+    return 4 * nnz + 4 * (n + 1) + 4 * nnz * S_local * K + 24 * n * S_local * K
 
 
 def measured_peaks():
@@ -118,12 +119,18 @@ def oracle_sample(w, n_steps: int, threads: int):
     """Time the fp32 contract oracle (as it stands) for n_steps annealing steps of w."""
     import oracle
     (g, _), seed = w.batched(), w.seeds[0]
-    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
-    cfg = oracle.make_cfg(w.problem, S=w.S, seed=seed, threads=threads, **hp)
+    hp = {k: v for k, v in w.hparams().items() if k not in ("problem", "n_colors")}
     gam = oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:n_steps]
-    st = oracle.init(g, cfg)
-    t0 = time.perf_counter()
-    oracle.run(g, cfg, gam, state=st)
+    if w.n_colors:                     # K-ary (NEXT-4)
+        cfg = oracle.make_cfg("mis", S=w.S, seed=seed, threads=threads, **hp)
+        st = oracle.init_K(g, cfg, w.n_colors)
+        t0 = time.perf_counter()
+        oracle.run_K(g, cfg, w.n_colors, gam, state=st)
+    else:
+        cfg = oracle.make_cfg(w.problem, S=w.S, seed=seed, threads=threads, **hp)
+        st = oracle.init(g, cfg)
+        t0 = time.perf_counter()
+        oracle.run(g, cfg, gam, state=st)
     dt = time.perf_counter() - t0
     return g.n * w.S * n_steps / dt, dt
 
@@ -159,8 +166,13 @@ def workload_config(w, world):
     g, _ = w.batched()
     S_l = w.S // world
     state_bytes = 5 * g.n * ((S_l + 7) // 8 * 8) * 4
+    extra = {}
+    if w.map != "sigmoid" or w.temperature:
+        extra.update(map=w.map, temperature=w.temperature)
+    if w.n_colors:
+        extra.update(n_colors=w.n_colors)
     return {"workload": w.name, "problem": w.problem, "recipe": w.recipe, "N": g.n, "nnz": g.nnz, "S": w.S,
-            "S_local": S_l, "anneal_steps": w.steps, "instances": len(w.graphs),
+            "S_local": S_l, "anneal_steps": w.steps, "instances": len(w.graphs), **extra,
             "parallelism": (f"replica-sharded x{world}" if world > 1 else "single GPU")
                            + (f", {len(w.graphs)} instances batched block-diagonally in one handle"
                               if len(w.graphs) > 1 else ""),
@@ -173,7 +185,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "q13", "k8"])
+    ap.add_argument("--map", default=None, choices=["sigmoid", "clamp"],
+                    help="override the map (clamp = the paper's sensitive transition, NEXT-1)")
+    ap.add_argument("--temperature", type=float, default=None, help="Langevin T (NEXT-2; the paper: 0.001)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--anneal-steps", type=int, default=None, help="override T (diagnostics only)")
     ap.add_argument("--cpu-sample-steps", type=int, default=20)
@@ -186,6 +201,10 @@ def main():
     w = gen.workload(args.workload)
     if args.anneal_steps:
         w.steps = args.anneal_steps
+    if args.map:
+        w.map = args.map
+    if args.temperature is not None:
+        w.temperature = args.temperature
     if args.impl == "reference":
         run_reference(args, w)
         return
@@ -253,7 +272,7 @@ def main():
 
     total_updates = g.n * w.S * w.steps * args.steps
     value = total_updates / (t_ms / 1e3)
-    B = algorithmic_bytes(g.n, g.nnz, S_l)
+    B = algorithmic_bytes(g.n, g.nnz, S_l, max(1, w.n_colors))
     avg_kernel_s = kern_ms / 1e3 / max(kern_launches, 1)
     peak, peak_src = measured_peaks()
     achieved = B / avg_kernel_s / 1e9
@@ -261,7 +280,8 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(f"{w.name}_x{world}")
+            variant = ("_" + w.map if w.map != "sigmoid" else "") + ("_T" if w.temperature else "")
+            traffic = json.load(f).get(f"{w.name}{variant}_x{world}")
 
     # ------------------------------------------------------------- e2e
     e2e = None
@@ -315,7 +335,8 @@ def main():
                 "config": workload_config(w, world),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
-                             "kernel": "qqa::k_step (fused gather + gradient + AdamW + stats)",
+                             "kernel": ("qqa::k_step_K (fused K-ary gather + gradient + AdamW + normalise + stats)"
+                                        if w.n_colors else "qqa::k_step (fused gather + gradient + AdamW + stats)"),
                              "bytes_per_launch": B, "avg_launch_ms": avg_kernel_s * 1e3,
                              "launches_timed": kern_launches, "peak_source": peak_src,
                              "step_kernel_share": kern_ms / t_ms},

@@ -206,6 +206,9 @@ class Workload:
     weight_decay: float = 0.01
     init_lo: float = -0.01
     init_hi: float = 0.01
+    map: str = "sigmoid"
+    temperature: float = 0.0
+    n_colors: int = 0
     recipe: str = ""
 
     def batched(self):
@@ -216,9 +219,14 @@ class Workload:
         return disjoint_union(self.graphs)
 
     def hparams(self) -> dict:
-        return dict(problem=self.problem, alpha=self.alpha, penalty=self.penalty, comm=self.comm,
-                    lr=self.lr, beta1=self.beta1, beta2=self.beta2, eps=self.eps,
-                    weight_decay=self.weight_decay, init_lo=self.init_lo, init_hi=self.init_hi)
+        d = dict(problem=self.problem, alpha=self.alpha, penalty=self.penalty, comm=self.comm,
+                 lr=self.lr, beta1=self.beta1, beta2=self.beta2, eps=self.eps,
+                 weight_decay=self.weight_decay, init_lo=self.init_lo, init_hi=self.init_hi)
+        if self.map != "sigmoid" or self.temperature:
+            d.update(map=self.map, temperature=self.temperature)
+        if self.n_colors:
+            d.update(n_colors=self.n_colors, temperature=self.temperature)
+        return d
 
 
 def c2_sizes() -> list[int]:
@@ -251,4 +259,13 @@ def workload(name: str, n_instances: int | None = None) -> Workload:
     if name == "c5":
         return Workload("c5", "mis", [random_regular(1_000_000, 20, 5)], [5], S=64, steps=3000,
                         recipe="MIS, random 20-regular N=1,000,000 (seed 5); S=64; 3000 steps")
+    # NEXT-4 (K-ary) workloads -- not BASELINE.json configs; measurement cases of the colouring path
+    if name == "q13":
+        return Workload("q13", "coloring", [queens(13, 13)], [13], S=1000, steps=3000, lr=0.01, n_colors=13,
+                        recipe="colouring, queen13-13 (169 nodes, 3328 edges, Table 13) with K=13; S=1000; "
+                               "3000 steps; lr 0.01 (the paper's largest COLOR instance, P:447)")
+    if name == "k8":
+        return Workload("k8", "coloring", [random_regular(100_000, 20, 8)], [8], S=64, steps=3000, lr=0.01,
+                        n_colors=8, recipe="colouring, random 20-regular N=100,000 (seed 8) with K=8; S=64; "
+                                           "3000 steps; lr 0.01 (scale case of the K-ary kernel)")
     raise KeyError(name)

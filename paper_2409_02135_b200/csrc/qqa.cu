@@ -471,10 +471,11 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
     P.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
     P.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
     const int a = h->cur, b = h->cur ^ 1;
-    const int sa = h->scur, sb = (h->scur + 1) % 3;
+    const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
     P.p_cur = h->p[a]; P.p_next = h->p[b];
     P.ms = h->ms;
     P.sums_next = h->sums[sb];
+    P.sums_zero = h->sums[sz];
     if (s.n > 0) {
       qqa::k_finalize<<<h->grid_fin, 256, 0, h->stream>>>(h->c[a], h->sums[sa], (int)nk, (double)s.S_total, h->ms,
                                                            h->c[b]);
@@ -748,7 +749,8 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     InitKKernel ki;
     PackKKernel kp;
     if (!pick_kary(s.KP, step_mode(*cfg), ks, ki, kp)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no K-ary kernel"));
-    if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.LK, h->grid_step))) return cleanup(st);
+    const int64_t chunks = (s.S_local + s.LK - 1) / s.LK;   // work item = (variable, replica chunk)
+    if ((st = grid_for((const void*)ks, h->sm_count, (int64_t)s.n * chunks, s.LK, h->grid_step))) return cleanup(st);
     if ((st = grid_for((const void*)ki, h->sm_count, (int64_t)s.n * s.S_local, 1, h->grid_init))) return cleanup(st);
     const int64_t nk = (int64_t)s.n * s.K;
     h->grid_fin = (int)std::max<int64_t>(1, std::min<int64_t>((nk + 255) / 256, (int64_t)h->sm_count * 8));

@@ -672,7 +672,8 @@ struct StepKParams {
   float* __restrict__ m;
   float* __restrict__ v;
   const float2* __restrict__ ms;        // [n][K] (mu, STD) of the current P
-  long long* __restrict__ sums_next;    // [2][n K]
+  long long* __restrict__ sums_next;    // [2][n K]; zero on entry when S > L (chunk atomics)
+  long long* __restrict__ sums_zero;    // [2][n K] buffer of the step after next (zeroed here)
   int* __restrict__ flag;
   int n, S, K, L;
   float Kf, comm, b1, c1, b2, c2, eps, unif;   // unif = (float)(1/K)
@@ -707,37 +708,54 @@ __device__ __forceinline__ void normalize_colours(float (&w)[KP], int K, float u
   for (int k = 0; k < KP; ++k) w[k] = (k < K) ? ((Z > 0.0f) ? fdiv(clamp01(w[k]), Z) : unif) : 0.0f;
 }
 
+// Work item = (variable i, replica chunk c): a group of L lanes (L a power of two
+// in [4, 32], so a group lies inside one warp) takes replicas c L + lane. The
+// fixed-point sums of a chunk are reduced by shuffles within the group and, with
+// several chunks, meet in global u64 atomics (exact, order-free); chunk 0 zeroes
+// the variable's entries of the buffer used two steps later.
 template <int KP, int MODE>
 __global__ void __launch_bounds__(256) k_step_K(const StepKParams P) {
-  __shared__ unsigned long long red[256 / 4][2][KP];   // per group (L >= 4 lanes) and colour: sum D, sum D2
-  const int L = P.L;                                   // power of two in [4, 32]: a group lies in one warp
+  constexpr int U = (KP <= 8) ? 4 : 2;                   // neighbour rows in flight per lane
+  const int L = P.L;
   const int lane = threadIdx.x & (L - 1);
-  const int gl = threadIdx.x / L;                      // group within the CTA
+  const int gl = threadIdx.x / L;
   const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
   const int groups_cta = blockDim.x / L;
-  const int vpl = (P.S + L - 1) / L;
+  const int nch = (P.S + L - 1) / L;
+  const long long items = (long long)P.n * nch;
   bool bad = false;
-  for (int i = blockIdx.x * groups_cta + gl; i < P.n; i += gridDim.x * groups_cta) {
-    for (int k = lane; k < KP; k += L) { red[gl][0][k] = 0ull; red[gl][1][k] = 0ull; }
-    __syncwarp(gmask);
-    const int e0 = __ldg(P.rowptr + i), e1 = __ldg(P.rowptr + i + 1);
-    const unsigned long long rkey = P.nkey + (unsigned long long)i * (unsigned long long)P.K * P.S_total_u;
-    for (int vv = 0; vv < vpl; ++vv) {
-      const int r = lane + vv * L;
-      if (r >= P.S) break;
-      // q_k = sum_{j in N(i)} p_j[r][k], CSR order
+  for (long long it = (long long)blockIdx.x * groups_cta + gl; it < items; it += (long long)gridDim.x * groups_cta) {
+    const int i = (int)(it / nch), ch = (int)(it - (long long)i * nch);
+    const int r = ch * L + lane;
+    const bool live = r < P.S;
+    float w[KP];                                          // the replica's new P (0 on idle lanes)
+#pragma unroll
+    for (int k = 0; k < KP; ++k) w[k] = 0.0f;
+    if (live) {
+      const int e0 = __ldg(P.rowptr + i), e1 = __ldg(P.rowptr + i + 1);
+      // q_k = sum_{j in N(i)} p_j[r][k] in CSR order (U rows loaded before the adds)
       float q[KP];
 #pragma unroll
       for (int k = 0; k < KP; ++k) q[k] = 0.0f;
-      for (int e = e0; e < e1; ++e) {
-        const int j = __ldg(P.colidx + e);
+      int e = e0;
+      for (; e + U <= e1; e += U) {
+        float pj[U][KP];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ld_colours<KP>(P.p_cur + ((size_t)__ldg(P.colidx + e + u) * P.S + r) * KP, pj[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < KP; ++k) q[k] = fadd(q[k], pj[u][k]);
+      }
+      for (; e < e1; ++e) {
         float pj[KP];
-        ld_colours<KP>(P.p_cur + ((size_t)j * P.S + r) * KP, pj);
+        ld_colours<KP>(P.p_cur + ((size_t)__ldg(P.colidx + e) * P.S + r) * KP, pj);
 #pragma unroll
         for (int k = 0; k < KP; ++k) q[k] = fadd(q[k], pj[k]);
       }
+      const unsigned long long rkey = P.nkey + (unsigned long long)i * (unsigned long long)P.K * P.S_total_u;
       const size_t at = ((size_t)i * P.S + r) * KP;
-      float w[KP], mm[KP], vv2[KP];
+      float mm[KP], vv2[KP];
       ld_colours<KP>(P.p_cur + at, w);
       ld_colours<KP>(P.m + at, mm);
       ld_colours<KP>(P.v + at, vv2);
@@ -766,22 +784,29 @@ __global__ void __launch_bounds__(256) k_step_K(const StepKParams P) {
       st_colours<KP>(P.m + at, mm);
       st_colours<KP>(P.v + at, vv2);
       st_colours<KP>(P.p_next + at, w);
+    }
+    // fixed-point statistics of the new P per colour: shuffle-reduce over the group's replicas
 #pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        if (k >= P.K) continue;
-        long long D, D2;
-        stat_terms(w[k], P.ms[(size_t)i * P.K + k].x, D, D2);
-        atomicAdd(&red[gl][0][k], (unsigned long long)D);
-        atomicAdd(&red[gl][1][k], (unsigned long long)D2);
+    for (int k = 0; k < KP; ++k) {
+      if (k >= P.K) continue;
+      const size_t ik = (size_t)i * P.K + k, nk = (size_t)P.n * P.K;
+      long long D = 0, D2 = 0;
+      if (live) stat_terms(w[k], P.ms[ik].x, D, D2);
+      for (int off = L / 2; off > 0; off >>= 1) {
+        D += __shfl_xor_sync(gmask, D, off, L);
+        D2 += __shfl_xor_sync(gmask, D2, off, L);
+      }
+      if (lane == (k & (L - 1))) {
+        if (nch == 1) {
+          P.sums_next[ik] = D;
+          P.sums_next[nk + ik] = D2;
+        } else {
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + ik), (unsigned long long)D);
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + nk + ik), (unsigned long long)D2);
+          if (ch == 0) { P.sums_zero[ik] = 0; P.sums_zero[nk + ik] = 0; }
+        }
       }
     }
-    __syncwarp(gmask);
-    for (int k = lane; k < P.K; k += L) {
-      const size_t ik = (size_t)i * P.K + k;
-      P.sums_next[ik] = (long long)red[gl][0][k];
-      P.sums_next[(size_t)P.n * P.K + ik] = (long long)red[gl][1][k];
-    }
-    __syncwarp(gmask);
   }
   if (bad) atomicOr(P.flag, 1);
 }
