@@ -288,16 +288,16 @@ def main():
     if not args.no_e2e:
         rp = torch.from_numpy(g.rowptr).pin_memory().numpy()
         ci = torch.from_numpy(g.colidx).pin_memory().numpy()
-        ws = sol.workspace
-        sol.close()
-        del sol
+        # a fresh handle per step (graph H2D from pinned memory, validation, init); with N > 1 it
+        # joins the communicator of the handle timed above instead of bootstrapping NCCL again
+        ws = torch.empty_like(sol.workspace)
 
         gp = None if gor is None else torch.from_numpy(gor).pin_memory().numpy()
 
         def e2e_step():
             s = Q.Solver(rp, ci, cfg, device=dev, stream=stream, workspace=ws, group_of_row=gp)
             if world > 1:
-                qdist.attach(s, rank, world)
+                s.share_comm(sol)
             s.run_linear(w.gamma_min, w.gamma_max, w.steps)
             r = (s.round_evaluate_groups(want_x=True, want_counts=True) if gp is not None
                  else s.round_evaluate(want_x=True, want_replicas=True))

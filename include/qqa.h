@@ -168,6 +168,12 @@ QQA_API int qqa_reset(qqa_handle* h);
  * all-reduces the 2n int64 statistic sums over NCCL. (sync) */
 QQA_API int qqa_nccl_unique_id(uint8_t out[128]);
 QQA_API int qqa_attach_comm(qqa_handle* h, const uint8_t id[128], int rank, int nranks);
+/* Use donor's communicator (same device, same rank layout) instead of creating
+ * one: a handle for a new input can join a running job without another NCCL
+ * bootstrap. The communicator lives until the last handle using it is
+ * destroyed. Re-initialises h's replica state like qqa_attach_comm. Collective
+ * over the donor's ranks. (sync) */
+QQA_API int qqa_share_comm(qqa_handle* h, qqa_handle* donor);
 
 /* Run n_steps annealing steps with the given per-step gamma (host float[n_steps]).
  * The Adam step counter persists across calls. Async. */

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <memory>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -274,8 +275,14 @@ struct qqa_handle {
   int scur = 0;  // sums buffer of the current step (mod 3)
   int64_t step = 0;
   ncclComm_t comm = nullptr;
+  std::shared_ptr<ncclComm_t> comm_box;   // owner of comm (shared by qqa_share_comm; destroyed with the last user)
   int rank = 0, nranks = 1;
   int grid_step = 0, grid_init = 0, grid_fin = 0;
+  // compute / all-reduce overlap (N > 1): the step's rows run as comm_chunks launches; chunk c's
+  // sums are all-reduced on cstream while chunk c+1 computes
+  int comm_chunks = 1;
+  cudaStream_t cstream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;   // [comm_chunks] chunk computed; [comm_chunks] all-reduces done
   bool profiling = false;
   std::vector<cudaEvent_t> ev;  // pairs (start, end)
   size_t ev_used = 0;
@@ -530,6 +537,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
     P.ms = h->ms;
     P.sums_next = h->sums[sb];
     P.sums_zero = (h->s.B > 1) ? h->sums[sz] : nullptr;
+    const int C = (h->comm && h->s.n > 0) ? h->comm_chunks : 1;
     if (h->s.n > 0) {
       // K0: (mu_i, STD_i) of the current p, shift of the next sums
       qqa::k_finalize<<<h->grid_fin, 256, 0, h->stream>>>(h->c[a], h->sums[sa], h->s.n, (double)h->s.S_total,
@@ -538,12 +546,30 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
       h->launches++;
       int st;
       if ((st = record_start(h))) return st;
-      ks<<<h->grid_step, 256, 0, h->stream>>>(P);
-      QQA_CUDA(cudaGetLastError());
-      h->launches++;
+      for (int ch = 0; ch < C; ++ch) {
+        P.row_begin = (int)((int64_t)h->s.n * ch / C);
+        P.row_end = (int)((int64_t)h->s.n * (ch + 1) / C);
+        ks<<<h->grid_step, 256, 0, h->stream>>>(P);
+        QQA_CUDA(cudaGetLastError());
+        h->launches++;
+        if (C > 1) {  // all-reduce this chunk's rows on the comm stream while the next chunk computes
+          QQA_CUDA(cudaEventRecord(h->chunk_ev[ch], h->stream));
+          QQA_CUDA(cudaStreamWaitEvent(h->cstream, h->chunk_ev[ch], 0));
+          const size_t r0 = (size_t)P.row_begin, rows = (size_t)(P.row_end - P.row_begin);
+          QQA_NCCL(ncclGroupStart());
+          QQA_NCCL(ncclAllReduce(h->sums[sb] + r0, h->sums[sb] + r0, rows, ncclInt64, ncclSum, h->comm, h->cstream));
+          QQA_NCCL(ncclAllReduce(h->sums[sb] + h->s.n + r0, h->sums[sb] + h->s.n + r0, rows, ncclInt64, ncclSum,
+                                 h->comm, h->cstream));
+          QQA_NCCL(ncclGroupEnd());
+        }
+      }
       if ((st = record_end(h))) return st;
+      if (C > 1) {  // the next step's finalize needs every chunk's reduced sums
+        QQA_CUDA(cudaEventRecord(h->chunk_ev[C], h->cstream));
+        QQA_CUDA(cudaStreamWaitEvent(h->stream, h->chunk_ev[C], 0));
+      }
     }
-    if (h->comm) {
+    if (h->comm && C == 1) {
       QQA_NCCL(ncclAllReduce(h->sums[sb], h->sums[sb], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
     }
     h->cur = b;
@@ -585,6 +611,26 @@ int set_device(qqa_handle* h) {
   int cur = -1;
   QQA_CUDA(cudaGetDevice(&cur));
   if (cur != h->device) QQA_CUDA(cudaSetDevice(h->device));
+  return QQA_OK;
+}
+
+// Chunked compute / all-reduce overlap for the binary step (K-ary keeps one all-reduce per
+// step). QQA_COMM_CHUNKS overrides the default: 4 chunks with > 1 rank, none with one.
+int setup_overlap(qqa_handle* h) {
+  int C = (h->nranks > 1 && !h->s.kary) ? 4 : 1;
+  if (const char* env = std::getenv("QQA_COMM_CHUNKS")) C = std::max(1, std::min(64, std::atoi(env)));
+  if (h->s.kary || h->s.n < C) C = 1;
+  h->comm_chunks = C;
+  if (C > 1 && !h->cstream) {
+    int lo = 0, hi = 0;
+    QQA_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    QQA_CUDA(cudaStreamCreateWithPriority(&h->cstream, cudaStreamNonBlocking, hi));   // comm first
+  }
+  while ((int)h->chunk_ev.size() < C + 1) {
+    cudaEvent_t e;
+    QQA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->chunk_ev.push_back(e);
+  }
   return QQA_OK;
 }
 
@@ -794,17 +840,42 @@ int qqa_attach_comm(qqa_handle* h, const uint8_t id[128], int rank, int nranks) 
     return fail(QQA_ERR_INVALID_ARG, "sharding must be S_total = nranks * S_local and replica_offset = rank * S_local");
   int st = set_device(h);
   if (st) return st;
-  if (h->comm) {
-    ncclCommDestroy(h->comm);
-    h->comm = nullptr;
-  }
+  h->comm_box.reset();
+  h->comm = nullptr;
   ncclUniqueId uid;
   std::memcpy(&uid, id, 128);
-  QQA_NCCL(ncclCommInitRank(&h->comm, nranks, uid, rank));
+  ncclComm_t comm = nullptr;
+  QQA_NCCL(ncclCommInitRank(&comm, nranks, uid, rank));
+  h->comm_box = std::shared_ptr<ncclComm_t>(new ncclComm_t(comm), [](ncclComm_t* c) {
+    ncclCommDestroy(*c);
+    delete c;
+  });
+  h->comm = comm;
   h->rank = rank;
   h->nranks = nranks;
   h->step = 0;
+  if ((st = setup_overlap(h))) return st;
   if ((st = launch_init(h, false, nullptr))) return st;
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  return QQA_OK;
+}
+
+int qqa_share_comm(qqa_handle* h, qqa_handle* donor) {
+  if (!h || !donor) return fail(QQA_ERR_INVALID_ARG, "handle or donor is NULL");
+  if (!donor->comm) return fail(QQA_ERR_INVALID_ARG, "donor has no communicator");
+  if (donor->device != h->device) return fail(QQA_ERR_INVALID_ARG, "donor lives on another device");
+  const int rank = donor->rank, nranks = donor->nranks;
+  if ((int64_t)h->s.S_local * nranks != h->s.S_total || h->cfg.replica_offset != rank * h->s.S_local)
+    return fail(QQA_ERR_INVALID_ARG, "sharding must be S_total = nranks * S_local and replica_offset = rank * S_local");
+  int st = set_device(h);
+  if (st) return st;
+  h->comm_box = donor->comm_box;
+  h->comm = donor->comm;
+  h->rank = rank;
+  h->nranks = nranks;
+  h->step = 0;
+  if ((st = setup_overlap(h))) return st;
+  if ((st = launch_init(h, false, nullptr))) return st;   // collective: every rank's statistics
   QQA_CUDA(cudaStreamSynchronize(h->stream));
   return QQA_OK;
 }
@@ -1163,7 +1234,10 @@ int qqa_destroy(qqa_handle* h) {
   int st = set_device(h);
   if (st) return st;
   cudaStreamSynchronize(h->stream);
-  if (h->comm) ncclCommDestroy(h->comm);
+  h->comm = nullptr;
+  h->comm_box.reset();   // destroys the communicator when no other handle shares it
+  for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   delete h;
   return QQA_OK;

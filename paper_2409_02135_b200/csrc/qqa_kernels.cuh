@@ -217,6 +217,7 @@ struct StepParams {
   long long* __restrict__ sums_zero;    // [2][n] buffer of the step after next (zeroed here), B > 1
   int* __restrict__ flag;               // bit 0: non-finite theta
   int n, SB, B, S_local;
+  int row_begin, row_end;               // rows [row_begin, row_end) of this launch (comm overlap chunks)
   double S_total;
   int problem, alpha;
   float lam, comm, b1, c1, b2, c2, eps;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
   for (int b = 0; b < P.B; ++b) {
     const size_t blk = (size_t)b * NR * P.SB;     // float offset of block b
     const float* __restrict__ pc = P.p_cur + blk;
-    for (int i = group; i < P.n; i += ngroups) {
+    for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
       // ---- gather q_i over block b
       V8 acc[VPL];
       const int e0 = __ldg(P.rowptr_pad + i), e1 = __ldg(P.rowptr_pad + i + 1);

@@ -185,6 +185,10 @@ class Solver:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         check(lib.qqa_attach_comm(self._h, buf, rank, nranks))
 
+    def share_comm(self, donor: "Solver"):
+        """Join donor's communicator (no new NCCL bootstrap); collective over its ranks."""
+        check(lib.qqa_share_comm(self._h, donor._h))
+
     # ------------------------------------------------------------ profiling
     def profile(self, enable=True):
         check(lib.qqa_profile(self._h, 1 if enable else 0))

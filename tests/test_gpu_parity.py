@@ -314,3 +314,37 @@ def test_replica_blocked_layout_parity(Q, monkeypatch, SB, problem, S):
     sol2 = gpu(Q, g, problem, S, 5, comm=0.3)
     sol2.set_state(ck["theta"], ck["m"], ck["v"], ck["step"], c=sol.get_stats()["c"])
     assert np.array_equal(sol2.get_state()["p"], ck["p"])
+
+
+@pytest.mark.parametrize("chunks", ["3", "7"])
+def test_nccl_chunked_overlap_identical(Q, monkeypatch, chunks):
+    """The compute / all-reduce overlap (rows in chunks, each chunk's sums all-reduced on a second
+    stream while the next chunk computes) is bit-identical to the unchunked path."""
+    monkeypatch.setenv("QQA_COMM_CHUNKS", chunks)
+    g = gen.erdos_renyi(1000, 0.02, 5)
+    a = gpu(Q, g, "maxcut", 24, 8, comm=0.5)
+    b = gpu(Q, g, "maxcut", 24, 8, comm=0.5)
+    b.attach_comm(Q.Solver.nccl_unique_id(), 0, 1)
+    b.profile(True)
+    for s in (a, b):
+        s.run_linear(-5.0, 0.1, 100, 0, 60)
+    assert b.profile_read()[1] == 60                  # one timed span per step
+    for k in ("theta", "m", "v", "p"):
+        assert np.array_equal(a.get_state()[k], b.get_state()[k])
+    assert np.array_equal(a.get_stats()["sumD2"], b.get_stats()["sumD2"])
+
+
+def test_share_comm(Q):
+    """A second handle joins the first one's communicator; it survives the donor's destruction."""
+    g = gen.erdos_renyi(600, 0.02, 6)
+    a = gpu(Q, g, "mis", 16, 2)
+    a.attach_comm(Q.Solver.nccl_unique_id(), 0, 1)
+    b = gpu(Q, g, "mis", 16, 2)
+    b.share_comm(a)
+    c = gpu(Q, g, "mis", 16, 2)
+    a.close()
+    for s in (b, c):
+        s.run_linear(-2.0, 0.1, 100, 0, 40)
+    for k in ("theta", "p"):
+        assert np.array_equal(b.get_state()[k], c.get_state()[k])
+    assert b.round_evaluate().best_replica == c.round_evaluate().best_replica
