@@ -75,7 +75,7 @@ __device__ __forceinline__ float sigmoid_c(float th) {
   const float Ec = exp_neg_c(fminf(a, 87.0f));     // evaluated unconditionally (no branch)
   const float E = (a > 87.0f) ? 0.0f : Ec;
   const float den = fadd(1.0f, E);
-  return (th >= 0.0f) ? fdiv(1.0f, den) : fdiv(E, den);
+  return fdiv((th >= 0.0f) ? 1.0f : E, den);   // one division (the numerator is selected, not the quotient)
 }
 
 // Clamp(w) into [0, 1]; NaN and -0 map to +0 (non-finite is flagged first).
@@ -162,6 +162,18 @@ struct V8 {
   float f[8];
 };
 
+// acc += b on 8 floats as 4 packed FADD2 (sm_100 add.rn.f32x2: per component exactly __fadd_rn).
+// Only pure add chains use packed ops: ptxas 12.9 contracts mul.rn.f32x2 -> add.rn.f32x2 into FFMA2
+// even with -fmad=false, which would break the contract.
+__device__ __forceinline__ void add8(V8& acc, const V8& b) {
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const float2 r = __fadd2_rn(make_float2(acc.f[k], acc.f[k + 1]), make_float2(b.f[k], b.f[k + 1]));
+    acc.f[k] = r.x;
+    acc.f[k + 1] = r.y;
+  }
+}
+
 __device__ __forceinline__ V8 zero8() {
   V8 r;
 #pragma unroll
@@ -174,12 +186,48 @@ __device__ __forceinline__ V8 zero8() {
 #define QQA_V8_IN(v) "f"(v.f[0]), "f"(v.f[1]), "f"(v.f[2]), "f"(v.f[3]), \
                      "f"(v.f[4]), "f"(v.f[5]), "f"(v.f[6]), "f"(v.f[7])
 
-// Gathered p rows: read-only during the step, reused by every neighbour -> keep in L2.
+// L2 policies (compile-time; measured in profiles/r1_design_iterations.md):
+//   QQA_GATHER_POLICY 0: gathered p rows evict_last, 1: evict_normal
+//   QQA_PNEXT_POLICY  0: p_next stored evict_normal, 1: evict_last (next step's gather source)
+//   QQA_INDEX_POLICY  0: CSR indices through the default path, 1: streamed (L1::no_allocate, L2 evict_first)
+#ifndef QQA_GATHER_POLICY
+#define QQA_GATHER_POLICY 0
+#endif
+#ifndef QQA_PNEXT_POLICY
+#define QQA_PNEXT_POLICY 0
+#endif
+#ifndef QQA_INDEX_POLICY
+#define QQA_INDEX_POLICY 0
+#endif
+// 1: the next round's CSR indices are loaded before this round's gathers (software pipeline;
+// measured slower on c5 -- extra live registers spill -- so off, profiles/r1_design_iterations.md)
+#ifndef QQA_IDX_PIPELINE
+#define QQA_IDX_PIPELINE 0
+#endif
+
+// Gathered p rows: read-only during the step, reused by every neighbour.
 __device__ __forceinline__ V8 ld8_gather(const float* ptr) {
   V8 r;
+#if QQA_GATHER_POLICY == 1
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : QQA_V8_OUT(r) : "l"(ptr));
+#else
   asm volatile("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : QQA_V8_OUT(r) : "l"(ptr));
+#endif
   return r;
+}
+
+// Four CSR indices (read once per step).
+__device__ __forceinline__ int4 ld_idx4(const int* ptr) {
+#if QQA_INDEX_POLICY == 1
+  int4 r;   // evict-first policy via an L2 cache hint (the qualifier form needs 256-bit accesses)
+  asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+               " ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], pol;\n}"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
+  return r;
+#else
+  return __ldg(reinterpret_cast<const int4*>(ptr));
+#endif
 }
 // theta / m / v: read once and written once per step -> first out of L2, bypass L1.
 __device__ __forceinline__ V8 ld8_stream(const float* ptr) {
@@ -195,6 +243,13 @@ __device__ __forceinline__ void st8_stream(float* ptr, const V8& v) {
 // p_next: gathered by the next step -> normal priority.
 __device__ __forceinline__ void st8(float* ptr, const V8& v) {
   asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" :: "l"(ptr), QQA_V8_IN(v) : "memory");
+}
+__device__ __forceinline__ void st8_pnext(float* ptr, const V8& v) {
+#if QQA_PNEXT_POLICY == 1
+  asm volatile("st.global.L2::evict_last.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" :: "l"(ptr), QQA_V8_IN(v) : "memory");
+#else
+  st8(ptr, v);
+#endif
 }
 __device__ __forceinline__ V8 ld8(const float* ptr) {
   V8 r;
@@ -323,15 +378,24 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
       V8 acc[VPL];
       const int e0 = __ldg(P.rowptr_pad + i), e1 = __ldg(P.rowptr_pad + i + 1);
       constexpr int U = (VPL == 1) ? QQA_GATHER_U : 4;   // neighbour rows in flight per lane
+      // The indices of round k+1 are loaded before the gathers of round k (software pipeline), so
+      // each round waits for one memory latency, not an index load followed by the gathers.
+      // Rows are padded to multiples of 4 (not of U): past the row end the sentinel row n is read.
+      int4 nxt[U / 4];
+#pragma unroll
+      for (int u4 = 0; u4 < U / 4; ++u4)
+        nxt[u4] = (e0 + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e0 + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
       for (int e = e0; e < e1; e += U) {
         int js[U];
 #pragma unroll
-        for (int u = 0; u < U; u += 4) {
-          // rows are padded to multiples of 4 (not of U): past the row end read the sentinel
-          const int4 j4 = (u == 0 || e + u < e1) ? __ldg(reinterpret_cast<const int4*>(P.colidx_pad + e + u))
-                                                 : make_int4(P.n, P.n, P.n, P.n);
-          js[u] = j4.x; js[u + 1] = j4.y; js[u + 2] = j4.z; js[u + 3] = j4.w;
+        for (int u4 = 0; u4 < U / 4; ++u4) {
+          js[4 * u4] = nxt[u4].x; js[4 * u4 + 1] = nxt[u4].y; js[4 * u4 + 2] = nxt[u4].z; js[4 * u4 + 3] = nxt[u4].w;
         }
+#if QQA_IDX_PIPELINE
+#pragma unroll
+        for (int u4 = 0; u4 < U / 4; ++u4)
+          nxt[u4] = (e + U + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e + U + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
+#endif
         V8 buf[U][VPL];
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -340,21 +404,22 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
             const int col8 = lane + w * LANES;
             buf[u][w] = (col8 < SB8) ? ld8_gather(pc + (size_t)js[u] * P.SB + col8 * 8) : zero8();
           }
+#if !QQA_IDX_PIPELINE
+#pragma unroll
+        for (int u4 = 0; u4 < U / 4; ++u4)
+          nxt[u4] = (e + U + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e + U + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
+#endif
         if (e == e0) {
 #pragma unroll
           for (int w = 0; w < VPL; ++w) acc[w] = buf[0][w];
         } else {
 #pragma unroll
-          for (int w = 0; w < VPL; ++w)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[w].f[k] = fadd(acc[w].f[k], buf[0][w].f[k]);
+          for (int w = 0; w < VPL; ++w) add8(acc[w], buf[0][w]);
         }
 #pragma unroll
         for (int u = 1; u < U; ++u)
 #pragma unroll
-          for (int w = 0; w < VPL; ++w)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[w].f[k] = fadd(acc[w].f[k], buf[u][w].f[k]);
+          for (int w = 0; w < VPL; ++w) add8(acc[w], buf[u][w]);
       }
       if (e0 == e1) {
 #pragma unroll
@@ -403,7 +468,7 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
         st8_stream(P.theta + at, th);
         st8_stream(P.m + at, mm);
         st8_stream(P.v + at, vv);
-        st8(P.p_next + at, pn);
+        st8_pnext(P.p_next + at, pn);
       }
       publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, P.sums_next, P.sums_zero);
     }
@@ -746,7 +811,11 @@ __global__ void __launch_bounds__(256) k_step_K(const StepKParams P) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int k = 0; k < KP; ++k) q[k] = fadd(q[k], pj[u][k]);
+          for (int k = 0; k < KP; k += 2) {   // packed FADD2 (pure add chain, see add8)
+            const float2 r = __fadd2_rn(make_float2(q[k], q[k + 1]), make_float2(pj[u][k], pj[u][k + 1]));
+            q[k] = r.x;
+            q[k + 1] = r.y;
+          }
       }
       for (; e < e1; ++e) {
         float pj[KP];
