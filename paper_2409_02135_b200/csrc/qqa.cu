@@ -42,6 +42,7 @@ int fail(int status, const std::string& msg) {
   } while (0)
 
 constexpr size_t kAlign = 256;
+constexpr int kSchedCap = 4096;   // steps per persistent launch (device table of per-step scalars)
 constexpr double kL2BlockBudget = 256.0 * 1024 * 1024;  // p larger than this is replica-blocked (measured)
 size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -59,7 +60,7 @@ struct Shape {
 
 struct Layout {
   size_t rowptr, colidx, rowptr_pad, colidx_pad, gor, theta, m, v, p0, p1, c0, c1, ms, s0, s1, s2, flag, X,
-      counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, total;
+      counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, sched, total;
 };
 
 Layout make_layout(const Shape& s) {
@@ -96,6 +97,7 @@ Layout make_layout(const Shape& s) {
   L.gbest = take((size_t)s.G * sizeof(int));
   L.gbeste = take((size_t)s.G * sizeof(double));
   L.xbuf = take((size_t)s.n);
+  L.sched = take((size_t)kSchedCap * sizeof(float4));
   L.total = o;
   return L;
 }
@@ -271,6 +273,8 @@ struct qqa_handle {
   int* gbest = nullptr;
   double* gbeste = nullptr;
   uint8_t* xbuf = nullptr;
+  float4* sched = nullptr;     // per-step scalars of a persistent launch
+  int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
   int cur = 0;   // p / c buffer of the current step (mod 2)
   int scur = 0;  // sums buffer of the current step (mod 3)
   int64_t step = 0;
@@ -295,11 +299,22 @@ namespace {
 
 using StepKernel = void (*)(const qqa::StepParams);
 using InitKernel = void (*)(const qqa::InitParams);
+using RunKernel = void (*)(const qqa::RunParams);
 
 // Step-kernel mode: bit 0 clamp map, bit 1 Langevin noise (template, so the
 // default sigmoid / no-noise kernel carries none of the optional code).
 int step_mode(const qqa_config& c) {
   return (c.map == QQA_MAP_CLAMP ? qqa::kModeClamp : 0) | (c.temperature > 0.0f ? qqa::kModeNoise : 0);
+}
+
+template <int L, int V>
+RunKernel run_for_mode(int mode) {
+  switch (mode) {
+    case 0: return qqa::k_run<L, V, 0>;
+    case 1: return qqa::k_run<L, V, 1>;
+    case 2: return qqa::k_run<L, V, 2>;
+    default: return qqa::k_run<L, V, 3>;
+  }
 }
 
 template <int L, int V>
@@ -312,11 +327,12 @@ StepKernel step_for_mode(int mode) {
   }
 }
 
-bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki) {
+bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki, RunKernel* kr = nullptr) {
 #define QQA_CASE(L, V)                                   \
   if (lanes == L && vpl == V) {                          \
     ks = step_for_mode<L, V>(mode);                      \
     ki = qqa::k_init<L, V>;                              \
+    if (kr) *kr = run_for_mode<L, V>(mode);              \
     return true;                                         \
   }
   QQA_CASE(1, 1) QQA_CASE(2, 1) QQA_CASE(4, 1) QQA_CASE(8, 1) QQA_CASE(16, 1)
@@ -503,10 +519,79 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
   return QQA_OK;
 }
 
+// Persistent path (k_run): one cooperative launch per chunk of <= kSchedCap steps. Used for
+// one-GPU, unblocked problems of up to 2^24 replica-variables (L2-resident / launch-bound);
+// QQA_PERSISTENT=0/1 overrides. Bit-identical to the launch-per-step path.
+bool use_persistent(const qqa_handle* h, int64_t n_steps) {
+  if (h->grid_run <= 0 || h->comm || h->s.B != 1 || h->s.kary || h->s.n == 0 || n_steps < 2) return false;
+  if (const char* env = std::getenv("QQA_PERSISTENT")) return std::atoi(env) != 0;
+  return (int64_t)h->s.n * h->s.S_p <= ((int64_t)1 << 24);
+}
+
+int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
+  StepKernel ks;
+  InitKernel ki;
+  RunKernel kr = nullptr;
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki, &kr);
+  const qqa_config& c = h->cfg;
+  qqa::RunParams R{};
+  qqa::StepParams& P = R.P;
+  P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
+  P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
+  P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
+  P.row_begin = 0; P.row_end = h->s.n;
+  P.problem = c.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;
+  P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
+  P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
+  P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
+  P.eps = c.eps;
+  P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
+  P.ns = (float)std::sqrt(2.0 * (double)c.lr * (double)c.temperature);
+  P.S_total_u = (unsigned long long)h->s.S_total;
+  R.c[0] = h->c[0]; R.c[1] = h->c[1];
+  R.sums[0] = h->sums[0]; R.sums[1] = h->sums[1]; R.sums[2] = h->sums[2];
+  R.p[0] = h->p[0]; R.p[1] = h->p[1];
+  R.nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);
+  R.off = (unsigned long long)c.replica_offset;
+  R.S_total = (double)h->s.S_total;
+  R.sched = h->sched;
+  std::vector<float4> tab((size_t)std::min<int64_t>(n_steps, kSchedCap));
+  for (int64_t k0 = 0; k0 < n_steps; k0 += kSchedCap) {
+    const int nk = (int)std::min<int64_t>(kSchedCap, n_steps - k0);
+    for (int j = 0; j < nk; ++j) {   // the same host double -> fp32 scalars as the launch-per-step path
+      const int64_t t = h->step + j + 1;
+      tab[j] = make_float4((float)(-2.0 * (double)c.alpha * (double)gamma[k0 + j]),
+                           (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t))),
+                           (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t))), 0.0f);
+    }
+    // stream-ordered after the previous chunk's launch (pageable source: staged before return)
+    QQA_CUDA(cudaMemcpyAsync(h->sched, tab.data(), (size_t)nk * sizeof(float4), cudaMemcpyHostToDevice, h->stream));
+    R.t0 = h->step;
+    R.nsteps = nk;
+    R.cur0 = h->cur;
+    R.scur0 = h->scur;
+    void* args[] = {(void*)&R};
+    int st;
+    if ((st = record_start(h))) return st;
+    QQA_CUDA(cudaLaunchCooperativeKernel((const void*)kr, dim3(h->grid_run), dim3(256), args, 0, h->stream));
+    h->launches++;
+    if (h->profiling) {   // one launch = nk steps: per-step kernel time = span / nk
+      QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
+      h->ev_used += 2;
+      h->prof_launches += nk;
+    }
+    h->cur = (h->cur + nk) & 1;
+    h->scur = (int)((h->scur + nk) % 3);
+    h->step += nk;
+  }
+  return QQA_OK;
+}
+
 int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (n_steps < 0) return fail(QQA_ERR_INVALID_ARG, "n_steps < 0");
   if (n_steps > 0 && !gamma) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
   if (h->s.kary) return do_steps_kary(h, gamma, n_steps);
+  if (use_persistent(h, n_steps)) return do_steps_persistent(h, gamma, n_steps);
   StepKernel ks;
   InitKernel ki;
   pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki);
@@ -526,17 +611,17 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   for (int64_t k = 0; k < n_steps; ++k) {
     const int64_t t = h->step + 1;  // Adam step index (reading R11)
     // xi key of (t, i, global s) = nbase + (t n + i) S_total + s  (mod 2^64)
-    P.nkey = nbase + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total + (uint64_t)c.replica_offset;
-    P.kt = (float)(-2.0 * (double)c.alpha * (double)gamma[k]);
+    P.var.nkey = nbase + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total + (uint64_t)c.replica_offset;
+    P.var.kt = (float)(-2.0 * (double)c.alpha * (double)gamma[k]);
     P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
-    P.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
-    P.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
+    P.var.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
+    P.var.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
     const int a = h->cur, b = h->cur ^ 1;
     const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
-    P.p_cur = h->p[a]; P.p_next = h->p[b];
+    P.var.p_cur = h->p[a]; P.var.p_next = h->p[b];
     P.ms = h->ms;
-    P.sums_next = h->sums[sb];
-    P.sums_zero = (h->s.B > 1) ? h->sums[sz] : nullptr;
+    P.var.sums_next = h->sums[sb];
+    P.var.sums_zero = (h->s.B > 1) ? h->sums[sz] : nullptr;
     const int C = (h->comm && h->s.n > 0) ? h->comm_chunks : 1;
     if (h->s.n > 0) {
       // K0: (mu_i, STD_i) of the current p, shift of the next sums
@@ -727,6 +812,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   h->gbeste = (double*)(ws + L.gbeste);
   h->gor = g->group_of_row ? (int*)(ws + L.gor) : nullptr;
   h->xbuf = (uint8_t*)(ws + L.xbuf);
+  h->sched = (float4*)(ws + L.sched);
 
   // Graph -> device (int32 offsets). Max clique walks the complement graph.
   std::vector<int> rp32, ci_c;
@@ -803,9 +889,16 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   } else {
     StepKernel ks;
     InitKernel ki;
-    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki))
+    RunKernel kr = nullptr;
+    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki, &kr))
       return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
     if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
+    {  // persistent kernel: every CTA must be co-resident (cooperative launch)
+      int coop = 0;
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
+      if (coop && s.B == 1 && (st = grid_for((const void*)kr, h->sm_count, s.n, s.lanes, h->grid_run)))
+        return cleanup(st);
+    }
     h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
     if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
   }

@@ -30,6 +30,7 @@
 // that is never -0.0f (p >= 0, q starts at +0), which leaves it unchanged.
 #pragma once
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace qqa {
@@ -257,28 +258,36 @@ __device__ __forceinline__ V8 ld8(const float* ptr) {
   return r;
 }
 
+// The per-step part of a step launch: buffers of this step and its scalars.
+// (A member of the kernel parameters for the launch-per-step kernel, so it stays in the
+// constant bank; a register copy per step in the persistent kernel.)
+struct StepVar {
+  const float* p_cur;                   // [B][NR][SB]
+  float* p_next;
+  long long* sums_next;                 // [2][n] this rank's sums; zero on entry when B > 1
+  long long* sums_zero;                 // [2][n] buffer of the step after next (zeroed here), B > 1
+  float kt, st, rt;                     // -2 alpha gamma_t, lr/(1-b1^t), 1/sqrt(1-b2^t) (host double -> float)
+  unsigned long long nkey;              // noise key of (t, row 0, replica_offset): nbase + t n S_total + offset
+};
+
 // ------------------------------------------------------------ parameters
 struct StepParams {
   const int* __restrict__ rowptr;       // [n+1]   original CSR (degree for Max-Cut)
   const int* __restrict__ rowptr_pad;   // [n+1]   multiples of 4
   const int* __restrict__ colidx_pad;   // padded CSR, sentinel n
-  const float* __restrict__ p_cur;      // [B][NR][SB]
-  float* __restrict__ p_next;
+  StepVar var;                          // this step: p_cur / p_next [B][NR][SB], sums, scalars
   float* __restrict__ theta;
   float* __restrict__ m;
   float* __restrict__ v;
   const float2* __restrict__ ms;        // [n] (mu_i, STD_i) of the current p (k_finalize)
-  long long* __restrict__ sums_next;    // [2][n] this rank's sums; zero on entry when B > 1
-  long long* __restrict__ sums_zero;    // [2][n] buffer of the step after next (zeroed here), B > 1
   int* __restrict__ flag;               // bit 0: non-finite theta
   int n, SB, B, S_local;
   int row_begin, row_end;               // rows [row_begin, row_end) of this launch (comm overlap chunks)
   double S_total;
   int problem, alpha;
   float lam, comm, b1, c1, b2, c2, eps;
-  float kt, at, st, rt;                 // per-step scalars (host double -> float)
+  float at;                             // 1 - lr wd (host double -> float)
   float ns;                             // Langevin scale sqrt(2 lr T) (host double -> float)
-  unsigned long long nkey;              // noise key of (t, row 0, replica_offset): nbase + t n S_total + offset
   unsigned long long S_total_u;         // key stride per row
 };
 
@@ -287,13 +296,13 @@ struct StepParams {
 // chain factor, p = Clamp(th)); otherwise p = sigmoid(th). Returns p_next; bad
 // is set when the pre-map parameter is non-finite.
 template <int MODE>
-__device__ __forceinline__ float update_element(const StepParams& P, float q, float degf, float pi,
-                                                float mu, float sd, float& th, float& mm, float& vv,
+__device__ __forceinline__ float update_element(const StepParams& P, const StepVar& V, float q, float degf,
+                                                float pi, float mu, float sd, float& th, float& mm, float& vv,
                                                 unsigned long long key, bool& bad) {
   const float e = fsub(fmul(2.0f, pi), 1.0f);
   float ep = e;
   for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);                 // (2p-1)^(alpha-1)
-  const float ent = fmul(P.kt, ep);                                   // -2 alpha gamma (2p-1)^(alpha-1)
+  const float ent = fmul(V.kt, ep);                                   // -2 alpha gamma (2p-1)^(alpha-1)
   const float obj = (P.problem == kMAXCUT) ? fsub(fmul(2.0f, q), degf)   // -deg + 2q
                                            : fsub(fmul(P.lam, q), 1.0f); // -1 + lambda q
   const float com = (sd >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, mu), sd)) : 0.0f;
@@ -303,8 +312,8 @@ __device__ __forceinline__ float update_element(const StepParams& P, float q, fl
   const float t1 = fmul(th, P.at);                                    // decoupled weight decay
   mm = fadd(fmul(P.b1, mm), fmul(P.c1, g));
   vv = fadd(fmul(P.b2, vv), fmul(fmul(P.c2, g), g));
-  const float den = fadd(fmul(__fsqrt_rn(vv), P.rt), P.eps);
-  float w = fsub(t1, fmul(P.st, fdiv(mm, den)));
+  const float den = fadd(fmul(__fsqrt_rn(vv), V.rt), P.eps);
+  float w = fsub(t1, fmul(V.st, fdiv(mm, den)));
   if (MODE & kModeNoise) w = fadd(w, fmul(P.ns, gauss_c(mix64(key))));   // + sqrt(2 lr T) xi
   bad |= !isfinite(w);
   if (MODE & kModeClamp) {
@@ -360,20 +369,13 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
 // which equals 0 + row exactly since p >= +0), gradient + AdamW + sigmoid for
 // the block's replicas with (mu_i, STD_i) from k_finalize, then the fixed-point
 // sums of p_next (shuffles; atomics across blocks).
+// One work item (replica block b, variable i) of the step: gather, update, statistics.
 template <int LANES, int VPL, int MODE>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
-  const int lane = threadIdx.x & (LANES - 1);
-  const unsigned gmask = group_mask<LANES>();
-  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
-  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
-  const int SB8 = P.SB >> 3;
-  const size_t NR = (size_t)P.n + 1;
-  bool bad = false;
-
-  for (int b = 0; b < P.B; ++b) {
-    const size_t blk = (size_t)b * NR * P.SB;     // float offset of block b
-    const float* __restrict__ pc = P.p_cur + blk;
-    for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
+__device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
+                                          unsigned gmask, float mu, float sd, bool& bad) {
+      const int SB8 = P.SB >> 3;
+      const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
+      const float* __restrict__ pc = V.p_cur + blk;
       // ---- gather q_i over block b
       V8 acc[VPL];
       const int e0 = __ldg(P.rowptr_pad + i), e1 = __ldg(P.rowptr_pad + i + 1);
@@ -426,13 +428,11 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
         for (int w = 0; w < VPL; ++w) acc[w] = zero8();
       }
 
-      const float2 msi = P.ms[i];
-      const float mu = msi.x, sd = msi.y;
       const float degf = (P.problem == kMAXCUT) ? (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i)) : 0.0f;
 
       // ---- gradient, AdamW, (noise), map, statistics of p_next
       long long sD = 0, sD2 = 0;
-      const unsigned long long rkey = P.nkey + (unsigned long long)i * P.S_total_u;  // noise key of (t, i, offset)
+      const unsigned long long rkey = V.nkey + (unsigned long long)i * P.S_total_u;  // noise key of (t, i, offset)
 #pragma unroll
       for (int w = 0; w < VPL; ++w) {
         const int col8 = lane + w * LANES;
@@ -441,13 +441,13 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
         V8 th = ld8_stream(P.theta + at);
         V8 mm = ld8_stream(P.m + at);
         V8 vv = ld8_stream(P.v + at);
-        const V8 pp = ld8(P.p_cur + at);
+        const V8 pp = ld8(V.p_cur + at);
         V8 pn = pp;
         const int s0 = b * P.SB + col8 * 8;          // local replica index of element 0
         if (s0 + 8 <= P.S_local) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            pn.f[k] = update_element<MODE>(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
+            pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
                                            rkey + (unsigned long long)(s0 + k), bad);
             long long D, D2;
             stat_terms(pn.f[k], mu, D, D2);
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (s0 + k < P.S_local) {
-              pn.f[k] = update_element<MODE>(P, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
+              pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
                                              rkey + (unsigned long long)(s0 + k), bad);
               long long D, D2;
               stat_terms(pn.f[k], mu, D, D2);
@@ -468,10 +468,70 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
         st8_stream(P.theta + at, th);
         st8_stream(P.m + at, mm);
         st8_stream(P.v + at, vv);
-        st8_pnext(P.p_next + at, pn);
+        st8_pnext(V.p_next + at, pn);
       }
-      publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, P.sums_next, P.sums_zero);
+      publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, V.sums_next, V.sums_zero);
+}
+
+template <int LANES, int VPL, int MODE>
+__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
+  const int lane = threadIdx.x & (LANES - 1);
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  bool bad = false;
+  for (int b = 0; b < P.B; ++b)
+    for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
+      const float2 msi = P.ms[i];
+      step_item<LANES, VPL, MODE>(P, P.var, b, i, lane, gmask, msi.x, msi.y, bad);
     }
+  if (bad) atomicOr(P.flag, 1);
+}
+
+// Persistent form for small / L2-resident problems (one replica block, one GPU): ONE
+// cooperative launch runs nsteps annealing steps with a grid barrier between them. A
+// group owns the same variables every step, so (mu_i, STD_i) come from the sums the
+// group itself published the step before (the k_finalize arithmetic, in registers) and
+// only the gather needs the barrier. Buffers rotate exactly as the launch-per-step path
+// does (p, c ping-pong; sums mod 3) and the per-step scalars come from a host-filled
+// table sched[j] = (k_t, s_t, r_t, 0) of step t = t0 + j + 1, so both paths are
+// bit-identical.
+struct RunParams {
+  StepParams P;                         // invariants (var and ms unused)
+  const float4* __restrict__ sched;     // [nsteps]
+  float* c[2];                          // shift of the statistics, ping-pong
+  long long* sums[3];                   // [2][n] rotating
+  float* p[2];
+  unsigned long long nbase;             // noise stream base; key of (t, i, s) = nbase + (t n + i) S_total + s
+  unsigned long long off;               // replica_offset
+  long long t0;                         // Adam steps taken before this launch
+  int nsteps, cur0, scur0;
+  double S_total;
+};
+
+template <int LANES, int VPL, int MODE>
+__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_run(const RunParams R) {
+  namespace cg = cooperative_groups;
+  const StepParams& P = R.P;
+  const int lane = threadIdx.x & (LANES - 1);
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  bool bad = false;
+  for (int j = 0; j < R.nsteps; ++j) {
+    const int a = (R.cur0 + j) & 1, sa = (R.scur0 + j) % 3, sb = (R.scur0 + j + 1) % 3;
+    const float4 sc = R.sched[j];
+    const unsigned long long t = (unsigned long long)(R.t0 + j + 1);
+    const StepVar V{R.p[a], R.p[a ^ 1], R.sums[sb], nullptr, sc.x, sc.y, sc.z,
+                    R.nbase + t * (unsigned long long)P.n * P.S_total_u + R.off};
+    const long long* __restrict__ sc_cur = R.sums[sa];
+    for (int i = group; i < P.n; i += ngroups) {
+      float mu, sd;
+      finalize_stats(R.c[a][i], sc_cur[i], sc_cur[P.n + i], R.S_total, mu, sd);
+      if (lane == 0) R.c[a ^ 1][i] = mu;
+      step_item<LANES, VPL, MODE>(P, V, 0, i, lane, gmask, mu, sd, bad);
+    }
+    cg::this_grid().sync();
   }
   if (bad) atomicOr(P.flag, 1);
 }

@@ -348,3 +348,30 @@ def test_share_comm(Q):
     for k in ("theta", "p"):
         assert np.array_equal(b.get_state()[k], c.get_state()[k])
     assert b.round_evaluate().best_replica == c.round_evaluate().best_replica
+
+
+@pytest.mark.parametrize("problem,S,mp,T", [("mis", 16, "sigmoid", 0.0), ("maxcut", 100, "clamp", 0.001),
+                                            ("maxclique", 40, "sigmoid", 0.001), ("mis", 256, "clamp", 0.0),
+                                            ("mis", 3, "sigmoid", 0.0)])
+def test_persistent_equals_launch_per_step(Q, monkeypatch, problem, S, mp, T):
+    """The persistent cooperative kernel (one launch per <= 4096 steps, grid barrier per step)
+    is bit-identical to one k_finalize + k_step launch per step, across a schedule-table chunk."""
+    g = gen.erdos_renyi(150, 0.5, 12) if problem == "maxclique" else gen.erdos_renyi(700, 0.02, 12)
+    steps = 4100 if S == 16 else 300
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("QQA_PERSISTENT", flag)
+        sol = gpu(Q, g, problem, S, 4, map=mp, temperature=T)
+        sol.profile(True)
+        l0 = sol.launch_count()
+        sol.run_linear(-2.0, 0.1, steps)
+        launches = sol.launch_count() - l0
+        assert sol.profile_read()[1] == steps
+        out.append((sol.get_state(), sol.get_stats(), launches, sol.round_evaluate()))
+    (a, sa, la, ra), (b, sb, lb, rb) = out
+    for k in ("theta", "m", "v", "p"):
+        assert np.array_equal(a[k], b[k]), k
+    for k in ("c", "sumD", "sumD2"):
+        assert np.array_equal(sa[k], sb[k]), k
+    assert ra.best_replica == rb.best_replica and np.array_equal(ra.best_x, rb.best_x)
+    assert la == (steps + 4095) // 4096 and lb == 2 * steps
