@@ -1,0 +1,49 @@
+"""bench.py contract on CPU: the reference arm (the CPU oracle, this tier's reference) prints ONE
+JSON line with the keys the driver reads; the byte model and workload configs are consistent."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import gen  # noqa: E402
+
+
+@pytest.mark.parametrize("workload", ["c1", "q13"])
+def test_reference_arm_prints_one_json_line(workload):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload",
+                          workload, "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == workload
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["metric"] == json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+
+
+def test_byte_model_matches_survey_c5():
+    """c5 moves 6,740 MB of algorithmic bytes per step at one GPU."""
+    assert bench.algorithmic_bytes(1_000_000, 20_000_000, 64) == 6_740_000_004
+    # K-ary: every replica-variable carries K colour columns
+    assert bench.algorithmic_bytes(10, 40, 8, 3) == 4 * 40 + 4 * 11 + 4 * 40 * 8 * 3 + 24 * 10 * 8 * 3
+
+
+def test_workload_configs_shard_for_the_scaling_run():
+    """The driver's scaling run shards BASELINE.json configs[4] (c5, S=64) over 1/2/4/8 GPUs."""
+    from paper_2409_02135_b200 import dist as qdist
+    for world in (1, 2, 4, 8):
+        offs = [qdist.shard(64, world, r) for r in range(world)]
+        assert sum(s for _, s in offs) == 64 and offs[-1][0] + offs[-1][1] == 64
+    w = gen.workload("c1")
+    cfg = bench.workload_config(w, 1)
+    assert cfg["N"] == 256 and cfg["S"] == 16 and cfg["anneal_steps"] == 1000
