@@ -200,6 +200,12 @@ __device__ __forceinline__ V8 zero8() {
 #ifndef QQA_INDEX_POLICY
 #define QQA_INDEX_POLICY 0
 #endif
+// 1: the sigmoid step recomputes its own p row as sigmoid(theta) instead of reading p_cur
+// (bit-identical; saves N S 4 mostly L2-missing bytes per step but costs more issue than it
+// saves on c5, so off -- profiles/r1_design_iterations.md). Under clamp p == theta is reused.
+#ifndef QQA_RECOMPUTE_P
+#define QQA_RECOMPUTE_P 0
+#endif
 // 1: the next round's CSR indices are loaded before this round's gathers (software pipeline;
 // measured slower on c5 -- extra live registers spill -- so off, profiles/r1_design_iterations.md)
 #ifndef QQA_IDX_PIPELINE
@@ -441,7 +447,15 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         V8 th = ld8_stream(P.theta + at);
         V8 mm = ld8_stream(P.m + at);
         V8 vv = ld8_stream(P.v + at);
-        const V8 pp = ld8(V.p_cur + at);
+        V8 pp;
+        if (MODE & kModeClamp) {
+          pp = th;                                    // clamp map: the parameter is p
+        } else if (QQA_RECOMPUTE_P) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pp.f[k] = sigmoid_c(th.f[k]);   // == p_cur (same contract function)
+        } else {
+          pp = ld8(V.p_cur + at);
+        }
         V8 pn = pp;
         const int s0 = b * P.SB + col8 * 8;          // local replica index of element 0
         if (s0 + 8 <= P.S_local) {

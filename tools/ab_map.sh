@@ -1,0 +1,9 @@
+#!/bin/bash
+for r in 1 2; do
+for v in norecomp recomp; do
+  for mp in sigmoid clamp; do
+    QQA_LIB_PATH=exp/libqqa_$v.so python bench.py --map $mp --anneal-steps 300 --steps 2 --warmup 1 --no-e2e --no-cpu 2>/dev/null \
+      | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$v', '$mp', 'kernel_ms %.4f' % r['avg_launch_ms'], 'sm_mhz', d['clocks']['sm_mhz'])"
+  done
+done
+done
