@@ -853,9 +853,15 @@ __device__ __forceinline__ void normalize_colours(float (&w)[KP], int K, float u
 // fixed-point sums of a chunk are reduced by shuffles within the group and, with
 // several chunks, meet in global u64 atomics (exact, order-free); chunk 0 zeroes
 // the variable's entries of the buffer used two steps later.
+#ifndef QQA_KARY_MINB
+#define QQA_KARY_MINB 3      // min CTAs per SM for k_step_K, KP > 8 (measured: q13 0.141 -> 0.098 ms at 3)
+#endif
+#ifndef QQA_KARY_U_WIDE
+#define QQA_KARY_U_WIDE 2    // neighbour rows in flight per lane for KP > 8
+#endif
 template <int KP, int MODE>
-__global__ void __launch_bounds__(256) k_step_K(const StepKParams P) {
-  constexpr int U = (KP <= 8) ? 4 : 2;                   // neighbour rows in flight per lane
+__global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 1)) k_step_K(const StepKParams P) {
+  constexpr int U = (KP <= 8) ? 4 : QQA_KARY_U_WIDE;     // neighbour rows in flight per lane
   const int L = P.L;
   const int lane = threadIdx.x & (L - 1);
   const int gl = threadIdx.x / L;
