@@ -275,6 +275,7 @@ struct qqa_handle {
   uint8_t* xbuf = nullptr;
   float4* sched = nullptr;     // per-step scalars of a persistent launch
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
+  int run_cta = 256;           // threads per CTA of k_run (1024: contiguous rows per SM)
   int cur = 0;   // p / c buffer of the current step (mod 2)
   int scur = 0;  // sums buffer of the current step (mod 3)
   int64_t step = 0;
@@ -307,13 +308,13 @@ int step_mode(const qqa_config& c) {
   return (c.map == QQA_MAP_CLAMP ? qqa::kModeClamp : 0) | (c.temperature > 0.0f ? qqa::kModeNoise : 0);
 }
 
-template <int L, int V>
+template <int L, int V, int CT>
 RunKernel run_for_mode(int mode) {
   switch (mode) {
-    case 0: return qqa::k_run<L, V, 0>;
-    case 1: return qqa::k_run<L, V, 1>;
-    case 2: return qqa::k_run<L, V, 2>;
-    default: return qqa::k_run<L, V, 3>;
+    case 0: return qqa::k_run<L, V, 0, CT>;
+    case 1: return qqa::k_run<L, V, 1, CT>;
+    case 2: return qqa::k_run<L, V, 2, CT>;
+    default: return qqa::k_run<L, V, 3, CT>;
   }
 }
 
@@ -327,13 +328,16 @@ StepKernel step_for_mode(int mode) {
   }
 }
 
-bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki, RunKernel* kr = nullptr) {
-#define QQA_CASE(L, V)                                   \
-  if (lanes == L && vpl == V) {                          \
-    ks = step_for_mode<L, V>(mode);                      \
-    ki = qqa::k_init<L, V>;                              \
-    if (kr) *kr = run_for_mode<L, V>(mode);              \
-    return true;                                         \
+// run_cta: 1024 (contiguous rows per SM) or 256 threads per CTA of the persistent kernel (VPL 1 only).
+bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki, RunKernel* kr = nullptr,
+                  int run_cta = 256) {
+#define QQA_CASE(L, V)                                                                  \
+  if (lanes == L && vpl == V) {                                                         \
+    ks = step_for_mode<L, V>(mode);                                                     \
+    ki = qqa::k_init<L, V>;                                                             \
+    if (kr) *kr = (V == 1 && run_cta == 1024) ? run_for_mode<L, 1, 1024>(mode)          \
+                                              : run_for_mode<L, V, 256>(mode);          \
+    return true;                                                                        \
   }
   QQA_CASE(1, 1) QQA_CASE(2, 1) QQA_CASE(4, 1) QQA_CASE(8, 1) QQA_CASE(16, 1)
   QQA_CASE(32, 1) QQA_CASE(32, 2) QQA_CASE(32, 4)
@@ -373,10 +377,10 @@ float kt_kary(int K, int alpha, float gamma) {
   return (float)(-(double)gamma * cK * (double)alpha * (double)K);
 }
 
-int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& grid) {
+int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& grid, int threads = 256) {
   int per_sm = 0;
-  QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
-  const int need = (int)std::max<int64_t>(1, std::min<int64_t>(INT32_MAX, (items * lanes + 255) / 256));
+  QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
+  const int need = (int)std::max<int64_t>(1, std::min<int64_t>(INT32_MAX, (items * lanes + threads - 1) / threads));
   grid = std::max(1, std::min(need, std::max(1, per_sm) * sm_count));
   return QQA_OK;
 }
@@ -532,7 +536,7 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
   StepKernel ks;
   InitKernel ki;
   RunKernel kr = nullptr;
-  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki, &kr);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki, &kr, h->run_cta);
   const qqa_config& c = h->cfg;
   qqa::RunParams R{};
   qqa::StepParams& P = R.P;
@@ -573,7 +577,8 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
     void* args[] = {(void*)&R};
     int st;
     if ((st = record_start(h))) return st;
-    QQA_CUDA(cudaLaunchCooperativeKernel((const void*)kr, dim3(h->grid_run), dim3(256), args, 0, h->stream));
+    QQA_CUDA(cudaLaunchCooperativeKernel((const void*)kr, dim3(h->grid_run), dim3(h->run_cta), args, 0,
+                                         h->stream));
     h->launches++;
     if (h->profiling) {   // one launch = nk steps: per-step kernel time = span / nk
       QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
@@ -890,14 +895,22 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     StepKernel ks;
     InitKernel ki;
     RunKernel kr = nullptr;
-    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki, &kr))
+    // contiguous-row persistent CTAs when the kernel fits 64 registers (VPL 1) and the work
+    // fills every SM with a 1024-thread CTA (measured: profiles/r1_design_iterations.md)
+    h->run_cta = (s.vpl == 1 && (int64_t)s.n * s.lanes >= (int64_t)h->sm_count * 1024) ? 1024 : 256;
+    if (const char* env = std::getenv("QQA_RUN_CTA")) h->run_cta = (std::atoi(env) == 1024 && s.vpl == 1) ? 1024 : 256;
+    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki, &kr, h->run_cta))
       return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
     if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
     {  // persistent kernel: every CTA must be co-resident (cooperative launch)
       int coop = 0;
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
-      if (coop && s.B == 1 && (st = grid_for((const void*)kr, h->sm_count, s.n, s.lanes, h->grid_run)))
-        return cleanup(st);
+      if (coop && s.B == 1) {
+        // no shared memory in k_run: give the SM's unified L1 / shared storage to L1
+        QQA_CUDA_C(cudaFuncSetAttribute((const void*)kr, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+        if ((st = grid_for((const void*)kr, h->sm_count, s.n, s.lanes, h->grid_run, h->run_cta)))
+          return cleanup(st);
+      }
     }
     h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
     if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);

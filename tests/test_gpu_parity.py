@@ -375,3 +375,21 @@ def test_persistent_equals_launch_per_step(Q, monkeypatch, problem, S, mp, T):
         assert np.array_equal(sa[k], sb[k]), k
     assert ra.best_replica == rb.best_replica and np.array_equal(ra.best_x, rb.best_x)
     assert la == (steps + 4095) // 4096 and lb == 2 * steps
+
+
+@pytest.mark.parametrize("cta", ["1024", "256"])
+def test_persistent_cta_layouts_identical(Q, monkeypatch, cta):
+    """Contiguous-row 1024-thread CTAs and strided 256-thread CTAs of the persistent kernel give the
+    launch-per-step result bit for bit (c2-like batch of small instances)."""
+    gs = [gen.erdos_renyi(300, 0.1, 60 + k) for k in range(6)]
+    U, gor = gen.disjoint_union(gs)
+    gam = oracle.schedule(-2.0, 0.1, 300)[:80]
+    monkeypatch.setenv("QQA_RUN_CTA", cta)
+    monkeypatch.setenv("QQA_PERSISTENT", "1")
+    a = Q.Solver(U.rowptr, U.colidx, Q.make_config("mis", S_total=72, seed=3), group_of_row=gor)
+    a.run(gam)
+    monkeypatch.setenv("QQA_PERSISTENT", "0")
+    b = Q.Solver(U.rowptr, U.colidx, Q.make_config("mis", S_total=72, seed=3), group_of_row=gor)
+    b.run(gam)
+    for k in ("theta", "m", "v", "p"):
+        assert np.array_equal(a.get_state()[k], b.get_state()[k]), k
