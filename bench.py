@@ -162,6 +162,9 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+args_lr_override = [None]
+
+
 def workload_config(w, world):
     g, _ = w.batched()
     S_l = w.S // world
@@ -171,6 +174,10 @@ def workload_config(w, world):
         extra.update(map=w.map, temperature=w.temperature)
     if w.n_colors:
         extra.update(n_colors=w.n_colors)
+    if w.alpha != 2:
+        extra.update(alpha=w.alpha)
+    if args_lr_override[0] is not None:
+        extra.update(lr=w.lr)
     return {"workload": w.name, "problem": w.problem, "recipe": w.recipe, "N": g.n, "nnz": g.nnz, "S": w.S,
             "S_local": S_l, "anneal_steps": w.steps, "instances": len(w.graphs), **extra,
             "parallelism": (f"replica-sharded x{world}" if world > 1 else "single GPU")
@@ -189,6 +196,8 @@ def main():
     ap.add_argument("--map", default=None, choices=["sigmoid", "clamp"],
                     help="override the map (clamp = the paper's sensitive transition, NEXT-1)")
     ap.add_argument("--temperature", type=float, default=None, help="Langevin T (NEXT-2; the paper: 0.001)")
+    ap.add_argument("--alpha", type=int, default=None, help="override the alpha-entropy exponent (the paper: 4, P:244)")
+    ap.add_argument("--lr", type=float, default=None, help="override the AdamW learning rate (the paper: 1, 0.1 or 0.01, P:670)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--anneal-steps", type=int, default=None, help="override T (diagnostics only)")
     ap.add_argument("--cpu-sample-steps", type=int, default=20)
@@ -205,6 +214,11 @@ def main():
         w.map = args.map
     if args.temperature is not None:
         w.temperature = args.temperature
+    if args.alpha is not None:
+        w.alpha = args.alpha
+    if args.lr is not None:
+        w.lr = args.lr
+        args_lr_override[0] = args.lr
     if args.impl == "reference":
         run_reference(args, w)
         return
