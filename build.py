@@ -28,23 +28,45 @@ def nccl_dir() -> str:
 
 
 def build_qqa(force=False, verbose=False, out=None, defines=()) -> str:
+    """Compile every csrc/*.cu to an object in parallel (one translation unit per step mode, one for
+    the K-ary kernels, the host engine), then link libqqa.so against torch's NCCL."""
+    from concurrent.futures import ThreadPoolExecutor
+
     srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
-    deps = srcs + sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "qqa.h")]
+    deps = srcs + sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + \
+        sorted(glob.glob(os.path.join(PKG, "csrc", "*.h"))) + [os.path.join(ROOT, "include", "qqa.h")]
     lib = out or LIB
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in deps):
         return lib
     os.makedirs(os.path.dirname(lib), exist_ok=True)
+    objdir = os.path.join(os.path.dirname(lib), "obj_" + os.path.splitext(os.path.basename(lib))[0])
+    os.makedirs(objdir, exist_ok=True)
     nd = nccl_dir()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
-           "-fmad=false",                        # fp32 contract: never contract a*b+c
-           "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
-           *[f"-D{d}" for d in defines], "-o", lib, *srcs]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17",
+             "-fmad=false",                        # fp32 contract: never contract a*b+c (DESIGN.md §3)
+             "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+             *[f"-D{d}" for d in defines]]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        flags.insert(0, "-Xptxas=-v")
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC, *flags, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode:
+            sys.stdout.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise subprocess.CalledProcessError(r.returncode, cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, srcs))
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", lib, *objs,
+                           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+                           "-Xlinker", "-rpath," + os.path.join(nd, "lib")])
     return lib
 
 

@@ -1,0 +1,19 @@
+// k_kary.cu -- the K-ary (graph colouring, NEXT-4) kernel instantiations.
+#define QQA_INST_ONLY
+#include "qqa_dispatch.h"
+
+namespace qqa {
+bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp) {
+  const bool noise = (mode & kModeNoise) != 0;
+#define QQA_KCASE(KPV)                                            \
+  if (KP == KPV) {                                                \
+    ks = noise ? k_step_K<KPV, kModeNoise> : k_step_K<KPV, 0>;    \
+    ki = k_init_K<KPV>;                                           \
+    kp = k_pack_K<KPV>;                                           \
+    return true;                                                  \
+  }
+  QQA_KCASE(4) QQA_KCASE(8) QQA_KCASE(12) QQA_KCASE(16)
+#undef QQA_KCASE
+  return false;
+}
+}  // namespace qqa

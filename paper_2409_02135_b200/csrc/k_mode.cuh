@@ -1,0 +1,31 @@
+// k_mode.cuh -- body of k_mode<M>.cu: the k_step / k_run instantiations of one step mode.
+#pragma once
+#define QQA_INST_ONLY
+#include "qqa_dispatch.h"
+
+namespace qqa {
+template <int M, int CT>
+RunKernel run_for(int lanes, int vpl) {
+#define QQA_RCASE(L, V) \
+  if (lanes == L && vpl == V) return k_run<L, V, M, (V == 1 ? CT : 256)>;
+  QQA_RCASE(1, 1) QQA_RCASE(2, 1) QQA_RCASE(4, 1) QQA_RCASE(8, 1) QQA_RCASE(16, 1)
+  QQA_RCASE(32, 1) QQA_RCASE(32, 2) QQA_RCASE(32, 4)
+#undef QQA_RCASE
+  return nullptr;
+}
+
+template <int M>
+StepKernel step_for(int lanes, int vpl) {
+#define QQA_SCASE(L, V) \
+  if (lanes == L && vpl == V) return k_step<L, V, M>;
+  QQA_SCASE(1, 1) QQA_SCASE(2, 1) QQA_SCASE(4, 1) QQA_SCASE(8, 1) QQA_SCASE(16, 1)
+  QQA_SCASE(32, 1) QQA_SCASE(32, 2) QQA_SCASE(32, 4)
+#undef QQA_SCASE
+  return nullptr;
+}
+
+template <int M>
+RunKernel run_kernel_for(int lanes, int vpl, int cta) {
+  return (cta == 1024 && vpl == 1) ? run_for<M, 1024>(lanes, vpl) : run_for<M, 256>(lanes, vpl);
+}
+}  // namespace qqa

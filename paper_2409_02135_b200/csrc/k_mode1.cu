@@ -1,0 +1,7 @@
+// k_mode1.cu -- k_step / k_run of step mode 1 (bit 0 clamp, bit 1 Langevin noise).
+#include "k_mode.cuh"
+
+namespace qqa {
+StepKernel step_kernel_m1(int lanes, int vpl) { return step_for<1>(lanes, vpl); }
+RunKernel run_kernel_m1(int lanes, int vpl, int cta) { return run_kernel_for<1>(lanes, vpl, cta); }
+}  // namespace qqa

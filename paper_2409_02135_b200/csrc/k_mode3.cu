@@ -1,0 +1,7 @@
+// k_mode3.cu -- k_step / k_run of step mode 3 (bit 0 clamp, bit 1 Langevin noise).
+#include "k_mode.cuh"
+
+namespace qqa {
+StepKernel step_kernel_m3(int lanes, int vpl) { return step_for<3>(lanes, vpl); }
+RunKernel run_kernel_m3(int lanes, int vpl, int cta) { return run_kernel_for<3>(lanes, vpl, cta); }
+}  // namespace qqa

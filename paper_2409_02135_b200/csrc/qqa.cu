@@ -5,7 +5,7 @@
 // communicator attached it follows it with one ncclAllReduce of the 2n int64
 // replica-statistic sums (the only cross-GPU exchange of the method, Eq. 10).
 #include "qqa.h"
-#include "qqa_kernels.cuh"
+#include "qqa_dispatch.h"
 
 #include <nccl.h>
 
@@ -298,9 +298,9 @@ struct qqa_handle {
 
 namespace {
 
-using StepKernel = void (*)(const qqa::StepParams);
+using StepKernel = qqa::StepKernel;
 using InitKernel = void (*)(const qqa::InitParams);
-using RunKernel = void (*)(const qqa::RunParams);
+using RunKernel = qqa::RunKernel;
 
 // Step-kernel mode: bit 0 clamp map, bit 1 Langevin noise (template, so the
 // default sigmoid / no-noise kernel carries none of the optional code).
@@ -308,41 +308,26 @@ int step_mode(const qqa_config& c) {
   return (c.map == QQA_MAP_CLAMP ? qqa::kModeClamp : 0) | (c.temperature > 0.0f ? qqa::kModeNoise : 0);
 }
 
-template <int L, int V, int CT>
-RunKernel run_for_mode(int mode) {
-  switch (mode) {
-    case 0: return qqa::k_run<L, V, 0, CT>;
-    case 1: return qqa::k_run<L, V, 1, CT>;
-    case 2: return qqa::k_run<L, V, 2, CT>;
-    default: return qqa::k_run<L, V, 3, CT>;
-  }
-}
-
 template <int L, int V>
-StepKernel step_for_mode(int mode) {
-  switch (mode) {
-    case 0: return qqa::k_step<L, V, 0>;
-    case 1: return qqa::k_step<L, V, 1>;
-    case 2: return qqa::k_step<L, V, 2>;
-    default: return qqa::k_step<L, V, 3>;
-  }
-}
+InitKernel init_for() { return qqa::k_init<L, V>; }
 
 // run_cta: 1024 (contiguous rows per SM) or 256 threads per CTA of the persistent kernel (VPL 1 only).
+// The k_step / k_run instantiations live in k_mode<mode>.cu (compiled in parallel).
 bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki, RunKernel* kr = nullptr,
                   int run_cta = 256) {
-#define QQA_CASE(L, V)                                                                  \
-  if (lanes == L && vpl == V) {                                                         \
-    ks = step_for_mode<L, V>(mode);                                                     \
-    ki = qqa::k_init<L, V>;                                                             \
-    if (kr) *kr = (V == 1 && run_cta == 1024) ? run_for_mode<L, 1, 1024>(mode)          \
-                                              : run_for_mode<L, V, 256>(mode);          \
-    return true;                                                                        \
+  switch (mode) {
+    case 0: ks = qqa::step_kernel_m0(lanes, vpl); if (kr) *kr = qqa::run_kernel_m0(lanes, vpl, run_cta); break;
+    case 1: ks = qqa::step_kernel_m1(lanes, vpl); if (kr) *kr = qqa::run_kernel_m1(lanes, vpl, run_cta); break;
+    case 2: ks = qqa::step_kernel_m2(lanes, vpl); if (kr) *kr = qqa::run_kernel_m2(lanes, vpl, run_cta); break;
+    default: ks = qqa::step_kernel_m3(lanes, vpl); if (kr) *kr = qqa::run_kernel_m3(lanes, vpl, run_cta); break;
   }
-  QQA_CASE(1, 1) QQA_CASE(2, 1) QQA_CASE(4, 1) QQA_CASE(8, 1) QQA_CASE(16, 1)
-  QQA_CASE(32, 1) QQA_CASE(32, 2) QQA_CASE(32, 4)
-#undef QQA_CASE
-  return false;
+  ki = nullptr;
+#define QQA_ICASE(L, V) \
+  if (lanes == L && vpl == V) ki = init_for<L, V>();
+  QQA_ICASE(1, 1) QQA_ICASE(2, 1) QQA_ICASE(4, 1) QQA_ICASE(8, 1) QQA_ICASE(16, 1)
+  QQA_ICASE(32, 1) QQA_ICASE(32, 2) QQA_ICASE(32, 4)
+#undef QQA_ICASE
+  return ks != nullptr && ki != nullptr;
 }
 
 uint64_t mix64_host(uint64_t z) {
@@ -353,22 +338,12 @@ uint64_t mix64_host(uint64_t z) {
 }
 
 // ------------------------------------------------------------- K-ary kernels
-using StepKKernel = void (*)(const qqa::StepKParams);
-using InitKKernel = void (*)(const qqa::InitKParams);
-using PackKKernel = void (*)(const float*, uint8_t*, int, int, int);
+using StepKKernel = qqa::StepKKernel;
+using InitKKernel = qqa::InitKKernel;
+using PackKKernel = qqa::PackKKernel;
 
 bool pick_kary(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp) {
-  const bool noise = (mode & qqa::kModeNoise) != 0;
-#define QQA_KCASE(KPV)                                                          \
-  if (KP == KPV) {                                                              \
-    ks = noise ? qqa::k_step_K<KPV, qqa::kModeNoise> : qqa::k_step_K<KPV, 0>;   \
-    ki = qqa::k_init_K<KPV>;                                                    \
-    kp = qqa::k_pack_K<KPV>;                                                    \
-    return true;                                                                \
-  }
-  QQA_KCASE(4) QQA_KCASE(8) QQA_KCASE(12) QQA_KCASE(16)
-#undef QQA_KCASE
-  return false;
+  return qqa::kary_kernels(KP, mode, ks, ki, kp);   // k_kary.cu
 }
 
 // k_t of the K-ary entropy: -gamma c_K alpha K, c_K = 1/((K-1)((K-1)^(alpha-1) + 1)) (host double -> fp32)

@@ -1,0 +1,27 @@
+// qqa_dispatch.h -- kernel pointers of the template kernels, one translation unit per step
+// mode (k_mode0..3.cu) and one for the K-ary kernels (k_kary.cu), so the library compiles in
+// parallel. Only plain host functions cross translation units (no extern kernel templates).
+#pragma once
+#include "qqa_kernels.cuh"
+
+namespace qqa {
+using StepKernel = void (*)(const StepParams);
+using RunKernel = void (*)(const RunParams);
+using StepKKernel = void (*)(const StepKParams);
+using InitKKernel = void (*)(const InitKParams);
+using PackKKernel = void (*)(const float*, uint8_t*, int, int, int);
+
+// k_step<lanes, vpl, MODE> and k_run<lanes, vpl, MODE, cta> (cta 1024 only for vpl 1); nullptr if
+// no kernel exists for (lanes, vpl).
+StepKernel step_kernel_m0(int lanes, int vpl);
+StepKernel step_kernel_m1(int lanes, int vpl);
+StepKernel step_kernel_m2(int lanes, int vpl);
+StepKernel step_kernel_m3(int lanes, int vpl);
+RunKernel run_kernel_m0(int lanes, int vpl, int cta);
+RunKernel run_kernel_m1(int lanes, int vpl, int cta);
+RunKernel run_kernel_m2(int lanes, int vpl, int cta);
+RunKernel run_kernel_m3(int lanes, int vpl, int cta);
+
+// K-ary kernels for KP in {4, 8, 12, 16}; false otherwise.
+bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);
+}  // namespace qqa

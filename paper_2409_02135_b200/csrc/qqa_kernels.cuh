@@ -357,6 +357,7 @@ __device__ __forceinline__ unsigned group_mask() {
   return (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
 }
 
+#ifndef QQA_INST_ONLY   // non-template kernels: compiled once, in qqa.cu
 // K0: per-variable replica mean / STD of the current p, once per step:
 // (mu_i, STD_i) from the shift c_i and the (all-rank) fixed-point sums; the
 // shift of the next step's sums is mu_i (written to c_next).
@@ -369,6 +370,8 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
     c_next[i] = mu;
   }
 }
+
+#endif  // QQA_INST_ONLY
 
 // K2: the fused step. Per item (b, i): gather q = A p over block b (4 neighbour
 // rows in flight per lane, CSR-order adds; the first row initialises the sum,
@@ -636,6 +639,7 @@ __global__ void __launch_bounds__(256) k_init(const InitParams P) {
   }
 }
 
+#ifndef QQA_INST_ONLY   // non-template kernels: compiled once, in qqa.cu
 // --------------------------------------------------------- graph checks
 // Original CSR: bit 1: column out of range, bit 2: row not strictly ascending
 // (unsorted / duplicate), bit 3: self-loop, bit 4: asymmetric (j's row lacks i).
@@ -809,6 +813,8 @@ __global__ void k_extract_groups(const uint32_t* __restrict__ X, const int* __re
     out[i] = (s >= 0 && s < S_local) ? (uint8_t)((X[(size_t)i * W + (s >> 5)] >> (s & 31)) & 1u) : (uint8_t)0;
   }
 }
+
+#endif  // QQA_INST_ONLY
 
 // ======================================================== K-ary (NEXT-4)
 // Graph colouring with K <= KP colours (App. B, map P:672-676, energy
@@ -1050,6 +1056,7 @@ __global__ void k_pack_K(const float* __restrict__ Pm, uint8_t* __restrict__ X8,
   }
 }
 
+#ifndef QQA_INST_ONLY   // non-template kernels: compiled once, in qqa.cu
 // K4 for K-ary: conflicts per replica; lane = replica 32 w + lane, warp k takes word k % W and the
 // row chunk [c CH, (c+1) CH), c = k / W. counts[s][3] = (0, conflicts, |E| - conflicts) (the last
 // term is added by the host-known |E| in k_conflicts_finish).
@@ -1083,5 +1090,7 @@ __global__ void k_extract_K(const uint8_t* __restrict__ X8, int n, int S, int s_
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = X8[(size_t)i * S + s_local];
 }
+
+#endif  // QQA_INST_ONLY
 
 }  // namespace qqa
