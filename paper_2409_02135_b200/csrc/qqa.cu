@@ -498,6 +498,8 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
   return QQA_OK;
 }
 
+int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps);
+
 // Persistent path (k_run): one cooperative launch per chunk of <= kSchedCap steps. Used for
 // one-GPU, unblocked problems of up to 2^24 replica-variables (L2-resident / launch-bound);
 // QQA_PERSISTENT=0/1 overrides. Bit-identical to the launch-per-step path.
@@ -552,8 +554,16 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
     void* args[] = {(void*)&R};
     int st;
     if ((st = record_start(h))) return st;
-    QQA_CUDA(cudaLaunchCooperativeKernel((const void*)kr, dim3(h->grid_run), dim3(h->run_cta), args, 0,
-                                         h->stream));
+    const cudaError_t le = cudaLaunchCooperativeKernel((const void*)kr, dim3(h->grid_run), dim3(h->run_cta), args,
+                                                       0, h->stream);
+    if (le == cudaErrorCooperativeLaunchTooLarge) {
+      // the grid cannot be co-resident now (e.g. a shared GPU): the launch-per-step path
+      // runs the remaining steps (bit-identical) and the handle stops using k_run
+      (void)cudaGetLastError();   // (the unmatched start event is re-recorded by the next step)
+      h->grid_run = 0;
+      return do_steps(h, gamma + k0, n_steps - k0);
+    }
+    QQA_CUDA(le);
     h->launches++;
     if (h->profiling) {   // one launch = nk steps: per-step kernel time = span / nk
       QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));

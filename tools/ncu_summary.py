@@ -16,7 +16,9 @@ KEYS = re.compile(r"^(gpu__time_duration.sum|dram__bytes_(read|write).sum|dram__
                   r"launch__grid_size|launch__block_size|launch__occupancy_limit_registers|smsp__inst_executed.sum|"
                   r"smsp__issue_active.avg.pct_of_peak_sustained_active|sm__throughput.avg.pct_of_peak_sustained_elapsed|"
                   r"smsp__average_warps_issue_stalled_(long_scoreboard|wait|short_scoreboard|not_selected|branch_resolving)_per_issue_active.ratio|"
-                  r"sm__sass_inst_executed_op_global_ld.sum|sm__sass_inst_executed_op_global_st.sum)$")
+                  r"sm__sass_inst_executed_op_global_ld.sum|sm__sass_inst_executed_op_global_st.sum|"
+                  r"l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum|l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum|"
+                  r"sm__maximum_warps_per_active_cycle_pct|sm__warps_active.avg.per_cycle_active)$")
 
 
 def launches(path):
