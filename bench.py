@@ -200,7 +200,8 @@ def main():
     ap.add_argument("--lr", type=float, default=None, help="override the AdamW learning rate (the paper: 1, 0.1 or 0.01, P:670)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--anneal-steps", type=int, default=None, help="override T (diagnostics only)")
-    ap.add_argument("--cpu-sample-steps", type=int, default=20)
+    ap.add_argument("--cpu-sample-steps", type=int, default=60, help="annealing steps of the cpu_baseline sample "
+                    "(c5: about 15 s on 16 cores)")
     ap.add_argument("--ref-sample-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
