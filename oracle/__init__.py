@@ -27,7 +27,8 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 MIS, MAXCUT, MAXCLIQUE = 0, 1, 2
-PROBLEM_IDS = {"mis": MIS, "maxcut": MAXCUT, "maxclique": MAXCLIQUE}
+MAXCLIQUE_SPARSE = 4   # printed clique relaxation on the original graph
+PROBLEM_IDS = {"mis": MIS, "maxcut": MAXCUT, "maxclique": MAXCLIQUE, "maxclique_sparse": MAXCLIQUE_SPARSE}
 
 
 def build(force: bool = False) -> str:
@@ -111,6 +112,8 @@ def _L():
         lib.oc_eval_K.restype = None
         lib.oc_eval_K.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_int32, f32, u8, i64, f64,
                                   ctypes.POINTER(ctypes.c_int32)]
+        lib.oc_colsum.restype = None
+        lib.oc_colsum.argtypes = [ctypes.c_int32, ctypes.c_int32, f32, f32]
         lib.oc_complement.restype = ctypes.c_int64
         lib.oc_complement.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_void_p, ctypes.c_void_p]
         _lib = lib
@@ -384,3 +387,11 @@ def evaluate_K(g, P: np.ndarray):
     _L().oc_eval_K(n, np.ascontiguousarray(g.rowptr, np.int64), np.ascontiguousarray(g.colidx, np.int32), S, K,
                    P, X, counts, energy, ctypes.byref(best))
     return counts, energy, int(best.value), X
+
+
+def colsum(P) -> np.ndarray:
+    """T_s of the printed clique relaxation: (float)((double)sum_k llrint(p_ks 2^40) 2^-40)."""
+    P = np.ascontiguousarray(P, np.float32)
+    out = np.empty(P.shape[1], np.float32)
+    _L().oc_colsum(P.shape[0], P.shape[1], P, out)
+    return out

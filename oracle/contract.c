@@ -20,6 +20,10 @@
  *   dR/dtheta = dR/dp * p (1 - p)
  *   AdamW, decoupled weight decay
  *   x = Theta(p - 1/2) evaluated as theta >= 0
+ *   max clique, printed relaxation on the original graph (problem 4):
+ *     dl/dp_i = -1 + lam ((T - 1/2) - q_i), T = sum_k p_k of the replica, as
+ *     fl(fl(lam fl(fl(T_f - 1/2) - q)) - 1) with T_f = (float)((double)C 2^-40),
+ *     C = sum_k llrint(p_k 2^40) (int64, exact)
  *   map = CLAMP (sensitive transition, NEXT-1): AdamW on p itself with
  *     dR/dp (no chain factor), then p = Clamp(p') into [0, 1]         Eq. 11
  *     x = Theta(p - 1/2) evaluated as p >= 1/2
@@ -45,7 +49,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-enum { OC_MIS = 0, OC_MAXCUT = 1, OC_MAXCLIQUE = 2 };
+enum { OC_MIS = 0, OC_MAXCUT = 1, OC_MAXCLIQUE = 2, OC_MAXCLIQUE_SPARSE = 4 };
 
 typedef struct {
     int32_t problem;     /* 0 MIS, 1 Max-Cut, 2 max clique (caller passes the complement CSR) */
@@ -261,7 +265,8 @@ void oc_init(int32_t n, const oc_cfg* cf, float* theta, float* m, float* v, floa
  * updates th/mm/vv (row i, length S) in place; writes p_new (row i) and the
  * row's new stats (shift = this step's mean). */
 static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, const int32_t* colidx,
-                       const oc_cfg* cf, const float* sc, const float* p, float* th, float* mm, float* vv,
+                       const oc_cfg* cf, const float* sc, const float* Tcol, const float* p, float* th, float* mm,
+                       float* vv,
                        float c_i, int64_t sD_i, int64_t sD2_i,
                        float* p_new, float* c_new, int64_t* sD_new, int64_t* sD2_new, float* q) {
     const int32_t S = cf->S;
@@ -294,7 +299,9 @@ static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, co
         float ep = e;
         for (int32_t a = 2; a < cf->alpha; ++a) ep = ep * e;   /* (2p-1)^(alpha-1) */
         const float ent = kt * ep;
-        const float obj = (cf->problem == OC_MAXCUT) ? (2.0f * q[s] - degf) : (lam * q[s] - 1.0f);
+        const float obj = (cf->problem == OC_MAXCUT) ? (2.0f * q[s] - degf)
+                          : (cf->problem == OC_MAXCLIQUE_SPARSE) ? (lam * ((Tcol[s] - 0.5f) - q[s]) - 1.0f)
+                          : (lam * q[s] - 1.0f);
         const float com = (sd >= 1e-6f) ? (-ac) * ((pi - mu) / sd) : 0.0f;
         const float gp = (obj + ent) + com;
         /* sigmoid: chain rule dR/dtheta = dR/dp p (1-p); clamp: the parameter is p */
@@ -321,6 +328,16 @@ static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, co
     return nonfinite_flag;
 }
 
+/* Per-replica column sums of p for the printed clique relaxation: T_s = (float)((double)C_s 2^-40),
+ * C_s = sum_k llrint(p_ks 2^40) (exact int64, order-free). */
+void oc_colsum(int32_t n, int32_t S, const float* p, float* T) {
+    for (int32_t s = 0; s < S; ++s) {
+        int64_t C = 0;
+        for (int32_t k = 0; k < n; ++k) C += llrintf(p[(size_t)k * S + s] * 0x1p40f);
+        T[s] = (float)((double)C * 0x1p-40);
+    }
+}
+
 /* Run n_steps annealing steps. gamma[k] is gamma for step k; Adam index t = t0 + k + 1.
  * State arrays are updated in place (p/c/sums hold the state of the current p).
  * Returns 0, or 5 if a non-finite theta appeared (SPEC.md:396 abort). */
@@ -333,12 +350,14 @@ int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg
     float* c2 = (float*)malloc(sizeof(float) * (n ? n : 1));
     int64_t* d2a = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
     int64_t* d2b = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    float* Tcol = (float*)malloc(sizeof(float) * (S ? S : 1));
     int bad = 0;
     for (int64_t k = 0; k < n_steps && !bad; ++k) {
         float sc[4];
         oc_step_scalars(cf, t0 + k + 1, gamma[k], sc);
         const int thr = cf->threads > 1 ? cf->threads : 1;
         const int64_t t = t0 + k + 1;
+        if (cf->problem == OC_MAXCLIQUE_SPARSE) oc_colsum(n, S, p, Tcol);
         (void)thr;
 #pragma omp parallel num_threads(thr) reduction(| : bad)
         {
@@ -346,7 +365,7 @@ int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg
 #pragma omp for schedule(static)
             for (int32_t i = 0; i < n; ++i) {
                 const size_t r = (size_t)i * S;
-                bad |= update_row(i, n, t, rowptr, colidx, cf, sc, p, theta + r, m + r, v + r,
+                bad |= update_row(i, n, t, rowptr, colidx, cf, sc, Tcol, p, theta + r, m + r, v + r,
                                   c[i], sumD[i], sumD2[i], p2 + r, &c2[i], &d2a[i], &d2b[i], q);
             }
             free(q);
@@ -356,7 +375,7 @@ int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg
         memcpy(sumD, d2a, sizeof(int64_t) * n);
         memcpy(sumD2, d2b, sizeof(int64_t) * n);
     }
-    free(p2); free(c2); free(d2a); free(d2b);
+    free(p2); free(c2); free(d2a); free(d2b); free(Tcol);
     return bad ? 5 : 0;
 }
 
@@ -374,16 +393,19 @@ void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const
     float sc[4];
     oc_step_scalars(cf, t, gamma_t, sc);
     float* q = (float*)malloc(sizeof(float) * (S ? S : 1));
+    float* Tcol = (float*)malloc(sizeof(float) * (S ? S : 1));
+    if (cf->problem == OC_MAXCLIQUE_SPARSE) oc_colsum(n, S, p, Tcol);
     for (int32_t k = 0; k < nrows; ++k) {
         const int32_t i = rows[k];
         const size_t r = (size_t)k * S;
         memcpy(theta_out + r, theta_rows + r, sizeof(float) * S);
         memcpy(m_out + r, m_rows + r, sizeof(float) * S);
         memcpy(v_out + r, v_rows + r, sizeof(float) * S);
-        (void)update_row(i, n, t, rowptr, colidx, cf, sc, p, theta_out + r, m_out + r, v_out + r,
+        (void)update_row(i, n, t, rowptr, colidx, cf, sc, Tcol, p, theta_out + r, m_out + r, v_out + r,
                    c[i], sumD[i], sumD2[i], p_out + r, &c_out[k], &sD_out[k], &sD2_out[k], q);
     }
     free(q);
+    free(Tcol);
 }
 
 /* ------------------------------------------------------- evaluation ---- */
@@ -408,6 +430,12 @@ void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t pr
             }
         }
     }
+    if (problem == OC_MAXCLIQUE_SPARSE)   /* complement counts: pairs in x minus edges in x; size(n-size) - cut */
+        for (int32_t s = 0; s < S; ++s) {
+            const int64_t sz = counts[3 * s + 0];
+            counts[3 * s + 1] = sz * (sz - 1) / 2 - counts[3 * s + 1];
+            counts[3 * s + 2] = sz * ((int64_t)n - sz) - counts[3 * s + 2];
+        }
     int32_t b = 0;
     for (int32_t s = 0; s < S; ++s) {
         energy[s] = (problem == OC_MAXCUT) ? -(double)counts[3 * s + 2]

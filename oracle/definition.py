@@ -32,7 +32,8 @@ import itertools
 import numpy as np
 
 MIS, MAXCUT, MAXCLIQUE = 0, 1, 2
-PROBLEM_IDS = {"mis": MIS, "maxcut": MAXCUT, "maxclique": MAXCLIQUE}
+MAXCLIQUE_SPARSE = 4   # the printed max-clique relaxation on the original graph (NEXT-3 option)
+PROBLEM_IDS = {"mis": MIS, "maxcut": MAXCUT, "maxclique": MAXCLIQUE, "maxclique_sparse": MAXCLIQUE_SPARSE}
 
 # STD below this is treated as a non-differentiable point: comm gradient 0
 # (reading R6; 0 lies in the subgradient set of sqrt at 0).
@@ -75,6 +76,9 @@ def relaxed_objective(problem, A: np.ndarray, P: np.ndarray, lam: float = 2.0) -
     if pid in (MIS, MAXCLIQUE):
         B = problem_adjacency(pid, A)
         return -P.sum(axis=0) + lam * np.einsum("is,ij,js->s", P, B, P) / 2.0
+    if pid == MAXCLIQUE_SPARSE:   # P:715 as printed: -1^T p + (lam/2)(1^T p (1^T p - 1) - p^T A p)
+        T = P.sum(axis=0)
+        return -T + lam / 2.0 * (T * (T - 1.0) - np.einsum("is,ij,js->s", P, A, P))
     if pid == MAXCUT:
         Z = 2.0 * P - 1.0
         iu, ju = np.nonzero(np.triu(A, 1))  # each undirected edge once (reading R15)
@@ -126,6 +130,9 @@ def grad_objective(problem, A, P, lam) -> np.ndarray:
     if pid in (MIS, MAXCLIQUE):
         B = problem_adjacency(pid, A)
         return -1.0 + lam * (B @ P)
+    if pid == MAXCLIQUE_SPARSE:   # d/dp_i of P:715 = -1 + (lam/2)(2 T - 1 - 2 (A p)_i), T = 1^T p per replica
+        T = P.sum(axis=0)[None, :]
+        return -1.0 + lam * ((T - 0.5) - A @ P)
     if pid == MAXCUT:
         return -A.sum(axis=1)[:, None] + 2.0 * (A @ P)
     raise ValueError(problem)
@@ -279,6 +286,8 @@ def counts(problem, A: np.ndarray, X: np.ndarray) -> np.ndarray:
     violations: #{(i<j) in E' : x_i = x_j = 1} with E' = E (MIS, Max-Cut) or the
     complement (max clique); cut: #{(i<j) in E : x_i != x_j}."""
     pid = _pid(problem)
+    if pid == MAXCLIQUE_SPARSE:   # the same counts as max clique on the complement
+        return counts(MAXCLIQUE, A, X)
     B = problem_adjacency(pid, A)
     X = X.astype(np.int64)
     n, S = X.shape
