@@ -79,6 +79,11 @@ typedef enum {
   QQA_MAXCUT = 1,     /* max cut, l = -sum_{(i,j) in E} (1 - (2x_i-1)(2x_j-1))/2       */
   QQA_MAXCLIQUE = 2,  /* max clique, solved as MIS on the complement graph (the library
                          builds the complement on the host at create; n <= 65536)                */
+  QQA_MAXCLIQUE_SPARSE = 4,  /* max clique with the relaxation exactly as printed at P:715, on the
+                         ORIGINAL graph: dl/dp_i = -1 + lambda((T - 1/2) - sum_{j in N(i)} p_j), T =
+                         sum_k p_k per replica (exact fixed-point column sums). No complement, so no
+                         n limit; at binary x the energy equals QQA_MAXCLIQUE's; counts are reported
+                         for the complement as QQA_MAXCLIQUE does. No batches.                 */
   QQA_COLORING = 3    /* graph colouring with K = n_colors colours (NEXT-4, App. B):
                          every variable is a row of K probabilities, s_K entropy, map
                          Clamp-then-normalise, AdamW on the probabilities,

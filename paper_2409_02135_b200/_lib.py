@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "qqa.h")
 QQA_OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "BAD_GRAPH", 3: "CUDA", 4: "COMM", 5: "NONFINITE",
           6: "UNSUPPORTED", 7: "WORKSPACE"}
-PROBLEMS = {"mis": 0, "maxcut": 1, "maxclique": 2, "coloring": 3}
+PROBLEMS = {"mis": 0, "maxcut": 1, "maxclique": 2, "coloring": 3, "maxclique_sparse": 4}
 MAPS = {"sigmoid": 0, "clamp": 1}
 
 

@@ -26,6 +26,7 @@ StepKernel step_for(int lanes, int vpl) {
 
 template <int M>
 RunKernel run_kernel_for(int lanes, int vpl, int cta) {
+  if (M & kModeSparseClique) return nullptr;   // its column sums need a pass between steps: no k_run
   return (cta == 1024 && vpl == 1) ? run_for<M, 1024>(lanes, vpl) : run_for<M, 256>(lanes, vpl);
 }
 }  // namespace qqa

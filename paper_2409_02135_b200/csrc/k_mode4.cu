@@ -1,0 +1,7 @@
+// k_mode4.cu -- k_step of step mode 4 (bit 0 clamp, bit 1 Langevin noise, bit 2 printed clique).
+#include "k_mode.cuh"
+
+namespace qqa {
+StepKernel step_kernel_m4(int lanes, int vpl) { return step_for<4>(lanes, vpl); }
+RunKernel run_kernel_m4(int lanes, int vpl, int cta) { return run_kernel_for<4>(lanes, vpl, cta); }
+}  // namespace qqa

@@ -60,7 +60,7 @@ struct Shape {
 
 struct Layout {
   size_t rowptr, colidx, rowptr_pad, colidx_pad, gor, theta, m, v, p0, p1, c0, c1, ms, s0, s1, s2, flag, X,
-      counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, sched, total;
+      counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, sched, cs0, cs1, total;
 };
 
 Layout make_layout(const Shape& s) {
@@ -98,6 +98,8 @@ Layout make_layout(const Shape& s) {
   L.gbeste = take((size_t)s.G * sizeof(double));
   L.xbuf = take((size_t)s.n);
   L.sched = take((size_t)kSchedCap * sizeof(float4));
+  L.cs0 = take((size_t)s.S_p * sizeof(long long));   // printed clique: column sums of p[0] / p[1]
+  L.cs1 = take((size_t)s.S_p * sizeof(long long));
   L.total = o;
   return L;
 }
@@ -106,8 +108,9 @@ int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
 
 int check_config(const qqa_config* c) {
   if (!c) return fail(QQA_ERR_INVALID_ARG, "config is NULL");
-  if (c->problem < 0 || c->problem > 3)
-    return fail(QQA_ERR_INVALID_ARG, "problem must be 0 (MIS), 1 (Max-Cut), 2 (max clique) or 3 (colouring)");
+  if (c->problem < 0 || c->problem > 4)
+    return fail(QQA_ERR_INVALID_ARG,
+                "problem must be 0 (MIS), 1 (Max-Cut), 2 (max clique), 3 (colouring) or 4 (max clique, sparse)");
   if (c->problem == QQA_COLORING && (c->n_colors < 2 || c->n_colors > 16))
     return fail(QQA_ERR_INVALID_ARG, "n_colors must be in 2..16 for QQA_COLORING");
   if (c->alpha < 2 || c->alpha > 16 || (c->alpha & 1)) return fail(QQA_ERR_INVALID_ARG, "alpha must be even, 2..16 (Eq. 7)");
@@ -182,6 +185,8 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   s.S_local = c->S_local;
   s.S_total = c->S_total;
   s.G = g->group_of_row ? g->n_groups : 1;
+  if (c->problem == QQA_MAXCLIQUE_SPARSE && g->group_of_row)
+    return fail(QQA_ERR_UNSUPPORTED, "batches (group_of_row) are not supported for the sparse max-clique relaxation");
   if (c->problem == QQA_COLORING) {
     if (g->group_of_row) return fail(QQA_ERR_UNSUPPORTED, "batches (group_of_row) are not supported for colouring");
     s.kary = true;
@@ -274,6 +279,7 @@ struct qqa_handle {
   double* gbeste = nullptr;
   uint8_t* xbuf = nullptr;
   float4* sched = nullptr;     // per-step scalars of a persistent launch
+  long long* colsum[2] = {nullptr, nullptr};   // printed clique: per-replica column sums of p[0] / p[1]
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
   int run_cta = 256;           // threads per CTA of k_run (1024: contiguous rows per SM)
   int cur = 0;   // p / c buffer of the current step (mod 2)
@@ -305,7 +311,8 @@ using RunKernel = qqa::RunKernel;
 // Step-kernel mode: bit 0 clamp map, bit 1 Langevin noise (template, so the
 // default sigmoid / no-noise kernel carries none of the optional code).
 int step_mode(const qqa_config& c) {
-  return (c.map == QQA_MAP_CLAMP ? qqa::kModeClamp : 0) | (c.temperature > 0.0f ? qqa::kModeNoise : 0);
+  return (c.map == QQA_MAP_CLAMP ? qqa::kModeClamp : 0) | (c.temperature > 0.0f ? qqa::kModeNoise : 0) |
+         (c.problem == QQA_MAXCLIQUE_SPARSE ? qqa::kModeSparseClique : 0);
 }
 
 template <int L, int V>
@@ -319,7 +326,11 @@ bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki, 
     case 0: ks = qqa::step_kernel_m0(lanes, vpl); if (kr) *kr = qqa::run_kernel_m0(lanes, vpl, run_cta); break;
     case 1: ks = qqa::step_kernel_m1(lanes, vpl); if (kr) *kr = qqa::run_kernel_m1(lanes, vpl, run_cta); break;
     case 2: ks = qqa::step_kernel_m2(lanes, vpl); if (kr) *kr = qqa::run_kernel_m2(lanes, vpl, run_cta); break;
-    default: ks = qqa::step_kernel_m3(lanes, vpl); if (kr) *kr = qqa::run_kernel_m3(lanes, vpl, run_cta); break;
+    case 3: ks = qqa::step_kernel_m3(lanes, vpl); if (kr) *kr = qqa::run_kernel_m3(lanes, vpl, run_cta); break;
+    case 4: ks = qqa::step_kernel_m4(lanes, vpl); if (kr) *kr = qqa::run_kernel_m4(lanes, vpl, run_cta); break;
+    case 5: ks = qqa::step_kernel_m5(lanes, vpl); if (kr) *kr = qqa::run_kernel_m5(lanes, vpl, run_cta); break;
+    case 6: ks = qqa::step_kernel_m6(lanes, vpl); if (kr) *kr = qqa::run_kernel_m6(lanes, vpl, run_cta); break;
+    default: ks = qqa::step_kernel_m7(lanes, vpl); if (kr) *kr = qqa::run_kernel_m7(lanes, vpl, run_cta); break;
   }
   ki = nullptr;
 #define QQA_ICASE(L, V) \
@@ -358,6 +369,23 @@ int grid_for(const void* kernel, int sm_count, int64_t items, int lanes, int& gr
   const int need = (int)std::max<int64_t>(1, std::min<int64_t>(INT32_MAX, (items * lanes + threads - 1) / threads));
   grid = std::max(1, std::min(need, std::max(1, per_sm) * sm_count));
   return QQA_OK;
+}
+
+// Printed clique relaxation: column sums of p[buf] into colsum[buf] (exact int64).
+int launch_colsum(qqa_handle* h, int buf) {
+  const Shape& s = h->s;
+  QQA_CUDA(cudaMemsetAsync(h->colsum[buf], 0, (size_t)s.S_p * sizeof(long long), h->stream));
+  if (s.n == 0) return QQA_OK;
+  const int T = std::max(s.S_p, (h->sm_count * 4 * 256) / s.S_p * s.S_p);
+  qqa::k_colsum<<<(T + 255) / 256, 256, 0, h->stream>>>(h->p[buf], s.n, s.SB, s.S_p, s.S_local, T,
+                                                        (unsigned long long*)h->colsum[buf]);
+  QQA_CUDA(cudaGetLastError());
+  h->launches++;
+  return QQA_OK;
+}
+
+int problem_kind(int problem) {   // the kernels' problem code (max clique = MIS on the complement)
+  return problem == QQA_MAXCUT ? qqa::kMAXCUT : problem == QQA_MAXCLIQUE_SPARSE ? qqa::kMAXCLIQUE_SPARSE : qqa::kMIS;
 }
 
 int launch_init_kary(qqa_handle* h, bool use_given, const float* c_given) {
@@ -416,6 +444,10 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   }
   if (h->comm) {
     QQA_NCCL(ncclAllReduce(h->sums[0], h->sums[0], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
+  }
+  if (h->cfg.problem == QQA_MAXCLIQUE_SPARSE) {
+    int st;
+    if ((st = launch_colsum(h, 0))) return st;
   }
   h->cur = 0;
   h->scur = 0;
@@ -504,7 +536,9 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps);
 // one-GPU, unblocked problems of up to 2^24 replica-variables (L2-resident / launch-bound);
 // QQA_PERSISTENT=0/1 overrides. Bit-identical to the launch-per-step path.
 bool use_persistent(const qqa_handle* h, int64_t n_steps) {
-  if (h->grid_run <= 0 || h->comm || h->s.B != 1 || h->s.kary || h->s.n == 0 || n_steps < 2) return false;
+  if (h->grid_run <= 0 || h->comm || h->s.B != 1 || h->s.kary || h->s.n == 0 || n_steps < 2 ||
+      h->cfg.problem == QQA_MAXCLIQUE_SPARSE)   // its column sums need a pass between steps
+    return false;
   if (const char* env = std::getenv("QQA_PERSISTENT")) return std::atoi(env) != 0;
   return (int64_t)h->s.n * h->s.S_p <= ((int64_t)1 << 24);
 }
@@ -521,7 +555,7 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
   P.row_begin = 0; P.row_end = h->s.n;
-  P.problem = c.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;
+  P.problem = problem_kind(c.problem);
   P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
   P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
   P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
@@ -590,7 +624,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
-  P.problem = c.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;  // clique = MIS on the complement
+  P.problem = problem_kind(c.problem);  // dense clique = MIS on the complement
   P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
   P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
   P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
@@ -610,6 +644,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
     const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
     P.var.p_cur = h->p[a]; P.var.p_next = h->p[b];
     P.ms = h->ms;
+    P.colsum = h->colsum[a];
     P.var.sums_next = h->sums[sb];
     P.var.sums_zero = (h->s.B > 1) ? h->sums[sz] : nullptr;
     const int C = (h->comm && h->s.n > 0) ? h->comm_chunks : 1;
@@ -639,6 +674,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
         }
       }
       if ((st = record_end(h))) return st;
+      if (c.problem == QQA_MAXCLIQUE_SPARSE && (st = launch_colsum(h, b))) return st;
       if (C > 1) {  // the next step's finalize needs every chunk's reduced sums
         QQA_CUDA(cudaEventRecord(h->chunk_ev[C], h->cstream));
         QQA_CUDA(cudaStreamWaitEvent(h->stream, h->chunk_ev[C], 0));
@@ -803,6 +839,8 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   h->gor = g->group_of_row ? (int*)(ws + L.gor) : nullptr;
   h->xbuf = (uint8_t*)(ws + L.xbuf);
   h->sched = (float4*)(ws + L.sched);
+  h->colsum[0] = (long long*)(ws + L.cs0);
+  h->colsum[1] = (long long*)(ws + L.cs1);
 
   // Graph -> device (int32 offsets). Max clique walks the complement graph.
   std::vector<int> rp32, ci_c;
@@ -890,7 +928,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     {  // persistent kernel: every CTA must be co-resident (cooperative launch)
       int coop = 0;
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
-      if (coop && s.B == 1) {
+      if (coop && s.B == 1 && kr) {   // (no k_run for the printed clique relaxation)
         // no shared memory in k_run: give the SM's unified L1 / shared storage to L1
         QQA_CUDA_C(cudaFuncSetAttribute((const void*)kr, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
         if ((st = grid_for((const void*)kr, h->sm_count, s.n, s.lanes, h->grid_run, h->run_cta)))
@@ -1077,11 +1115,17 @@ int evaluate_core(qqa_handle* h) {
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }
+  if (h->cfg.problem == QQA_MAXCLIQUE_SPARSE) {   // original-graph counts -> complement counts (G = 1)
+    qqa::k_clique_counts<<<std::max(1, std::min((s.S_local + 255) / 256, h->sm_count)), 256, 0, h->stream>>>(
+        (long long*)h->counts + 3 * (size_t)off, s.S_local, (long long)s.n);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
   if (h->comm && h->nranks > 1) {
     QQA_NCCL(ncclAllGather(h->counts + 3 * (size_t)off * s.G, h->counts, 3 * (size_t)s.S_local * s.G, ncclInt64,
                            h->comm, h->stream));
   }
-  const int prob = h->cfg.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;
+  const int prob = h->cfg.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;   // cliques: complement counts
   const long long* tot = (const long long*)h->counts;
   if (s.G > 1) {  // totals over instances = the energy of the union graph
     qqa::k_sum_groups<<<std::max(1, std::min((3 * s.S_total + 255) / 256, h->sm_count * 4)), 256, 0, h->stream>>>(

@@ -12,15 +12,23 @@ using InitKKernel = void (*)(const InitKParams);
 using PackKKernel = void (*)(const float*, uint8_t*, int, int, int);
 
 // k_step<lanes, vpl, MODE> and k_run<lanes, vpl, MODE, cta> (cta 1024 only for vpl 1); nullptr if
-// no kernel exists for (lanes, vpl).
+// no kernel exists for (lanes, vpl). MODE bit 2 (printed clique) has no k_run.
 StepKernel step_kernel_m0(int lanes, int vpl);
 StepKernel step_kernel_m1(int lanes, int vpl);
 StepKernel step_kernel_m2(int lanes, int vpl);
 StepKernel step_kernel_m3(int lanes, int vpl);
+StepKernel step_kernel_m4(int lanes, int vpl);
+StepKernel step_kernel_m5(int lanes, int vpl);
+StepKernel step_kernel_m6(int lanes, int vpl);
+StepKernel step_kernel_m7(int lanes, int vpl);
 RunKernel run_kernel_m0(int lanes, int vpl, int cta);
 RunKernel run_kernel_m1(int lanes, int vpl, int cta);
 RunKernel run_kernel_m2(int lanes, int vpl, int cta);
 RunKernel run_kernel_m3(int lanes, int vpl, int cta);
+RunKernel run_kernel_m4(int lanes, int vpl, int cta);   // nullptr: modes 4-7 run launch-per-step
+RunKernel run_kernel_m5(int lanes, int vpl, int cta);
+RunKernel run_kernel_m6(int lanes, int vpl, int cta);
+RunKernel run_kernel_m7(int lanes, int vpl, int cta);
 
 // K-ary kernels for KP in {4, 8, 12, 16}; false otherwise.
 bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);

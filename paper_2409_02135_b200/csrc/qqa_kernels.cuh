@@ -35,10 +35,11 @@
 
 namespace qqa {
 
-enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2, kCOLORING = 3 };
+enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2, kCOLORING = 3, kMAXCLIQUE_SPARSE = 4 };
 // Step-kernel mode (template): bit 0 = clamp map (Eq. 11),
-// bit 1 = Langevin noise (Eq. 9 / 11).
-enum : int { kModeClamp = 1, kModeNoise = 2 };
+// bit 1 = Langevin noise (Eq. 9 / 11), bit 2 = the printed clique relaxation on
+// the original graph (per-replica column sums enter the objective).
+enum : int { kModeClamp = 1, kModeNoise = 2, kModeSparseClique = 4 };
 
 #ifndef QQA_GATHER_U
 #define QQA_GATHER_U 4         // neighbour rows in flight per lane (multiple of 4)
@@ -286,6 +287,7 @@ struct StepParams {
   float* __restrict__ m;
   float* __restrict__ v;
   const float2* __restrict__ ms;        // [n] (mu_i, STD_i) of the current p (k_finalize)
+  const long long* __restrict__ colsum; // [S_p] sum_k rint(p_ks 2^40) of the current p (printed clique only)
   int* __restrict__ flag;               // bit 0: non-finite theta
   int n, SB, B, S_local;
   int row_begin, row_end;               // rows [row_begin, row_end) of this launch (comm overlap chunks)
@@ -302,15 +304,17 @@ struct StepParams {
 // chain factor, p = Clamp(th)); otherwise p = sigmoid(th). Returns p_next; bad
 // is set when the pre-map parameter is non-finite.
 template <int MODE>
-__device__ __forceinline__ float update_element(const StepParams& P, const StepVar& V, float q, float degf,
+__device__ __forceinline__ float update_element(const StepParams& P, const StepVar& V, float q, float aux,
                                                 float pi, float mu, float sd, float& th, float& mm, float& vv,
                                                 unsigned long long key, bool& bad) {
   const float e = fsub(fmul(2.0f, pi), 1.0f);
   float ep = e;
   for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);                 // (2p-1)^(alpha-1)
   const float ent = fmul(V.kt, ep);                                   // -2 alpha gamma (2p-1)^(alpha-1)
-  const float obj = (P.problem == kMAXCUT) ? fsub(fmul(2.0f, q), degf)   // -deg + 2q
-                                           : fsub(fmul(P.lam, q), 1.0f); // -1 + lambda q
+  // aux: the degree (Max-Cut) or the replica's column sum T (printed clique relaxation)
+  const float obj = (MODE & kModeSparseClique) ? fsub(fmul(P.lam, fsub(fsub(aux, 0.5f), q)), 1.0f)
+                    : (P.problem == kMAXCUT) ? fsub(fmul(2.0f, q), aux)                   // -deg + 2q
+                                             : fsub(fmul(P.lam, q), 1.0f);                // -1 + lambda q
   const float com = (sd >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, mu), sd)) : 0.0f;
   const float gp = fadd(fadd(obj, ent), com);
   const float g = (MODE & kModeClamp) ? gp                             // sensitive transition: d/dp
@@ -328,6 +332,14 @@ __device__ __forceinline__ float update_element(const StepParams& P, const StepV
   }
   th = w;
   return sigmoid_c(w);
+}
+
+// Per-element extra input of the objective: the variable's degree (Max-Cut), or the replica's column
+// sum T_s = (float)((double)C_s 2^-40) of the printed clique relaxation.
+template <int MODE>
+__device__ __forceinline__ float aux_of(const StepParams& P, float degf, int s) {
+  if (!(MODE & kModeSparseClique)) return degf;
+  return __double2float_rn(__dmul_rn(__ll2double_rn(__ldg(P.colsum + s)), 0x1p-40));
 }
 
 // Reduce the group's fixed-point partial sums and publish them for variable i.
@@ -464,7 +476,8 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         if (s0 + 8 <= P.S_local) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
+            pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, sd, th.f[k],
+                                           mm.f[k], vv.f[k],
                                            rkey + (unsigned long long)(s0 + k), bad);
             long long D, D2;
             stat_terms(pn.f[k], mu, D, D2);
@@ -474,7 +487,8 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (s0 + k < P.S_local) {
-              pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], degf, pp.f[k], mu, sd, th.f[k], mm.f[k], vv.f[k],
+              pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, sd, th.f[k],
+                                             mm.f[k], vv.f[k],
                                              rkey + (unsigned long long)(s0 + k), bad);
               long long D, D2;
               stat_terms(pn.f[k], mu, D, D2);
@@ -794,6 +808,34 @@ __global__ void k_argmin(const long long* __restrict__ counts, int stride, int S
       if (oi >= 0 && (bi < 0 || oe < be || (oe == be && oi < bi))) { be = oe; bi = oi; }
     }
     if (threadIdx.x == 0) { *best = bi; *best_e = be; }
+  }
+}
+
+// Printed clique relaxation: per-replica column sums C_s = sum_k rint(p_ks 2^40) (exact int64,
+// order-free) of p [B][n+1][SB]. The grid-stride step T is a multiple of S_p, so a thread
+// always sums the same column c = tid mod S_p and adds its partial once. out must be zero.
+__global__ void k_colsum(const float* __restrict__ p, int n, int SB, int S_p, int S_local, int T,
+                         unsigned long long* __restrict__ out) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= T) return;
+  const int c = tid % S_p, b = c / SB, col = c - b * SB;
+  if (c >= S_local) return;
+  const float* __restrict__ base = p + (size_t)b * ((size_t)n + 1) * SB + col;
+  long long acc = 0;
+  for (long long e = tid; e < (long long)n * S_p; e += T) {
+    const int r = (int)(e / S_p);
+    acc += __float2ll_rn(fmul(__ldg(base + (size_t)r * SB), 0x1p40f));
+  }
+  if (acc) atomicAdd(out + c, (unsigned long long)acc);
+}
+
+// Printed clique relaxation evaluated on the ORIGINAL graph: k_eval's (size, edges inside x, cut)
+// become the complement's (size, non-adjacent pairs inside x, non-adjacent pairs across x).
+__global__ void k_clique_counts(long long* __restrict__ counts, int S, long long n) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    const long long sz = counts[3 * s];
+    counts[3 * s + 1] = sz * (sz - 1) / 2 - counts[3 * s + 1];
+    counts[3 * s + 2] = sz * (n - sz) - counts[3 * s + 2];
   }
 }
 
