@@ -69,7 +69,7 @@ def _L():
         lib.oc_sigmoid_array.argtypes = [ctypes.c_int64, f32, f32]
         lib.oc_exp_neg.restype = ctypes.c_float
         lib.oc_exp_neg.argtypes = [ctypes.c_float]
-        for name in ("oc_clamp01", "oc_ln", "oc_cos2pi"):
+        for name in ("oc_clamp01", "oc_ln", "oc_cos2pi", "oc_sin2pi"):
             getattr(lib, name).restype = ctypes.c_float
             getattr(lib, name).argtypes = [ctypes.c_float]
         lib.oc_gauss_from_hash.restype = ctypes.c_float
@@ -175,6 +175,10 @@ def ln(u: float) -> float:
 
 def cos2pi(x: float) -> float:
     return float(_L().oc_cos2pi(float(x)))
+
+
+def sin2pi(x: float) -> float:
+    return float(_L().oc_sin2pi(float(x)))
 
 
 def gauss_from_hash(h: int) -> float:

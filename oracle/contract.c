@@ -128,9 +128,37 @@ float oc_ln(float u) {
     return (ef * 0.693145751953125f + lnm) + ef * 1.428606765330187e-6f;
 }
 
-/* cos(2 pi x), x in [0, 1): y = 4x (exact), k = rint(y), r = y - k in [-1/2, 1/2]
- * (exact), a = r pi/2 in [-pi/4, pi/4]; cos(k pi/2 + a) from the Taylor
- * polynomials of cos a (to a^8) and sin a (to a^9) by quadrant k mod 4. */
+/* cos(2 pi x) and sin(2 pi x), x in [0, 1): y = 4x (exact), k = rint(y), r = y - k in
+ * [-1/2, 1/2] (exact), a = r pi/2 in [-pi/4, pi/4]; from the Taylor polynomials of cos a (to a^8)
+ * and sin a (to a^9) by quadrant k mod 4. */
+void oc_cossin2pi(float x, float* c, float* sn) {
+    const float y = 4.0f * x;
+    const float k = rintf(y);
+    const float r = y - k;
+    const float a = r * 1.57079632679489662f;
+    const float a2 = a * a;
+    float C = 1.0f / 40320.0f;
+    C = C * a2 - 1.0f / 720.0f;
+    C = C * a2 + 1.0f / 24.0f;
+    C = C * a2 - 0.5f;
+    C = C * a2 + 1.0f;
+    float Sn = 1.0f / 362880.0f;
+    Sn = Sn * a2 - 1.0f / 5040.0f;
+    Sn = Sn * a2 + 1.0f / 120.0f;
+    Sn = Sn * a2 - 1.0f / 6.0f;
+    Sn = Sn * a2 + 1.0f;
+    Sn = Sn * a;
+    const int q = ((int)k) & 3;
+    *c = (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
+    *sn = (q == 0) ? Sn : (q == 1) ? C : (q == 2) ? -Sn : -C;
+}
+
+float oc_sin2pi(float x) {
+    float c, sn;
+    oc_cossin2pi(x, &c, &sn);
+    return sn;
+}
+
 float oc_cos2pi(float x) {
     const float y = 4.0f * x;
     const float k = rintf(y);
@@ -152,14 +180,23 @@ float oc_cos2pi(float x) {
     return (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
 }
 
-/* xi ~ N(0, 1) from one 64-bit hash h by Box-Muller:
+/* Two independent N(0, 1) from one 64-bit hash h by Box-Muller:
  * u1 = (top 24 bits + 1) 2^-24 in (0, 1], u2 = (bits 16..39) 2^-24 in [0, 1),
- * xi = sqrt(-2 ln u1) cos(2 pi u2). */
-float oc_gauss_from_hash(uint64_t h) {
+ * r = sqrt(-2 ln u1); zc = r cos(2 pi u2), zs = r sin(2 pi u2). */
+void oc_gauss_pair_from_hash(uint64_t h, float* zc, float* zs) {
     const float u1 = (float)((h >> 40) + 1u) * 0x1p-24f;
     const float u2 = (float)((h >> 16) & 0xFFFFFFu) * 0x1p-24f;
     const float r = sqrtf(-2.0f * oc_ln(u1));
-    return r * oc_cos2pi(u2);
+    float c, sn;
+    oc_cossin2pi(u2, &c, &sn);
+    *zc = r * c;
+    *zs = r * sn;
+}
+
+float oc_gauss_from_hash(uint64_t h) {
+    float zc, zs;
+    oc_gauss_pair_from_hash(h, &zc, &zs);
+    return zc;
 }
 
 /* ------------------------------------------------------ step scalars ---- */
@@ -211,13 +248,16 @@ static uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-/* Noise of (Adam step t, variable i, global replica s):
- * xi = gauss(mix64(mix64(seed ^ 0x6A09E667F3BCC909) + (t n + i) S_total + s)). */
+/* Noise of (Adam step t, variable i, global replica s): replicas pair up (s even, s + 1) on
+ * h = mix64(mix64(seed ^ 0x6A09E667F3BCC909) + (t n + i) S_total + s_even); xi = zc (s even) or
+ * zs (s odd) of oc_gauss_pair_from_hash(h). */
 uint64_t oc_noise_base(uint64_t seed) { return mix64(seed ^ 0x6A09E667F3BCC909ULL); }
 
 float oc_noise(uint64_t base, int64_t t, int32_t n, int32_t i, int32_t S_total, int32_t s) {
-    const uint64_t key = base + ((uint64_t)t * (uint64_t)n + (uint64_t)i) * (uint64_t)S_total + (uint64_t)s;
-    return oc_gauss_from_hash(mix64(key));
+    const uint64_t key = base + ((uint64_t)t * (uint64_t)n + (uint64_t)i) * (uint64_t)S_total + (uint64_t)(s & ~1);
+    float zc, zs;
+    oc_gauss_pair_from_hash(mix64(key), &zc, &zs);
+    return (s & 1) ? zs : zc;
 }
 
 void oc_noise_array(uint64_t seed, int64_t t, int32_t n, int32_t S, float* out) {
@@ -514,7 +554,8 @@ int64_t oc_complement(int32_t n, const int64_t* rowptr, const int32_t* colidx,
  * fp32 contract for the K-ary parts:
  *   - the entropy factor e = fl(fl(K p) - 1), e^(alpha-1) left to right;
  *   - the normaliser Z = ((c_0 + c_1) + c_2) + ..., p_k = c_k / Z;
- *   - noise key of (t, i, k, s) = base + ((t n + i) K + k) S_total + s. */
+ *   - noise: colours pair up, key of (t, i, k, s) = base + ((t n + i) K + k_even) S_total + s;
+ *     cos half for even k, sin half for odd k. */
 
 /* k_t for the K-ary entropy, host double -> fp32 */
 float oc_kt_K(int32_t K, int32_t alpha, float gamma_t) {
@@ -605,10 +646,12 @@ static int update_row_K(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, 
             const float v1 = b2 * vv[at_s + k] + (c2 * g) * g;
             const float den = sqrtf(v1) * rt + eps;
             t1 = t1 - st * (m1 / den);
-            if (cf->temperature > 0.0f) {
-                const uint64_t key = nbase + (((uint64_t)t * (uint64_t)n + (uint64_t)i) * (uint64_t)K + (uint64_t)k)
+            if (cf->temperature > 0.0f) {   /* colours pair up (k even, k + 1) on one hash */
+                const uint64_t key = nbase + (((uint64_t)t * (uint64_t)n + (uint64_t)i) * (uint64_t)K + (uint64_t)(k & ~1))
                                                  * (uint64_t)S + (uint64_t)s;
-                t1 = t1 + ns * oc_gauss_from_hash(mix64(key));
+                float zc, zs;
+                oc_gauss_pair_from_hash(mix64(key), &zc, &zs);
+                t1 = t1 + ns * ((k & 1) ? zs : zc);
             }
             if (!isfinite(t1)) bad = 1;
             w[k] = t1;

@@ -231,20 +231,26 @@ def clamp01(w):
 NOISE_SALT = 0x6A09E667F3BCC909
 
 
+def _box_muller_pair(h: np.ndarray):
+    """Both Box-Muller outputs of one hash: u1 = (h >> 40 + 1) 2^-24 in (0, 1], u2 = ((h >> 16) & (2^24 - 1))
+    2^-24 in [0, 1); r = sqrt(-2 ln u1); (r cos 2 pi u2, r sin 2 pi u2) -- two independent N(0, 1)."""
+    u1 = ((h >> np.uint64(40)) + np.uint64(1)).astype(np.float64) * 2.0 ** -24
+    u2 = ((h >> np.uint64(16)) & np.uint64(0xFFFFFF)).astype(np.float64) * 2.0 ** -24
+    r = np.sqrt(-2.0 * np.log(u1))
+    return r * np.cos(2.0 * np.pi * u2), r * np.sin(2.0 * np.pi * u2)
+
+
 def gauss_noise(seed: int, t: int, n: int, S_total: int) -> np.ndarray:
-    """xi ~ N(0, 1) [n][S_total] for Adam step t by Box-Muller in fp64 from a counter hash:
-    h = splitmix64(splitmix64(seed ^ salt) + (t n + i) S_total + s);
-    u1 = (h >> 40 + 1) 2^-24 in (0, 1]; u2 = ((h >> 16) & (2^24 - 1)) 2^-24 in [0, 1);
-    xi = sqrt(-2 ln u1) cos(2 pi u2)."""
+    """xi ~ N(0, 1) [n][S_total] for Adam step t by Box-Muller in fp64 from a counter hash. Replicas pair up
+    (s even, s + 1) on one hash h = splitmix64(splitmix64(seed ^ salt) + (t n + i) S_total + s_even):
+    xi = r cos 2 pi u2 for the even replica and r sin 2 pi u2 for the odd one (reading R24)."""
     base = _splitmix64(np.array([(seed ^ NOISE_SALT) & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64))[0]
     i = np.arange(n, dtype=np.uint64)[:, None]
     s = np.arange(S_total, dtype=np.uint64)[None, :]
     with np.errstate(over="ignore"):
-        key = base + (np.uint64(t) * np.uint64(n) + i) * np.uint64(S_total) + s
-    h = _splitmix64(key)
-    u1 = ((h >> np.uint64(40)) + np.uint64(1)).astype(np.float64) * 2.0 ** -24
-    u2 = ((h >> np.uint64(16)) & np.uint64(0xFFFFFF)).astype(np.float64) * 2.0 ** -24
-    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+        key = base + (np.uint64(t) * np.uint64(n) + i) * np.uint64(S_total) + (s & ~np.uint64(1))
+    zc, zs = _box_muller_pair(_splitmix64(key))
+    return np.where((s & np.uint64(1)) == 0, zc, zs)
 
 
 # --------------------------------------------------------------- the loop
@@ -406,9 +412,16 @@ def init_W_K(n: int, S_total: int, K: int, seed: int, lo: float = -0.01, hi: flo
 
 
 def gauss_noise_K(seed: int, t: int, n: int, S_total: int, K: int) -> np.ndarray:
-    """xi [n][S][K]: the Box-Muller draw of gauss_noise with row index i K + k of n K rows."""
-    z = gauss_noise(seed, t, n * K, S_total)          # [(i K + k)][s]
-    return z.reshape(n, K, S_total).transpose(0, 2, 1)
+    """xi [n][S][K] of the K-ary path: colours pair up (k even, k + 1) on one hash
+    h = splitmix64(splitmix64(seed ^ salt) + ((t n + i) K + k_even) S_total + s); cos for even k, sin for odd."""
+    base = _splitmix64(np.array([(seed ^ NOISE_SALT) & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64))[0]
+    i = np.arange(n, dtype=np.uint64)[:, None, None]
+    s = np.arange(S_total, dtype=np.uint64)[None, :, None]
+    k = np.arange(K, dtype=np.uint64)[None, None, :]
+    with np.errstate(over="ignore"):
+        key = base + ((np.uint64(t) * np.uint64(n) + i) * np.uint64(K) + (k & ~np.uint64(1))) * np.uint64(S_total) + s
+    zc, zs = _box_muller_pair(_splitmix64(key))
+    return np.where((k & np.uint64(1)) == 0, zc, zs)
 
 
 def run_K(A, P0, gammas, alpha=2, comm=0.1, lr=1.0, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.01,

@@ -42,6 +42,24 @@ def test_contract_cos2pi_matches_libm():
     assert oracle.cos2pi(0.25) == 0.0 and oracle.cos2pi(0.75) == 0.0
 
 
+def test_contract_sin2pi_matches_libm():
+    xs = np.arange(0, 1 << 24, 97, dtype=np.int64).astype(np.float64) * 2.0 ** -24
+    got = np.array([oracle.sin2pi(float(x)) for x in xs[::50]])
+    assert np.abs(got - np.sin(2 * np.pi * xs[::50])).max() <= 3e-7
+    assert oracle.sin2pi(0.0) == 0.0 and oracle.sin2pi(0.25) == 1.0 and oracle.sin2pi(0.75) == -1.0
+
+
+def test_paired_noise_halves_are_independent():
+    """Replicas (2j, 2j+1) share one hash (cos / sin halves of Box-Muller): each half is N(0,1) and the
+    two are uncorrelated (reading R24)."""
+    z = D.gauss_noise(5, 3, 4000, 64)
+    even, odd = z[:, 0::2].ravel(), z[:, 1::2].ravel()
+    for h in (even, odd):
+        assert stats.kstest(h, "norm").statistic < 3e-3
+    assert abs(np.corrcoef(even, odd)[0, 1]) < 0.01
+    assert abs(np.corrcoef(even ** 2, odd ** 2)[0, 1]) < 0.02   # not just uncorrelated: independent radii mix
+
+
 def test_contract_noise_equals_fp64_box_muller():
     """Same integer hash -> the fp32 contract's xi is the fp64 Box-Muller value to rounding."""
     for seed, t, n, S in [(7, 1, 300, 64), (123456789, 2999, 50, 100), (0, 5, 1, 1)]:
