@@ -567,7 +567,7 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
   R.sums[0] = h->sums[0]; R.sums[1] = h->sums[1]; R.sums[2] = h->sums[2];
   R.p[0] = h->p[0]; R.p[1] = h->p[1];
   R.nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);
-  R.off = (unsigned long long)c.replica_offset;
+  P.off = c.replica_offset;
   R.S_total = (double)h->s.S_total;
   R.sched = h->sched;
   std::vector<float4> tab((size_t)std::min<int64_t>(n_steps, kSchedCap));
@@ -624,6 +624,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
+  P.off = c.replica_offset;
   P.problem = problem_kind(c.problem);  // dense clique = MIS on the complement
   P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
   P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
@@ -634,8 +635,8 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   const uint64_t nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);    // noise stream
   for (int64_t k = 0; k < n_steps; ++k) {
     const int64_t t = h->step + 1;  // Adam step index (reading R11)
-    // xi key of (t, i, global s) = nbase + (t n + i) S_total + s  (mod 2^64)
-    P.var.nkey = nbase + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total + (uint64_t)c.replica_offset;
+    // xi key of (t, i, global s) = nbase + (t n + i) S_total + s_even  (mod 2^64; replica pairs, R24)
+    P.var.nkey = nbase + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total;
     P.var.kt = (float)(-2.0 * (double)c.alpha * (double)gamma[k]);
     P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
     P.var.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));

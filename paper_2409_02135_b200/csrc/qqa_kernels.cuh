@@ -103,9 +103,9 @@ __device__ __forceinline__ float ln_c(float u) {
   return fadd(fadd(fmul(ef, 0.693145751953125f), lnm), fmul(ef, 1.428606765330187e-6f));
 }
 
-// cos(2 pi x), x in [0, 1): quadrant k = rint(4x), a = (4x - k) pi/2 in [-pi/4, pi/4],
-// Taylor cos a (to a^8) / sin a (to a^9).
-__device__ __forceinline__ float cos2pi_c(float x) {
+// cos(2 pi x) and sin(2 pi x), x in [0, 1): quadrant k = rint(4x), a = (4x - k) pi/2 in
+// [-pi/4, pi/4], Taylor cos a (to a^8) / sin a (to a^9).
+__device__ __forceinline__ void cossin2pi_c(float x, float& cs, float& sn) {
   const float y = fmul(4.0f, x);
   const float k = rintf(y);
   const float r = fsub(y, k);
@@ -123,7 +123,8 @@ __device__ __forceinline__ float cos2pi_c(float x) {
   Sn = fadd(fmul(Sn, a2), 1.0f);
   Sn = fmul(Sn, a);
   const int q = ((int)k) & 3;
-  return (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
+  cs = (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
+  sn = (q == 0) ? Sn : (q == 1) ? C : (q == 2) ? -Sn : -C;
 }
 
 // Replica mean / population STD of one variable from its fixed-point sums.
@@ -150,13 +151,24 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// xi ~ N(0,1) from one hash by Box-Muller: u1 = (h>>40 + 1) 2^-24 in (0,1],
-// u2 = ((h>>16) & 0xFFFFFF) 2^-24 in [0,1), xi = sqrt(-2 ln u1) cos(2 pi u2).
-__device__ __forceinline__ float gauss_c(uint64_t h) {
+// Two independent N(0,1) from one hash by Box-Muller: u1 = (h>>40 + 1) 2^-24 in (0,1],
+// u2 = ((h>>16) & 0xFFFFFF) 2^-24 in [0,1), r = sqrt(-2 ln u1); zc = r cos(2 pi u2), zs = r sin(2 pi u2).
+__device__ __forceinline__ void gauss_pair_c(uint64_t h, float& zc, float& zs) {
   const float u1 = fmul(__ull2float_rn((h >> 40) + 1ull), 0x1p-24f);
   const float u2 = fmul(__ull2float_rn((h >> 16) & 0xFFFFFFull), 0x1p-24f);
   const float r = __fsqrt_rn(fmul(-2.0f, ln_c(u1)));
-  return fmul(r, cos2pi_c(u2));
+  float c, sn;
+  cossin2pi_c(u2, c, sn);
+  zc = fmul(r, c);
+  zs = fmul(r, sn);
+}
+
+// The noise of global replica sg from the row key rk: replicas pair up (sg even, sg + 1) on
+// mix64(rk + sg_even); the even one takes the cos half, the odd one the sin half (reading R24).
+__device__ __forceinline__ float noise_of(unsigned long long rk, int sg) {
+  float zc, zs;
+  gauss_pair_c(mix64(rk + (unsigned long long)(sg & ~1)), zc, zs);
+  return (sg & 1) ? zs : zc;
 }
 
 // ------------------------------------------------------ 256-bit accesses
@@ -274,7 +286,7 @@ struct StepVar {
   long long* sums_next;                 // [2][n] this rank's sums; zero on entry when B > 1
   long long* sums_zero;                 // [2][n] buffer of the step after next (zeroed here), B > 1
   float kt, st, rt;                     // -2 alpha gamma_t, lr/(1-b1^t), 1/sqrt(1-b2^t) (host double -> float)
-  unsigned long long nkey;              // noise key of (t, row 0, replica_offset): nbase + t n S_total + offset
+  unsigned long long nkey;              // noise key of (t, row 0): nbase + t n S_total (binary) / + offset (K-ary)
 };
 
 // ------------------------------------------------------------ parameters
@@ -290,6 +302,7 @@ struct StepParams {
   const long long* __restrict__ colsum; // [S_p] sum_k rint(p_ks 2^40) of the current p (printed clique only)
   int* __restrict__ flag;               // bit 0: non-finite theta
   int n, SB, B, S_local;
+  int off;                              // replica_offset: global index of local replica 0 (noise pairing)
   int row_begin, row_end;               // rows [row_begin, row_end) of this launch (comm overlap chunks)
   double S_total;
   int problem, alpha;
@@ -306,7 +319,7 @@ struct StepParams {
 template <int MODE>
 __device__ __forceinline__ float update_element(const StepParams& P, const StepVar& V, float q, float aux,
                                                 float pi, float mu, float sd, float& th, float& mm, float& vv,
-                                                unsigned long long key, bool& bad) {
+                                                float xi, bool& bad) {
   const float e = fsub(fmul(2.0f, pi), 1.0f);
   float ep = e;
   for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);                 // (2p-1)^(alpha-1)
@@ -324,7 +337,7 @@ __device__ __forceinline__ float update_element(const StepParams& P, const StepV
   vv = fadd(fmul(P.b2, vv), fmul(fmul(P.c2, g), g));
   const float den = fadd(fmul(__fsqrt_rn(vv), V.rt), P.eps);
   float w = fsub(t1, fmul(V.st, fdiv(mm, den)));
-  if (MODE & kModeNoise) w = fadd(w, fmul(P.ns, gauss_c(mix64(key))));   // + sqrt(2 lr T) xi
+  if (MODE & kModeNoise) w = fadd(w, fmul(P.ns, xi));                   // + sqrt(2 lr T) xi
   bad |= !isfinite(w);
   if (MODE & kModeClamp) {
     th = clamp01(w);
@@ -453,7 +466,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 
       // ---- gradient, AdamW, (noise), map, statistics of p_next
       long long sD = 0, sD2 = 0;
-      const unsigned long long rkey = V.nkey + (unsigned long long)i * P.S_total_u;  // noise key of (t, i, offset)
+      const unsigned long long rkey = V.nkey + (unsigned long long)i * P.S_total_u;  // noise key of (t, i, replica 0)
 #pragma unroll
       for (int w = 0; w < VPL; ++w) {
         const int col8 = lane + w * LANES;
@@ -473,23 +486,28 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         }
         V8 pn = pp;
         const int s0 = b * P.SB + col8 * 8;          // local replica index of element 0
-        if (s0 + 8 <= P.S_local) {
+        if (s0 + 8 <= P.S_local && (!(MODE & kModeNoise) || ((P.off + s0) & 1) == 0)) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
+          for (int k = 0; k < 8; k += 2) {            // a replica pair shares one noise hash (cos / sin halves)
+            float z0 = 0.0f, z1 = 0.0f;
+            if (MODE & kModeNoise) gauss_pair_c(mix64(rkey + (unsigned long long)(P.off + s0 + k)), z0, z1);
             pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, sd, th.f[k],
-                                           mm.f[k], vv.f[k],
-                                           rkey + (unsigned long long)(s0 + k), bad);
+                                           mm.f[k], vv.f[k], z0, bad);
+            pn.f[k + 1] = update_element<MODE>(P, V, acc[w].f[k + 1], aux_of<MODE>(P, degf, s0 + k + 1), pp.f[k + 1],
+                                               mu, sd, th.f[k + 1], mm.f[k + 1], vv.f[k + 1], z1, bad);
             long long D, D2;
             stat_terms(pn.f[k], mu, D, D2);
             sD += D; sD2 += D2;
+            stat_terms(pn.f[k + 1], mu, D, D2);
+            sD += D; sD2 += D2;
           }
-        } else {                                      // ragged last vector: padding is never updated
+        } else {   // ragged last vector (padding is never updated), or an odd shard offset under noise
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (s0 + k < P.S_local) {
+              const float z = (MODE & kModeNoise) ? noise_of(rkey, P.off + s0 + k) : 0.0f;
               pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, sd, th.f[k],
-                                             mm.f[k], vv.f[k],
-                                             rkey + (unsigned long long)(s0 + k), bad);
+                                             mm.f[k], vv.f[k], z, bad);
               long long D, D2;
               stat_terms(pn.f[k], mu, D, D2);
               sD += D; sD2 += D2;
@@ -533,8 +551,7 @@ struct RunParams {
   float* c[2];                          // shift of the statistics, ping-pong
   long long* sums[3];                   // [2][n] rotating
   float* p[2];
-  unsigned long long nbase;             // noise stream base; key of (t, i, s) = nbase + (t n + i) S_total + s
-  unsigned long long off;               // replica_offset
+  unsigned long long nbase;             // noise stream base; key of (t, i, s) = nbase + (t n + i) S_total + s_even
   long long t0;                         // Adam steps taken before this launch
   int nsteps, cur0, scur0;
   double S_total;
@@ -569,7 +586,7 @@ __global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 2 ? 2 : QQA_STEP
     const float4 sc = R.sched[j];
     const unsigned long long t = (unsigned long long)(R.t0 + j + 1);
     const StepVar V{R.p[a], R.p[a ^ 1], R.sums[sb], nullptr, sc.x, sc.y, sc.z,
-                    R.nbase + t * (unsigned long long)P.n * P.S_total_u + R.off};
+                    R.nbase + t * (unsigned long long)P.n * P.S_total_u};
     const long long* __restrict__ sc_cur = R.sums[sa];
     for (int i = group; i < row1; i += ngroups) {
       float mu, sd;
@@ -972,6 +989,14 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 1)) k_step_K(co
       ld_colours<KP>(P.p_cur + at, w);
       ld_colours<KP>(P.m + at, mm);
       ld_colours<KP>(P.v + at, vv2);
+      float xi[KP];                                 // colours pair up (k even, k + 1) on one noise hash
+#pragma unroll
+      for (int k = 0; k < KP; k += 2) {
+        xi[k] = 0.0f;
+        xi[k + 1] = 0.0f;
+        if ((MODE & kModeNoise) && k < P.K)
+          gauss_pair_c(mix64(rkey + (unsigned long long)k * P.S_total_u + (unsigned long long)r), xi[k], xi[k + 1]);
+      }
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
         if (k >= P.K) continue;
@@ -988,8 +1013,7 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 1)) k_step_K(co
         vv2[k] = fadd(fmul(P.b2, vv2[k]), fmul(fmul(P.c2, g), g));
         const float den = fadd(fmul(__fsqrt_rn(vv2[k]), P.rt), P.eps);
         float x = fsub(t1, fmul(P.st, fdiv(mm[k], den)));
-        if (MODE & kModeNoise)
-          x = fadd(x, fmul(P.ns, gauss_c(mix64(rkey + (unsigned long long)k * P.S_total_u + (unsigned long long)r))));
+        if (MODE & kModeNoise) x = fadd(x, fmul(P.ns, xi[k]));
         bad |= !isfinite(x);
         w[k] = x;
       }

@@ -104,7 +104,7 @@ def test_noise_keyed_by_global_replica(Q, mp):
     full = gpu(Q, g, "mis", 96, 3, comm=0.0, map=mp, temperature=0.01)
     full.run(gam)
     fs = full.get_state()
-    for off, S in [(0, 32), (32, 32), (40, 8), (88, 8)]:
+    for off, S in [(0, 32), (32, 32), (40, 8), (88, 8), (33, 13), (61, 35)]:   # odd offsets split noise pairs
         sh = gpu(Q, g, "mis", S, 3, S_total=96, offset=off, comm=0.0, map=mp, temperature=0.01)
         sh.run(gam)
         ss = sh.get_state()
