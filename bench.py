@@ -350,6 +350,10 @@ def main():
                 "config": workload_config(w, world),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
+                             # the DRAM bytes ncu measured per launch over the same launch time: the byte
+                             # model counts every gathered row, L2 hits included, so frac can exceed 1
+                             "traffic_achieved": (traffic / avg_kernel_s / 1e9) if traffic else None,
+                             "traffic_frac": (traffic / avg_kernel_s / 1e9 / peak) if traffic else None,
                              "kernel": ("qqa::k_step_K (fused K-ary gather + gradient + AdamW + normalise + stats)"
                                         if w.n_colors else "qqa::k_step (fused gather + gradient + AdamW + stats)"),
                              "bytes_per_launch": B, "avg_launch_ms": avg_kernel_s * 1e3,
