@@ -940,7 +940,7 @@ __device__ __forceinline__ void normalize_colours(float (&w)[KP], int K, float u
 #define QQA_KARY_U_WIDE 2    // neighbour rows in flight per lane for KP > 8
 #endif
 template <int KP, int MODE>
-__global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 1)) k_step_K(const StepKParams P) {
+__global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(const StepKParams P) {
   constexpr int U = (KP <= 8) ? 4 : QQA_KARY_U_WIDE;     // neighbour rows in flight per lane
   const int L = P.L;
   const int lane = threadIdx.x & (L - 1);
@@ -989,17 +989,16 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 1)) k_step_K(co
       ld_colours<KP>(P.p_cur + at, w);
       ld_colours<KP>(P.m + at, mm);
       ld_colours<KP>(P.v + at, vv2);
-      float xi[KP];                                 // colours pair up (k even, k + 1) on one noise hash
-#pragma unroll
-      for (int k = 0; k < KP; k += 2) {
-        xi[k] = 0.0f;
-        xi[k + 1] = 0.0f;
-        if ((MODE & kModeNoise) && k < P.K)
-          gauss_pair_c(mix64(rkey + (unsigned long long)k * P.S_total_u + (unsigned long long)r), xi[k], xi[k + 1]);
-      }
+      float xi = 0.0f, xi_odd = 0.0f;              // colours pair up (k even, k + 1) on one noise hash
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
         if (k >= P.K) continue;
+        if (MODE & kModeNoise) {
+          if ((k & 1) == 0)
+            gauss_pair_c(mix64(rkey + (unsigned long long)k * P.S_total_u + (unsigned long long)r), xi, xi_odd);
+          else
+            xi = xi_odd;
+        }
         const float pi = w[k];
         const float2 st = P.ms[(size_t)i * P.K + k];
         const float e = fsub(fmul(P.Kf, pi), 1.0f);
@@ -1013,7 +1012,7 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 1)) k_step_K(co
         vv2[k] = fadd(fmul(P.b2, vv2[k]), fmul(fmul(P.c2, g), g));
         const float den = fadd(fmul(__fsqrt_rn(vv2[k]), P.rt), P.eps);
         float x = fsub(t1, fmul(P.st, fdiv(mm[k], den)));
-        if (MODE & kModeNoise) x = fadd(x, fmul(P.ns, xi[k]));
+        if (MODE & kModeNoise) x = fadd(x, fmul(P.ns, xi));
         bad |= !isfinite(x);
         w[k] = x;
       }
