@@ -58,10 +58,12 @@ def splitmix64(x: int) -> int:
 
 @dataclasses.dataclass
 class Graph:
-    """Undirected simple graph as symmetric CSR (rows sorted, no loops/duplicates)."""
+    """Undirected simple graph as symmetric CSR (rows sorted, no loops/duplicates), optionally with
+    symmetric edge weights (float32 [nnz], w_ij = w_ji; "A_ij denotes the edge weight")."""
     n: int
     rowptr: np.ndarray  # int64 [n+1]
     colidx: np.ndarray  # int32 [nnz]
+    weights: np.ndarray | None = None
 
     @property
     def nnz(self) -> int:
@@ -160,6 +162,29 @@ def mycielski(k: int) -> Graph:
     lo = np.minimum(eu, ev).astype(np.int32)
     hi = np.maximum(eu, ev).astype(np.int32)
     return from_edges(n, lo, hi)
+
+
+def with_weights(g: Graph, kind: str, seed: int) -> Graph:
+    """Symmetric edge weights drawn once per undirected edge from a seeded stream:
+    kind "pm1": {-1, +1} (the Optsicom Max-Cut family), "int": {1..4}, "uniform": U(0.5, 1.5)."""
+    u, v = g.edges()
+    rng = np.random.Generator(np.random.PCG64(seed))
+    if kind == "pm1":
+        w = rng.choice(np.float32([-1.0, 1.0]), size=len(u))
+    elif kind == "int":
+        w = rng.integers(1, 5, size=len(u)).astype(np.float32)
+    elif kind == "uniform":
+        w = rng.uniform(0.5, 1.5, size=len(u)).astype(np.float32)
+    else:
+        raise KeyError(kind)
+    # place w(u,v) at both CSR positions (u's row has v, v's row has u)
+    key = {}
+    for k, (a, b) in enumerate(zip(u.tolist(), v.tolist())):
+        key[(a, b)] = w[k]
+        key[(b, a)] = w[k]
+    rows = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    weights = np.fromiter((key[(int(a), int(b))] for a, b in zip(rows, g.colidx)), np.float32, count=g.nnz)
+    return Graph(g.n, g.rowptr, g.colidx, weights)
 
 
 def disjoint_union(graphs) -> tuple[Graph, np.ndarray]:

@@ -87,15 +87,16 @@ def _L():
         lib.oc_init.restype = None
         lib.oc_init.argtypes = [ctypes.c_int32, cfgp, f32, f32, f32, f32, f32, i64, i64]
         lib.oc_run.restype = ctypes.c_int
-        lib.oc_run.argtypes = [ctypes.c_int32, i64, i32, cfgp, f32, ctypes.c_int64, ctypes.c_int64,
+        vp = ctypes.c_void_p
+        lib.oc_run.argtypes = [ctypes.c_int32, i64, i32, vp, cfgp, f32, ctypes.c_int64, ctypes.c_int64,
                                f32, f32, f32, f32, f32, i64, i64]
         lib.oc_step_rows.restype = None
-        lib.oc_step_rows.argtypes = [ctypes.c_int32, i64, i32, cfgp, ctypes.c_float, ctypes.c_int64,
+        lib.oc_step_rows.argtypes = [ctypes.c_int32, i64, i32, vp, cfgp, ctypes.c_float, ctypes.c_int64,
                                      f32, f32, i64, i64, f32, f32, f32, i32, ctypes.c_int32,
                                      f32, f32, f32, f32, f32, i64, i64]
         lib.oc_eval.restype = None
-        lib.oc_eval.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
-                                f32, ctypes.c_float, i64, f64, ctypes.POINTER(ctypes.c_int32)]
+        lib.oc_eval.argtypes = [ctypes.c_int32, i64, i32, vp, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
+                                f32, ctypes.c_float, i64, i64, f64, ctypes.POINTER(ctypes.c_int32)]
         lib.oc_eval_groups.restype = None
         lib.oc_eval_groups.argtypes = [ctypes.c_int32, i64, i32, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
                                        f32, ctypes.c_float, i32, ctypes.c_int32, i64, f64, i32]
@@ -231,6 +232,15 @@ def _csr_for(g, cfg: OcCfg):
     return np.ascontiguousarray(g.rowptr, np.int64), np.ascontiguousarray(g.colidx, np.int32)
 
 
+def _wptr(g):
+    """(keep-alive array, pointer) of the graph's edge weights, or (None, None)."""
+    w = getattr(g, "weights", None)
+    if w is None:
+        return None, None
+    w = np.ascontiguousarray(w, np.float32)
+    return w, w.ctypes.data
+
+
 def init(g, cfg: OcCfg) -> State:
     n, S = g.n, cfg.S
     st = State(*(np.zeros((n, S), np.float32) for _ in range(4)), np.zeros(n, np.float32),
@@ -244,7 +254,8 @@ def run(g, cfg: OcCfg, gammas, state: State | None = None, csr=None) -> State:
     st = init(g, cfg) if state is None else state
     rp, ci = _csr_for(g, cfg) if csr is None else csr
     gam = np.ascontiguousarray(gammas, dtype=np.float32)
-    rc = _L().oc_run(g.n, rp, ci, ctypes.byref(cfg), gam, len(gam), st.t,
+    w, wp = _wptr(g) if cfg.problem in (MIS, MAXCUT) else (None, None)   # weights: MIS / Max-Cut only
+    rc = _L().oc_run(g.n, rp, ci, wp, ctypes.byref(cfg), gam, len(gam), st.t,
                      st.theta, st.m, st.v, st.p, st.c, st.sumD, st.sumD2)
     st.t += len(gam)
     if rc != 0:
@@ -261,7 +272,8 @@ def step_rows(g, cfg: OcCfg, gamma: float, t: int, p, c, sumD, sumD2, theta_rows
     out = dict(theta=np.empty((k, S), np.float32), m=np.empty((k, S), np.float32),
                v=np.empty((k, S), np.float32), p=np.empty((k, S), np.float32),
                c=np.empty(k, np.float32), sumD=np.empty(k, np.int64), sumD2=np.empty(k, np.int64))
-    _L().oc_step_rows(g.n, rp, ci, ctypes.byref(cfg), gamma, t,
+    w, wp = _wptr(g) if cfg.problem in (MIS, MAXCUT) else (None, None)
+    _L().oc_step_rows(g.n, rp, ci, wp, ctypes.byref(cfg), gamma, t,
                       np.ascontiguousarray(p, np.float32), np.ascontiguousarray(c, np.float32),
                       np.ascontiguousarray(sumD, np.int64), np.ascontiguousarray(sumD2, np.int64),
                       np.ascontiguousarray(theta_rows, np.float32), np.ascontiguousarray(m_rows, np.float32),
@@ -270,9 +282,10 @@ def step_rows(g, cfg: OcCfg, gamma: float, t: int, p, c, sumD, sumD2, theta_rows
     return out
 
 
-def evaluate(g, problem, penalty: float, theta: np.ndarray, csr=None, map="sigmoid"):
+def evaluate(g, problem, penalty: float, theta: np.ndarray, csr=None, map="sigmoid", wsums=False):
     """Round (theta >= thr, see threshold()), count, energies, best replica.
-    Returns (counts[S][3], energy[S], best)."""
+    Returns (counts[S][3], energy[S], best) (+ weight sums [S][2] of violated / cut edges, exact
+    int64 fixed point 2^24, with wsums=True). Energies use the weights of a weighted graph."""
     pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
     if csr is None:
         csr = complement(g) if pid == MAXCLIQUE else (g.rowptr, g.colidx)
@@ -280,10 +293,14 @@ def evaluate(g, problem, penalty: float, theta: np.ndarray, csr=None, map="sigmo
     th = np.ascontiguousarray(theta, np.float32)
     S = th.shape[1]
     counts = np.zeros((S, 3), np.int64)
+    ws = np.zeros((S, 2), np.int64)
     energy = np.zeros(S, np.float64)
     best = ctypes.c_int32(0)
-    _L().oc_eval(g.n, np.ascontiguousarray(rp, np.int64), np.ascontiguousarray(ci, np.int32),
-                 pid, penalty, S, th, threshold(map), counts, energy, ctypes.byref(best))
+    w, wp = _wptr(g) if pid in (MIS, MAXCUT) else (None, None)
+    _L().oc_eval(g.n, np.ascontiguousarray(rp, np.int64), np.ascontiguousarray(ci, np.int32), wp,
+                 pid, penalty, S, th, threshold(map), counts, ws, energy, ctypes.byref(best))
+    if wsums:
+        return counts, energy, int(best.value), ws
     return counts, energy, int(best.value)
 
 

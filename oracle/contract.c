@@ -20,6 +20,10 @@
  *   dR/dtheta = dR/dp * p (1 - p)
  *   AdamW, decoupled weight decay
  *   x = Theta(p - 1/2) evaluated as theta >= 0
+ *   weighted graphs (A_ij = w_ij; MIS and Max-Cut): q_i = sum_j w_ij p_j summed as
+ *     q = fl(q + fl(w_ij p_j)) in CSR order (w = 1 gives the unweighted sums bit for bit), the
+ *     Max-Cut degree sum_j w_ij as ((0 + w_1) + w_2) + ...; evaluation sums of w as exact int64
+ *     fixed point llrint(w 2^24)
  *   max clique, printed relaxation on the original graph (problem 4):
  *     dl/dp_i = -1 + lam ((T - 1/2) - q_i), T = sum_k p_k of the replica, as
  *     fl(fl(lam fl(fl(T_f - 1/2) - q)) - 1) with T_f = (float)((double)C 2^-40),
@@ -305,8 +309,8 @@ void oc_init(int32_t n, const oc_cfg* cf, float* theta, float* m, float* v, floa
  * updates th/mm/vv (row i, length S) in place; writes p_new (row i) and the
  * row's new stats (shift = this step's mean). */
 static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, const int32_t* colidx,
-                       const oc_cfg* cf, const float* sc, const float* Tcol, const float* p, float* th, float* mm,
-                       float* vv,
+                       const float* wts, const oc_cfg* cf, const float* sc, const float* Tcol, const float* p,
+                       float* th, float* mm, float* vv,
                        float c_i, int64_t sD_i, int64_t sD2_i,
                        float* p_new, float* c_new, int64_t* sD_new, int64_t* sD2_new, float* q) {
     const int32_t S = cf->S;
@@ -318,7 +322,11 @@ static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, co
     const float ns = oc_noise_scale(cf);
     const uint64_t nbase = oc_noise_base(cf->seed);
     const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
-    const float degf = (float)(e1 - e0);
+    float degf = (float)(e1 - e0);
+    if (wts) {                                   /* weighted degree, CSR order */
+        degf = 0.0f;
+        for (int64_t e = e0; e < e1; ++e) degf = degf + wts[e];
+    }
     const float* pown = p + (size_t)i * S;
     int nonfinite_flag = 0;
 
@@ -329,7 +337,12 @@ static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, co
     for (int32_t s = 0; s < S; ++s) q[s] = 0.0f;
     for (int64_t e = e0; e < e1; ++e) {
         const float* pj = p + (size_t)colidx[e] * S;
-        for (int32_t s = 0; s < S; ++s) q[s] = q[s] + pj[s];
+        if (wts) {
+            const float w = wts[e];
+            for (int32_t s = 0; s < S; ++s) q[s] = q[s] + w * pj[s];
+        } else {
+            for (int32_t s = 0; s < S; ++s) q[s] = q[s] + pj[s];
+        }
     }
 
     for (int32_t s = 0; s < S; ++s) {
@@ -381,7 +394,7 @@ void oc_colsum(int32_t n, int32_t S, const float* p, float* T) {
 /* Run n_steps annealing steps. gamma[k] is gamma for step k; Adam index t = t0 + k + 1.
  * State arrays are updated in place (p/c/sums hold the state of the current p).
  * Returns 0, or 5 if a non-finite theta appeared (SPEC.md:396 abort). */
-int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg* cf,
+int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const float* wts, const oc_cfg* cf,
            const float* gamma, int64_t n_steps, int64_t t0,
            float* theta, float* m, float* v, float* p, float* c, int64_t* sumD, int64_t* sumD2) {
     const int32_t S = cf->S;
@@ -405,7 +418,7 @@ int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg
 #pragma omp for schedule(static)
             for (int32_t i = 0; i < n; ++i) {
                 const size_t r = (size_t)i * S;
-                bad |= update_row(i, n, t, rowptr, colidx, cf, sc, Tcol, p, theta + r, m + r, v + r,
+                bad |= update_row(i, n, t, rowptr, colidx, wts, cf, sc, Tcol, p, theta + r, m + r, v + r,
                                   c[i], sumD[i], sumD2[i], p2 + r, &c2[i], &d2a[i], &d2b[i], q);
             }
             free(q);
@@ -423,7 +436,7 @@ int oc_run(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg
  * Inputs: the full p/c/sums at the start of the step, and theta/m/v of the
  * selected rows ([nrows][S]). Outputs for rows[k]: theta/m/v/p [nrows][S],
  * c/sums [nrows]. */
-void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const oc_cfg* cf,
+void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const float* wts, const oc_cfg* cf,
                   float gamma_t, int64_t t, const float* p, const float* c, const int64_t* sumD,
                   const int64_t* sumD2, const float* theta_rows, const float* m_rows, const float* v_rows,
                   const int32_t* rows, int32_t nrows,
@@ -441,7 +454,7 @@ void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const
         memcpy(theta_out + r, theta_rows + r, sizeof(float) * S);
         memcpy(m_out + r, m_rows + r, sizeof(float) * S);
         memcpy(v_out + r, v_rows + r, sizeof(float) * S);
-        (void)update_row(i, n, t, rowptr, colidx, cf, sc, Tcol, p, theta_out + r, m_out + r, v_out + r,
+        (void)update_row(i, n, t, rowptr, colidx, wts, cf, sc, Tcol, p, theta_out + r, m_out + r, v_out + r,
                    c[i], sumD[i], sumD2[i], p_out + r, &c_out[k], &sD_out[k], &sD2_out[k], q);
     }
     free(q);
@@ -454,9 +467,11 @@ void oc_step_rows(int32_t n, const int64_t* rowptr, const int32_t* colidx, const
  * undirected edge counted once (j > i); energy[s] = -size + lam*viol
  * (MIS / clique on the complement) or -cut (Max-Cut); *best = argmin energy,
  * lowest index on ties. */
-void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t problem, float lam,
-             int32_t S, const float* theta, float thr, int64_t* counts, double* energy, int32_t* best) {
+void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, const float* wts, int32_t problem, float lam,
+             int32_t S, const float* theta, float thr, int64_t* counts, int64_t* wsums, double* energy,
+             int32_t* best) {
     memset(counts, 0, sizeof(int64_t) * 3 * (size_t)S);
+    memset(wsums, 0, sizeof(int64_t) * 2 * (size_t)S);
     for (int32_t i = 0; i < n; ++i) {
         for (int32_t s = 0; s < S; ++s) {
             const int xi = theta[(size_t)i * S + s] >= thr;
@@ -467,6 +482,9 @@ void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t pr
                 const int xj = theta[(size_t)j * S + s] >= thr;
                 counts[3 * s + 1] += xi & xj;
                 counts[3 * s + 2] += xi ^ xj;
+                const int64_t W = wts ? llrintf(wts[e] * 0x1p24f) : ((int64_t)1 << 24);
+                wsums[2 * s + 0] += (xi & xj) ? W : 0;
+                wsums[2 * s + 1] += (xi ^ xj) ? W : 0;
             }
         }
     }
@@ -478,8 +496,10 @@ void oc_eval(int32_t n, const int64_t* rowptr, const int32_t* colidx, int32_t pr
         }
     int32_t b = 0;
     for (int32_t s = 0; s < S; ++s) {
-        energy[s] = (problem == OC_MAXCUT) ? -(double)counts[3 * s + 2]
-                                           : -(double)counts[3 * s + 0] + (double)lam * (double)counts[3 * s + 1];
+        /* weighted graphs: the penalty / cut are weight sums (exact fixed point), else edge counts */
+        const double viol = wts ? (double)wsums[2 * s + 0] * 0x1p-24 : (double)counts[3 * s + 1];
+        const double cut = wts ? (double)wsums[2 * s + 1] * 0x1p-24 : (double)counts[3 * s + 2];
+        energy[s] = (problem == OC_MAXCUT) ? -cut : -(double)counts[3 * s + 0] + (double)lam * viol;
         if (energy[s] < energy[b]) b = s;
     }
     *best = b;

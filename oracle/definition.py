@@ -45,12 +45,21 @@ def _pid(problem) -> int:
 
 
 # --------------------------------------------------------------- graphs
-def dense_adjacency(n: int, rowptr, colidx) -> np.ndarray:
+def dense_adjacency(n: int, rowptr, colidx, weights=None) -> np.ndarray:
+    """Dense A; with weights, A_ij is the edge weight."""
     A = np.zeros((n, n), dtype=np.float64)
     for i in range(n):
         for e in range(int(rowptr[i]), int(rowptr[i + 1])):
-            A[i, int(colidx[e])] = 1.0
+            A[i, int(colidx[e])] = 1.0 if weights is None else float(weights[e])
     return A
+
+
+def weighted_sums(A: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """Per replica [S][2]: (sum of w_ij over edges (i<j) with x_i = x_j = 1, sum over edges with x_i != x_j)."""
+    iu, ju = np.nonzero(np.triu(A != 0, 1))
+    w = A[iu, ju][:, None]
+    X = X.astype(np.int64)
+    return np.stack([(w * (X[iu] & X[ju])).sum(axis=0), (w * (X[iu] ^ X[ju])).sum(axis=0)], axis=1)
 
 
 def complement_adjacency(A: np.ndarray) -> np.ndarray:
