@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define QQA_ABI_VERSION 3
+#define QQA_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define QQA_API __attribute__((visibility("default")))
@@ -130,6 +130,11 @@ typedef struct {
   const int32_t* colidx;
   const int32_t* group_of_row;  /* [n] or NULL                                             */
   int32_t n_groups;             /* 1..2^24 when group_of_row is set                        */
+  const float* weights;         /* [nnz] symmetric edge weights (w_ij = w_ji bitwise, finite) or
+                                   NULL. P:687: A_ij is the edge weight. MIS: penalty
+                                   lambda sum_{(i,j)} w_ij x_i x_j; Max-Cut: cut weight. q_i =
+                                   sum_j w_ij p_j as fl(q + fl(w p)) in CSR order. MIS and
+                                   Max-Cut only, no batches (QQA_ERR_UNSUPPORTED otherwise) */
 } qqa_graph;
 
 /* Evaluation of one rounded replica (integer counts: bit-exact, order-free).
@@ -142,6 +147,9 @@ typedef struct {
   double energy;          /* -size + lambda*violations (MIS, clique) or -cut (Max-Cut)     */
   int32_t feasible;       /* violations == 0 (always 1 for Max-Cut)                        */
   int32_t replica;        /* global replica index                                          */
+  double wviolations;     /* weight sum of the violated edges (= violations unweighted),
+                             exact: sum of rint(w 2^24) 2^-24                              */
+  double wcut;            /* weight sum of the cut edges (= cut unweighted)                 */
 } qqa_replica_result;
 
 typedef struct qqa_handle qqa_handle;

@@ -40,12 +40,13 @@ class Config(ctypes.Structure):
 class Graph(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("nnz", ctypes.c_int64),
                 ("rowptr", ctypes.c_void_p), ("colidx", ctypes.c_void_p),
-                ("group_of_row", ctypes.c_void_p), ("n_groups", ctypes.c_int32)]
+                ("group_of_row", ctypes.c_void_p), ("n_groups", ctypes.c_int32), ("weights", ctypes.c_void_p)]
 
 
 class ReplicaResult(ctypes.Structure):
     _fields_ = [("size", ctypes.c_int64), ("violations", ctypes.c_int64), ("cut", ctypes.c_int64),
-                ("energy", ctypes.c_double), ("feasible", ctypes.c_int32), ("replica", ctypes.c_int32)]
+                ("energy", ctypes.c_double), ("feasible", ctypes.c_int32), ("replica", ctypes.c_int32),
+                ("wviolations", ctypes.c_double), ("wcut", ctypes.c_double)]
 
 
 def _declare(lib):

@@ -1,0 +1,7 @@
+// k_mode11.cu -- k_step / k_run of step mode 11 (bit 0 clamp, bit 1 Langevin noise, bit 3 edge weights).
+#include "k_mode.cuh"
+
+namespace qqa {
+StepKernel step_kernel_m11(int lanes, int vpl) { return step_for<11>(lanes, vpl); }
+RunKernel run_kernel_m11(int lanes, int vpl, int cta) { return run_kernel_for<11>(lanes, vpl, cta); }
+}  // namespace qqa

@@ -1,0 +1,7 @@
+// k_mode8.cu -- k_step / k_run of step mode 8 (bit 0 clamp, bit 1 Langevin noise, bit 3 edge weights).
+#include "k_mode.cuh"
+
+namespace qqa {
+StepKernel step_kernel_m8(int lanes, int vpl) { return step_for<8>(lanes, vpl); }
+RunKernel run_kernel_m8(int lanes, int vpl, int cta) { return run_kernel_for<8>(lanes, vpl, cta); }
+}  // namespace qqa

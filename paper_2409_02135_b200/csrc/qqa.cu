@@ -55,12 +55,14 @@ struct Shape {
   int64_t nnz_pad = 0;         // row-padded CSR (rows rounded up to 4 entries)
   int G = 1;                   // instances of a batch (NEXT-3); 1 without group_of_row
   bool kary = false;           // graph colouring (NEXT-4): layout [n][S_local][KP]
+  bool weighted = false;       // edge weights (MIS / Max-Cut)
   int K = 0, KP = 0, LK = 0;   // colours, padded to a multiple of 4, lanes per variable
 };
 
 struct Layout {
   size_t rowptr, colidx, rowptr_pad, colidx_pad, gor, theta, m, v, p0, p1, c0, c1, ms, s0, s1, s2, flag, X,
-      counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, sched, cs0, cs1, total;
+      counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, sched, cs0, cs1, w, w_pad, wdeg, wsums,
+      total;
 };
 
 Layout make_layout(const Shape& s) {
@@ -100,6 +102,10 @@ Layout make_layout(const Shape& s) {
   L.sched = take((size_t)kSchedCap * sizeof(float4));
   L.cs0 = take((size_t)s.S_p * sizeof(long long));   // printed clique: column sums of p[0] / p[1]
   L.cs1 = take((size_t)s.S_p * sizeof(long long));
+  L.w = take(s.weighted ? (size_t)s.nnz * sizeof(float) : 0);           // edge weights
+  L.w_pad = take(s.weighted ? (size_t)s.nnz_pad * sizeof(float) : 0);   // aligned with colidx_pad
+  L.wdeg = take(s.weighted ? (size_t)s.n * sizeof(float) : 0);
+  L.wsums = take(2 * (size_t)s.S_total * sizeof(long long));            // [S_total][2] weight sums
   L.total = o;
   return L;
 }
@@ -185,6 +191,12 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   s.S_local = c->S_local;
   s.S_total = c->S_total;
   s.G = g->group_of_row ? g->n_groups : 1;
+  if (g->weights) {
+    if (c->problem != QQA_MIS && c->problem != QQA_MAXCUT)
+      return fail(QQA_ERR_UNSUPPORTED, "edge weights are supported for MIS and Max-Cut (P:687)");
+    if (g->group_of_row) return fail(QQA_ERR_UNSUPPORTED, "batches (group_of_row) of weighted graphs are not supported");
+    s.weighted = true;
+  }
   if (c->problem == QQA_MAXCLIQUE_SPARSE && g->group_of_row)
     return fail(QQA_ERR_UNSUPPORTED, "batches (group_of_row) are not supported for the sparse max-clique relaxation");
   if (c->problem == QQA_COLORING) {
@@ -280,6 +292,10 @@ struct qqa_handle {
   uint8_t* xbuf = nullptr;
   float4* sched = nullptr;     // per-step scalars of a persistent launch
   long long* colsum[2] = {nullptr, nullptr};   // printed clique: per-replica column sums of p[0] / p[1]
+  float* w = nullptr;          // edge weights (NULL unweighted), padded copy, weighted degrees
+  float* w_pad = nullptr;
+  float* wdeg = nullptr;
+  long long* wsums = nullptr;  // [S_total][2] evaluation weight sums (fixed point 2^24)
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
   int run_cta = 256;           // threads per CTA of k_run (1024: contiguous rows per SM)
   int cur = 0;   // p / c buffer of the current step (mod 2)
@@ -310,9 +326,9 @@ using RunKernel = qqa::RunKernel;
 
 // Step-kernel mode: bit 0 clamp map, bit 1 Langevin noise (template, so the
 // default sigmoid / no-noise kernel carries none of the optional code).
-int step_mode(const qqa_config& c) {
+int step_mode(const qqa_config& c, bool weighted = false) {
   return (c.map == QQA_MAP_CLAMP ? qqa::kModeClamp : 0) | (c.temperature > 0.0f ? qqa::kModeNoise : 0) |
-         (c.problem == QQA_MAXCLIQUE_SPARSE ? qqa::kModeSparseClique : 0);
+         (c.problem == QQA_MAXCLIQUE_SPARSE ? qqa::kModeSparseClique : 0) | (weighted ? qqa::kModeWeighted : 0);
 }
 
 template <int L, int V>
@@ -330,7 +346,12 @@ bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki, 
     case 4: ks = qqa::step_kernel_m4(lanes, vpl); if (kr) *kr = qqa::run_kernel_m4(lanes, vpl, run_cta); break;
     case 5: ks = qqa::step_kernel_m5(lanes, vpl); if (kr) *kr = qqa::run_kernel_m5(lanes, vpl, run_cta); break;
     case 6: ks = qqa::step_kernel_m6(lanes, vpl); if (kr) *kr = qqa::run_kernel_m6(lanes, vpl, run_cta); break;
-    default: ks = qqa::step_kernel_m7(lanes, vpl); if (kr) *kr = qqa::run_kernel_m7(lanes, vpl, run_cta); break;
+    case 7: ks = qqa::step_kernel_m7(lanes, vpl); if (kr) *kr = qqa::run_kernel_m7(lanes, vpl, run_cta); break;
+    case 8: ks = qqa::step_kernel_m8(lanes, vpl); if (kr) *kr = qqa::run_kernel_m8(lanes, vpl, run_cta); break;
+    case 9: ks = qqa::step_kernel_m9(lanes, vpl); if (kr) *kr = qqa::run_kernel_m9(lanes, vpl, run_cta); break;
+    case 10: ks = qqa::step_kernel_m10(lanes, vpl); if (kr) *kr = qqa::run_kernel_m10(lanes, vpl, run_cta); break;
+    case 11: ks = qqa::step_kernel_m11(lanes, vpl); if (kr) *kr = qqa::run_kernel_m11(lanes, vpl, run_cta); break;
+    default: ks = nullptr; if (kr) *kr = nullptr; break;
   }
   ki = nullptr;
 #define QQA_ICASE(L, V) \
@@ -393,7 +414,7 @@ int launch_init_kary(qqa_handle* h, bool use_given, const float* c_given) {
   StepKKernel ks;
   InitKKernel ki;
   PackKKernel kp;
-  pick_kary(s.KP, step_mode(h->cfg), ks, ki, kp);
+  pick_kary(s.KP, step_mode(h->cfg, h->s.weighted), ks, ki, kp);
   qqa::InitKParams P{};
   P.p0 = h->p[0]; P.p1 = h->p[1]; P.m = h->m; P.v = h->v;
   P.c = h->c[0]; P.sums = h->sums[0];
@@ -422,7 +443,7 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   if (h->s.kary) return launch_init_kary(h, use_given, c_given);
   StepKernel ks;
   InitKernel ki;
-  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), ks, ki);
   qqa::InitParams P{};
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.p0 = h->p[0]; P.p1 = h->p[1];
   P.c = h->c[0]; P.sums = h->sums[0];
@@ -483,7 +504,7 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
   StepKKernel ks;
   InitKKernel ki;
   PackKKernel kp;
-  pick_kary(s.KP, step_mode(c), ks, ki, kp);
+  pick_kary(s.KP, step_mode(c, s.weighted), ks, ki, kp);
   const size_t nk = (size_t)s.n * s.K;
   qqa::StepKParams P{};
   P.rowptr = h->rowptr; P.colidx = h->colidx; P.m = h->m; P.v = h->v; P.flag = h->flag;
@@ -547,11 +568,12 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
   StepKernel ks;
   InitKernel ki;
   RunKernel kr = nullptr;
-  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki, &kr, h->run_cta);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), ks, ki, &kr, h->run_cta);
   const qqa_config& c = h->cfg;
   qqa::RunParams R{};
   qqa::StepParams& P = R.P;
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
+  P.w_pad = h->w_pad; P.wdeg = h->wdeg;
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
   P.row_begin = 0; P.row_end = h->s.n;
@@ -618,10 +640,11 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (use_persistent(h, n_steps)) return do_steps_persistent(h, gamma, n_steps);
   StepKernel ks;
   InitKernel ki;
-  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg), ks, ki);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), ks, ki);
   const qqa_config& c = h->cfg;
   qqa::StepParams P{};
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
+  P.w_pad = h->w_pad; P.wdeg = h->wdeg;
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
   P.off = c.replica_offset;
@@ -842,6 +865,12 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   h->sched = (float4*)(ws + L.sched);
   h->colsum[0] = (long long*)(ws + L.cs0);
   h->colsum[1] = (long long*)(ws + L.cs1);
+  if (s.weighted) {
+    h->w = (float*)(ws + L.w);
+    h->w_pad = (float*)(ws + L.w_pad);
+    h->wdeg = (float*)(ws + L.wdeg);
+  }
+  h->wsums = (long long*)(ws + L.wsums);
 
   // Graph -> device (int32 offsets). Max clique walks the complement graph.
   std::vector<int> rp32, ci_c;
@@ -864,6 +893,8 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     QQA_CUDA_C(cudaMemcpyAsync(h->colidx, ci_src, (size_t)s.nnz * sizeof(int), cudaMemcpyHostToDevice, h->stream));
   if (h->gor && s.n > 0)
     QQA_CUDA_C(cudaMemcpyAsync(h->gor, g->group_of_row, (size_t)s.n * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  if (h->w && s.nnz > 0)
+    QQA_CUDA_C(cudaMemcpyAsync(h->w, g->weights, (size_t)s.nnz * sizeof(float), cudaMemcpyHostToDevice, h->stream));
   QQA_CUDA_C(cudaMemsetAsync(h->flag, 0, 4 * sizeof(int), h->stream));
   // theta/m/v padding and the zero row n of both p buffers (K-ary: the colour padding)
   if (s.kary) {
@@ -876,7 +907,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   }
   if (cfg->problem != QQA_MAXCLIQUE && s.n > 0 && s.nnz > 0) {
     const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
-    qqa::k_validate<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, s.n, h->gor, h->flag);
+    qqa::k_validate<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, s.n, h->gor, h->w, h->flag);
     QQA_CUDA_C(cudaGetLastError());
     h->launches++;
     int flag = 0;
@@ -889,6 +920,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
       if (flag & 8) why += " self-loop;";
       if (flag & 16) why += " not symmetric;";
       if (flag & 32) why += " edge between two instances of the batch;";
+      if (flag & 64) why += " asymmetric (w_ij != w_ji) or non-finite edge weight;";
       return cleanup(fail(QQA_ERR_BAD_GRAPH, "graph rejected:" + why));
     }
   }
@@ -899,7 +931,8 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
                                h->stream));
     if (s.n > 0) {
       const int blocks = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
-      qqa::k_pad_csr<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, h->rowptr_pad, h->colidx_pad, s.n);
+      qqa::k_pad_csr<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, h->rowptr_pad, h->colidx_pad, s.n, h->w,
+                                                    h->w_pad, h->wdeg);
       QQA_CUDA_C(cudaGetLastError());
       h->launches++;
     }
@@ -909,7 +942,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     StepKKernel ks;
     InitKKernel ki;
     PackKKernel kp;
-    if (!pick_kary(s.KP, step_mode(*cfg), ks, ki, kp)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no K-ary kernel"));
+    if (!pick_kary(s.KP, step_mode(*cfg, s.weighted), ks, ki, kp)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no K-ary kernel"));
     const int64_t chunks = (s.S_local + s.LK - 1) / s.LK;   // work item = (variable, replica chunk)
     if ((st = grid_for((const void*)ks, h->sm_count, (int64_t)s.n * chunks, s.LK, h->grid_step))) return cleanup(st);
     if ((st = grid_for((const void*)ki, h->sm_count, (int64_t)s.n * s.S_local, 1, h->grid_init))) return cleanup(st);
@@ -923,7 +956,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     // fills every SM with a 1024-thread CTA (measured: profiles/r1_design_iterations.md)
     h->run_cta = (s.vpl == 1 && (int64_t)s.n * s.lanes >= (int64_t)h->sm_count * 1024) ? 1024 : 256;
     if (const char* env = std::getenv("QQA_RUN_CTA")) h->run_cta = (std::atoi(env) == 1024 && s.vpl == 1) ? 1024 : 256;
-    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg), ks, ki, &kr, h->run_cta))
+    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg, s.weighted), ks, ki, &kr, h->run_cta))
       return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
     if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
     {  // persistent kernel: every CTA must be co-resident (cooperative launch)
@@ -1043,7 +1076,7 @@ int evaluate_core_kary(qqa_handle* h) {
   StepKKernel ks;
   InitKKernel ki;
   PackKKernel kp;
-  pick_kary(s.KP, step_mode(h->cfg), ks, ki, kp);
+  pick_kary(s.KP, step_mode(h->cfg, h->s.weighted), ks, ki, kp);
   uint8_t* X8 = (uint8_t*)h->X;
   const int64_t ns = (int64_t)s.n * s.S_local;
   if (ns > 0) {  // K3: x = argmax_k P
@@ -1070,7 +1103,7 @@ int evaluate_core_kary(qqa_handle* h) {
   if (h->comm && h->nranks > 1)
     QQA_NCCL(ncclAllGather(mine, h->counts, 3 * (size_t)s.S_local, ncclInt64, h->comm, h->stream));
   qqa::k_argmin<<<1, 1024, 0, h->stream>>>((const long long*)h->counts, 3, s.S_total, qqa::kCOLORING, 0.0,
-                                           h->energy, h->best, h->beste);
+                                           h->energy, h->best, h->beste, nullptr);
   QQA_CUDA(cudaGetLastError());
   h->launches++;
   QQA_CUDA(cudaMemcpyAsync(h->genergy, h->energy, (size_t)s.S_total * sizeof(double), cudaMemcpyDeviceToDevice,
@@ -1106,13 +1139,15 @@ int evaluate_core(qqa_handle* h) {
   }
   // K4: counts of the local replicas at their global slots, [S_total][G][3]
   QQA_CUDA(cudaMemsetAsync(h->counts, 0, 3 * (size_t)s.S_total * s.G * sizeof(long long), h->stream));
+  if (s.weighted) QQA_CUDA(cudaMemsetAsync(h->wsums, 0, 2 * (size_t)s.S_total * sizeof(long long), h->stream));
   if (s.n > 0) {
     const int R = (int)std::max<int64_t>(1, std::min<int64_t>(s.n, (int64_t)h->sm_count * 64 / s.W));
     const int CH = (s.n + R - 1) / R;
     const int64_t warps = (int64_t)s.W * R;
     const int blocks = (int)((warps + 7) / 8);
     qqa::k_eval<<<blocks, 256, 0, h->stream>>>(h->rowptr, h->colidx, h->X, h->gor, s.n, s.W, R, CH, s.S_local, s.G,
-                                               h->counts + 3 * (size_t)off * s.G);
+                                               h->counts + 3 * (size_t)off * s.G, h->w,
+                                               (unsigned long long*)h->wsums + 2 * (size_t)off);
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }
@@ -1125,6 +1160,9 @@ int evaluate_core(qqa_handle* h) {
   if (h->comm && h->nranks > 1) {
     QQA_NCCL(ncclAllGather(h->counts + 3 * (size_t)off * s.G, h->counts, 3 * (size_t)s.S_local * s.G, ncclInt64,
                            h->comm, h->stream));
+    if (s.weighted)
+      QQA_NCCL(ncclAllGather(h->wsums + 2 * (size_t)off, h->wsums, 2 * (size_t)s.S_local, ncclInt64, h->comm,
+                             h->stream));
   }
   const int prob = h->cfg.problem == QQA_MAXCUT ? qqa::kMAXCUT : qqa::kMIS;   // cliques: complement counts
   const long long* tot = (const long long*)h->counts;
@@ -1135,13 +1173,13 @@ int evaluate_core(qqa_handle* h) {
     h->launches++;
     tot = h->tot;
     qqa::k_argmin<<<s.G, 1024, 0, h->stream>>>((const long long*)h->counts, 3 * s.G, s.S_total, prob,
-                                                (double)h->cfg.penalty, h->genergy, h->gbest, h->gbeste);
+                                                (double)h->cfg.penalty, h->genergy, h->gbest, h->gbeste, nullptr);
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }
   // K5: energies + argmin over all replicas (of the totals)
   qqa::k_argmin<<<1, 1024, 0, h->stream>>>(tot, 3, s.S_total, prob, (double)h->cfg.penalty, h->energy, h->best,
-                                           h->beste);
+                                           h->beste, s.weighted ? h->wsums : nullptr);
   QQA_CUDA(cudaGetLastError());
   h->launches++;
   if (s.G == 1) {  // the single instance is the whole graph
@@ -1183,11 +1221,16 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
   double be = 0.0;
   QQA_CUDA(cudaMemcpyAsync(&best, h->best, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   QQA_CUDA(cudaMemcpyAsync(&be, h->beste, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  std::vector<long long> cnt;
+  std::vector<long long> cnt, wsm;
   std::vector<double> en;
   if (per_replica) {
     cnt.resize(3 * (size_t)s.S_local);
     en.resize((size_t)s.S_local);
+    if (s.weighted) {
+      wsm.resize(2 * (size_t)s.S_local);
+      QQA_CUDA(cudaMemcpyAsync(wsm.data(), h->wsums + 2 * (size_t)off, wsm.size() * sizeof(long long),
+                               cudaMemcpyDeviceToHost, h->stream));
+    }
     QQA_CUDA(cudaMemcpyAsync(cnt.data(), tot + 3 * (size_t)off, cnt.size() * sizeof(long long),
                              cudaMemcpyDeviceToHost, h->stream));
     QQA_CUDA(cudaMemcpyAsync(en.data(), h->energy + off, en.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1214,6 +1257,8 @@ int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* 
       r.energy = en[k];
       r.feasible = (h->cfg.problem == QQA_MAXCUT) ? 1 : (r.violations == 0);   // colouring: proper
       r.replica = off + k;
+      r.wviolations = s.weighted ? (double)wsm[2 * k] * 0x1p-24 : (double)r.violations;
+      r.wcut = s.weighted ? (double)wsm[2 * k + 1] * 0x1p-24 : (double)r.cut;
     }
   }
   if (best_replica) *best_replica = best;

@@ -21,6 +21,10 @@ StepKernel step_kernel_m4(int lanes, int vpl);
 StepKernel step_kernel_m5(int lanes, int vpl);
 StepKernel step_kernel_m6(int lanes, int vpl);
 StepKernel step_kernel_m7(int lanes, int vpl);
+StepKernel step_kernel_m8(int lanes, int vpl);    // 8-11: weighted graphs (+ clamp / noise)
+StepKernel step_kernel_m9(int lanes, int vpl);
+StepKernel step_kernel_m10(int lanes, int vpl);
+StepKernel step_kernel_m11(int lanes, int vpl);
 RunKernel run_kernel_m0(int lanes, int vpl, int cta);
 RunKernel run_kernel_m1(int lanes, int vpl, int cta);
 RunKernel run_kernel_m2(int lanes, int vpl, int cta);
@@ -29,6 +33,10 @@ RunKernel run_kernel_m4(int lanes, int vpl, int cta);   // nullptr: modes 4-7 ru
 RunKernel run_kernel_m5(int lanes, int vpl, int cta);
 RunKernel run_kernel_m6(int lanes, int vpl, int cta);
 RunKernel run_kernel_m7(int lanes, int vpl, int cta);
+RunKernel run_kernel_m8(int lanes, int vpl, int cta);
+RunKernel run_kernel_m9(int lanes, int vpl, int cta);
+RunKernel run_kernel_m10(int lanes, int vpl, int cta);
+RunKernel run_kernel_m11(int lanes, int vpl, int cta);
 
 // K-ary kernels for KP in {4, 8, 12, 16}; false otherwise.
 bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);

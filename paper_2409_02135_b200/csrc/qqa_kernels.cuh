@@ -38,8 +38,9 @@ namespace qqa {
 enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2, kCOLORING = 3, kMAXCLIQUE_SPARSE = 4 };
 // Step-kernel mode (template): bit 0 = clamp map (Eq. 11),
 // bit 1 = Langevin noise (Eq. 9 / 11), bit 2 = the printed clique relaxation on
-// the original graph (per-replica column sums enter the objective).
-enum : int { kModeClamp = 1, kModeNoise = 2, kModeSparseClique = 4 };
+// the original graph (per-replica column sums enter the objective), bit 3 = edge weights
+// (q_i = sum_j w_ij p_j as fl(q + fl(w p)) in CSR order; MIS and Max-Cut).
+enum : int { kModeClamp = 1, kModeNoise = 2, kModeSparseClique = 4, kModeWeighted = 8 };
 
 #ifndef QQA_GATHER_U
 #define QQA_GATHER_U 4         // neighbour rows in flight per lane (multiple of 4)
@@ -294,6 +295,8 @@ struct StepParams {
   const int* __restrict__ rowptr;       // [n+1]   original CSR (degree for Max-Cut)
   const int* __restrict__ rowptr_pad;   // [n+1]   multiples of 4
   const int* __restrict__ colidx_pad;   // padded CSR, sentinel n
+  const float* __restrict__ w_pad;      // edge weights aligned with colidx_pad (0 on padding), weighted mode
+  const float* __restrict__ wdeg;       // [n] weighted degree sum_j w_ij in CSR order, weighted Max-Cut
   StepVar var;                          // this step: p_cur / p_next [B][NR][SB], sums, scalars
   float* __restrict__ theta;
   float* __restrict__ m;
@@ -445,24 +448,46 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         for (int u4 = 0; u4 < U / 4; ++u4)
           nxt[u4] = (e + U + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e + U + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
 #endif
-        if (e == e0) {
+        if (MODE & kModeWeighted) {   // q = fl(q + fl(w p)) in CSR order from +0 (padding: w = 0, p = 0)
+          float wt[U];
 #pragma unroll
-          for (int w = 0; w < VPL; ++w) acc[w] = buf[0][w];
+          for (int u = 0; u < U; u += 4) {
+            const float4 w4 = (u == 0 || e + u < e1) ? __ldg(reinterpret_cast<const float4*>(P.w_pad + e + u))
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            wt[u] = w4.x; wt[u + 1] = w4.y; wt[u + 2] = w4.z; wt[u + 3] = w4.w;
+          }
+          if (e == e0) {
+#pragma unroll
+            for (int w = 0; w < VPL; ++w) acc[w] = zero8();
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int w = 0; w < VPL; ++w)
+#pragma unroll
+              for (int k = 0; k < 8; ++k) acc[w].f[k] = fadd(acc[w].f[k], fmul(wt[u], buf[u][w].f[k]));
         } else {
+          if (e == e0) {
 #pragma unroll
-          for (int w = 0; w < VPL; ++w) add8(acc[w], buf[0][w]);
+            for (int w = 0; w < VPL; ++w) acc[w] = buf[0][w];
+          } else {
+#pragma unroll
+            for (int w = 0; w < VPL; ++w) add8(acc[w], buf[0][w]);
+          }
+#pragma unroll
+          for (int u = 1; u < U; ++u)
+#pragma unroll
+            for (int w = 0; w < VPL; ++w) add8(acc[w], buf[u][w]);
         }
-#pragma unroll
-        for (int u = 1; u < U; ++u)
-#pragma unroll
-          for (int w = 0; w < VPL; ++w) add8(acc[w], buf[u][w]);
       }
       if (e0 == e1) {
 #pragma unroll
         for (int w = 0; w < VPL; ++w) acc[w] = zero8();
       }
 
-      const float degf = (P.problem == kMAXCUT) ? (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i)) : 0.0f;
+      const float degf = (P.problem != kMAXCUT) ? 0.0f
+                         : (MODE & kModeWeighted) ? __ldg(P.wdeg + i)
+                                                  : (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i));
 
       // ---- gradient, AdamW, (noise), map, statistics of p_next
       long long sD = 0, sD2 = 0;
@@ -675,8 +700,9 @@ __global__ void __launch_bounds__(256) k_init(const InitParams P) {
 // Original CSR: bit 1: column out of range, bit 2: row not strictly ascending
 // (unsorted / duplicate), bit 3: self-loop, bit 4: asymmetric (j's row lacks i).
 // bit 5: edge between two instances of a batch (group_of_row[i] != group_of_row[j]).
+// bit 6: asymmetric weights (w_ij != w_ji bitwise) or a non-finite weight.
 __global__ void k_validate(const int* __restrict__ rowptr, const int* __restrict__ colidx, int n,
-                           const int* __restrict__ gor, int* __restrict__ flag) {
+                           const int* __restrict__ gor, const float* __restrict__ w, int* __restrict__ flag) {
   int bad = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int e0 = rowptr[i], e1 = rowptr[i + 1];
@@ -694,6 +720,7 @@ __global__ void k_validate(const int* __restrict__ rowptr, const int* __restrict
         if (colidx[mid] < i) lo = mid + 1; else hi = mid;
       }
       if (lo >= rowptr[j + 1] || colidx[lo] != i) bad |= 16;
+      else if (w && (__float_as_uint(w[lo]) != __float_as_uint(w[e]) || !isfinite(w[e]))) bad |= 64;
     }
   }
   if (bad) atomicOr(flag, bad);
@@ -701,11 +728,22 @@ __global__ void k_validate(const int* __restrict__ rowptr, const int* __restrict
 
 // Row-padded copy of the CSR: row i occupies [rowptr_pad[i], rowptr_pad[i+1]),
 // a multiple of 4 entries, the tail filled with the sentinel n (zero row of p).
+// (weights: w_pad aligned with colidx_pad, 0 on padding; wdeg[i] = ((0 + w_1) + w_2) + ... in CSR order)
 __global__ void k_pad_csr(const int* __restrict__ rowptr, const int* __restrict__ colidx,
-                          const int* __restrict__ rowptr_pad, int* __restrict__ colidx_pad, int n) {
+                          const int* __restrict__ rowptr_pad, int* __restrict__ colidx_pad, int n,
+                          const float* __restrict__ w, float* __restrict__ w_pad, float* __restrict__ wdeg) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int e0 = rowptr[i], e1 = rowptr[i + 1], f0 = rowptr_pad[i], f1 = rowptr_pad[i + 1];
     for (int k = 0; k < f1 - f0; ++k) colidx_pad[f0 + k] = (e0 + k < e1) ? colidx[e0 + k] : n;
+    if (w) {
+      float d = 0.0f;
+      for (int k = 0; k < f1 - f0; ++k) {
+        const float x = (e0 + k < e1) ? w[e0 + k] : 0.0f;
+        w_pad[f0 + k] = x;
+        if (e0 + k < e1) d = fadd(d, x);
+      }
+      wdeg[i] = d;
+    }
   }
 }
 
@@ -737,9 +775,11 @@ __global__ void k_pack(const float* __restrict__ theta, uint32_t* __restrict__ X
 // exact, order-free) whenever the instance of the row changes (rows of one
 // instance are contiguous) and at the end.
 // counts[s][g][3] = (size, violations, cut), s local (the caller offsets the pointer).
+// Weighted graphs (G = 1): wsums[s][2] += (sum of rint(w 2^24) over violated edges, over cut edges).
 __global__ void k_eval(const int* __restrict__ rowptr, const int* __restrict__ colidx,
                        const uint32_t* __restrict__ X, const int* __restrict__ gor, int n, int W, int R, int CH,
-                       int S_local, int G, unsigned long long* __restrict__ counts) {
+                       int S_local, int G, unsigned long long* __restrict__ counts,
+                       const float* __restrict__ wts, unsigned long long* __restrict__ wsums) {
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= W * R) return;
@@ -747,6 +787,7 @@ __global__ void k_eval(const int* __restrict__ rowptr, const int* __restrict__ c
   const int s = w * 32 + lane;
   const int i0 = (warp / W) * CH, i1 = min(n, i0 + CH);
   unsigned long long size = 0, viol = 0, cut = 0;
+  long long wv = 0, wc = 0;
   int cur = (gor && i0 < n) ? gor[i0] : 0;
   auto flush = [&](int g) {
     if (s < S_local && (size | viol | cut)) {
@@ -771,9 +812,18 @@ __global__ void k_eval(const int* __restrict__ rowptr, const int* __restrict__ c
       const uint32_t bj = (X[(size_t)j * W + w] >> lane) & 1u;
       viol += bi & bj;
       cut += bi ^ bj;
+      if (wts) {
+        const long long Wt = __float2ll_rn(fmul(__ldg(wts + e), 0x1p24f));
+        wv += (bi & bj) ? Wt : 0;
+        wc += (bi ^ bj) ? Wt : 0;
+      }
     }
   }
   flush(cur);
+  if (wts && s < S_local && (wv | wc)) {
+    atomicAdd(wsums + 2 * (size_t)s + 0, (unsigned long long)wv);
+    atomicAdd(wsums + 2 * (size_t)s + 1, (unsigned long long)wc);
+  }
 }
 
 // Totals over instances: tot[s][c] = sum_g counts[s][g][c] (the energy of the union graph).
@@ -789,8 +839,10 @@ __global__ void k_sum_groups(const long long* __restrict__ counts, int S_total, 
 // K5: energies of all S_total replicas and argmin (lowest index on ties). One CTA
 // per instance g = blockIdx.x: counts of replica s at counts[s stride + 3 g],
 // energy[g][S_total], best[g], best_e[g] (stride = 3 G; G = 1 for the totals).
+// (wsums [S_total][2], weighted graphs: the energy uses the weight sums instead of the edge counts)
 __global__ void k_argmin(const long long* __restrict__ counts, int stride, int S_total, int problem, double lam,
-                         double* __restrict__ energy, int* __restrict__ best, double* __restrict__ best_e) {
+                         double* __restrict__ energy, int* __restrict__ best, double* __restrict__ best_e,
+                         const long long* __restrict__ wsums) {
   __shared__ double se[32];
   __shared__ int si[32];
   counts += 3 * (size_t)blockIdx.x;
@@ -801,9 +853,11 @@ __global__ void k_argmin(const long long* __restrict__ counts, int stride, int S
   int bi = -1;
   for (int s = threadIdx.x; s < S_total; s += blockDim.x) {
     const long long* c = counts + (size_t)s * stride;
-    const double e = (problem == kMAXCUT)     ? -(double)c[2]
+    const double viol = wsums ? __dmul_rn((double)wsums[2 * s], 0x1p-24) : (double)c[1];
+    const double cut = wsums ? __dmul_rn((double)wsums[2 * s + 1], 0x1p-24) : (double)c[2];
+    const double e = (problem == kMAXCUT)     ? -cut
                      : (problem == kCOLORING) ? (double)c[1]                  // conflicts
-                                              : __dadd_rn(-(double)c[0], __dmul_rn(lam, (double)c[1]));
+                                              : __dadd_rn(-(double)c[0], __dmul_rn(lam, viol));
     energy[s] = e;
     if (bi < 0 || e < be) { be = e; bi = s; }
   }

@@ -31,19 +31,21 @@ def make_config(problem="mis", S_total=16, seed=1, replica_offset=0, S_local=Non
 
 
 def _as_graph(rowptr: np.ndarray, colidx: np.ndarray, group_of_row: np.ndarray | None = None,
-              n_groups: int | None = None) -> Graph:
+              n_groups: int | None = None, weights: np.ndarray | None = None) -> Graph:
     n = len(rowptr) - 1
+    wp = None if weights is None else weights.ctypes.data
     if group_of_row is None:
-        return Graph(n, int(rowptr[-1]) if n >= 0 else 0, rowptr.ctypes.data, colidx.ctypes.data, None, 1)
+        return Graph(n, int(rowptr[-1]) if n >= 0 else 0, rowptr.ctypes.data, colidx.ctypes.data, None, 1, wp)
     G = int(n_groups) if n_groups is not None else (int(group_of_row.max()) + 1 if group_of_row.size else 1)
-    return Graph(n, int(rowptr[-1]), rowptr.ctypes.data, colidx.ctypes.data, group_of_row.ctypes.data, G)
+    return Graph(n, int(rowptr[-1]), rowptr.ctypes.data, colidx.ctypes.data, group_of_row.ctypes.data, G, wp)
 
 
-def workspace_bytes(rowptr, colidx, cfg: Config, group_of_row=None, n_groups=None) -> int:
+def workspace_bytes(rowptr, colidx, cfg: Config, group_of_row=None, n_groups=None, weights=None) -> int:
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     colidx = np.ascontiguousarray(colidx, np.int32)
     gor = None if group_of_row is None else np.ascontiguousarray(group_of_row, np.int32)
-    g = _as_graph(rowptr, colidx, gor, n_groups)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float32)
+    g = _as_graph(rowptr, colidx, gor, n_groups, w)
     out = ctypes.c_size_t(0)
     check(lib.qqa_workspace_bytes(ctypes.byref(g), ctypes.byref(cfg), ctypes.byref(out)))
     return int(out.value)
@@ -71,10 +73,11 @@ class Solver:
     """One GPU's shard of the PQQA replica ensemble behind the C ABI.
 
     ``group_of_row`` (optional) makes the graph a batch of instances (block-diagonal
-    union, contiguous row ranges; NEXT-3)."""
+    union, contiguous row ranges; NEXT-3). ``weights`` (optional, float32 [nnz], symmetric)
+    are edge weights (MIS and Max-Cut)."""
 
     def __init__(self, rowptr, colidx, cfg: Config, device=None, stream=None, workspace=None,
-                 group_of_row=None, n_groups=None):
+                 group_of_row=None, n_groups=None, weights=None):
         import torch
 
         self._torch = torch
@@ -86,7 +89,8 @@ class Solver:
         self.S_local = cfg.S_local
         self.K = int(cfg.n_colors) if cfg.problem == _lib.PROBLEMS["coloring"] else 0   # NEXT-4
         self.group_of_row = None if group_of_row is None else np.ascontiguousarray(group_of_row, np.int32)
-        g = _as_graph(self.rowptr, self.colidx, self.group_of_row, n_groups)
+        self.weights = None if weights is None else np.ascontiguousarray(weights, np.float32)
+        g = _as_graph(self.rowptr, self.colidx, self.group_of_row, n_groups, self.weights)
         nbytes = ctypes.c_size_t(0)
         check(lib.qqa_workspace_bytes(ctypes.byref(g), ctypes.byref(cfg), ctypes.byref(nbytes)))
         self.workspace_bytes = int(nbytes.value)
