@@ -188,6 +188,15 @@ QQA_API int qqa_attach_comm(qqa_handle* h, const uint8_t id[128], int rank, int 
  * over the donor's ranks. (sync) */
 QQA_API int qqa_share_comm(qqa_handle* h, qqa_handle* donor);
 
+/* Loopback exchange (emulation and testing of the sharded path on ONE GPU): G handles hs[r]
+ * created with S_total = G S_local and replica_offset = r S_local, no communicator, on one device
+ * and one stream. qqa_loopback_sync_init adds their initial statistic sums (call after create /
+ * reset / set_state); qqa_loopback_run then runs n_steps in lockstep, adding the int64 sums of all
+ * shards after every step -- exactly the per-step NCCL all-reduce -- so the shards reproduce one
+ * handle holding all S_total replicas bit for bit. No kernel waits on another. (sync) */
+QQA_API int qqa_loopback_sync_init(qqa_handle** hs, int G);
+QQA_API int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps);
+
 /* Run n_steps annealing steps with the given per-step gamma (host float[n_steps]).
  * The Adam step counter persists across calls. Async. */
 QQA_API int qqa_run(qqa_handle* h, const float* gamma_host, int64_t n_steps);

@@ -1050,6 +1050,72 @@ int qqa_run(qqa_handle* h, const float* gamma_host, int64_t n_steps) {
   return do_steps(h, gamma_host, n_steps);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Loopback exchange: add the current statistic sums of all shards (on one device and stream) and
+// write the total back to every shard -- what the NCCL all-reduce does across GPUs.
+int loopback_reduce(qqa_handle** hs, int G) {
+  qqa_handle* h0 = hs[0];
+  const Shape& s = h0->s;
+  const long long len = 2 * (long long)s.n * (s.kary ? s.K : 1);
+  if (len == 0) return QQA_OK;
+  long long* acc = h0->sums[h0->scur];
+  const int blocks = (int)std::max<long long>(1, std::min<long long>((len + 255) / 256, (long long)h0->sm_count * 8));
+  for (int r = 1; r < G; ++r) {
+    qqa::k_add_i64<<<blocks, 256, 0, h0->stream>>>(acc, hs[r]->sums[hs[r]->scur], len);
+    QQA_CUDA(cudaGetLastError());
+  }
+  for (int r = 1; r < G; ++r)
+    QQA_CUDA(cudaMemcpyAsync(hs[r]->sums[hs[r]->scur], acc, (size_t)len * sizeof(long long), cudaMemcpyDeviceToDevice,
+                             h0->stream));
+  return QQA_OK;
+}
+
+int check_loopback(qqa_handle** hs, int G) {
+  if (!hs || G < 1) return fail(QQA_ERR_INVALID_ARG, "handles is NULL or G < 1");
+  for (int r = 0; r < G; ++r) {
+    if (!hs[r]) return fail(QQA_ERR_INVALID_ARG, "a handle is NULL");
+    const qqa_handle* h = hs[r];
+    if (h->comm) return fail(QQA_ERR_INVALID_ARG, "loopback shards must not have a communicator");
+    if (h->device != hs[0]->device || h->stream != hs[0]->stream)
+      return fail(QQA_ERR_INVALID_ARG, "loopback shards must share one device and one stream");
+    if (h->s.n != hs[0]->s.n || h->s.S_local != hs[0]->s.S_local || h->s.S_total != G * h->s.S_local ||
+        h->cfg.replica_offset != r * h->s.S_local || h->s.kary != hs[0]->s.kary || h->s.K != hs[0]->s.K ||
+        h->scur != hs[0]->scur || h->step != hs[0]->step)
+      return fail(QQA_ERR_INVALID_ARG, "loopback shards must be r = 0..G-1 of S_total = G S_local, in lockstep");
+  }
+  return QQA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qqa_loopback_sync_init(qqa_handle** hs, int G) {
+  int st = check_loopback(hs, G);
+  if (st) return st;
+  if ((st = set_device(hs[0]))) return st;
+  if ((st = loopback_reduce(hs, G))) return st;
+  QQA_CUDA(cudaStreamSynchronize(hs[0]->stream));
+  return QQA_OK;
+}
+
+int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps) {
+  int st = check_loopback(hs, G);
+  if (st) return st;
+  if ((st = set_device(hs[0]))) return st;
+  if (n_steps > 0 && !gamma_host) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
+  for (int64_t k = 0; k < n_steps; ++k) {
+    for (int r = 0; r < G; ++r)   // one launch-per-step step of every shard (n_steps = 1: no k_run)
+      if ((st = do_steps(hs[r], gamma_host + k, 1))) return st;
+    if ((st = loopback_reduce(hs, G))) return st;
+  }
+  QQA_CUDA(cudaStreamSynchronize(hs[0]->stream));
+  return QQA_OK;
+}
+
 int qqa_run_linear(qqa_handle* h, float gmin, float gmax, int64_t total_steps, int64_t t0, int64_t t1) {
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   if (total_steps < 1 || t0 < 0 || t1 < t0 || t1 > total_steps)

@@ -910,6 +910,12 @@ __global__ void k_clique_counts(long long* __restrict__ counts, int S, long long
   }
 }
 
+// Loopback exchange (emulated shards on one device): acc += x over len int64 entries.
+__global__ void k_add_i64(long long* __restrict__ acc, const long long* __restrict__ x, long long len) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < len; k += (long long)gridDim.x * blockDim.x)
+    acc[k] += x[k];
+}
+
 // x of one local replica as bytes.
 __global__ void k_extract(const uint32_t* __restrict__ X, int n, int W, int s_local, uint8_t* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)

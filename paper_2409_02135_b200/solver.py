@@ -218,3 +218,20 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def _handles(shards):
+    arr = (ctypes.c_void_p * len(shards))(*[s._h.value for s in shards])
+    return arr
+
+
+def loopback_sync_init(shards) -> None:
+    """Add the initial statistic sums of G shard solvers on one device / stream (emulated G GPUs)."""
+    check(lib.qqa_loopback_sync_init(_handles(shards), len(shards)))
+
+
+def loopback_run(shards, gammas) -> None:
+    """Run G shard solvers in lockstep with the loopback exchange of the statistic sums after every
+    step (the NCCL all-reduce of a real G-GPU run, emulated on one device)."""
+    g = np.ascontiguousarray(gammas, np.float32)
+    check(lib.qqa_loopback_run(_handles(shards), len(shards), g.ctypes.data, len(g)))
