@@ -8,6 +8,7 @@
 #include "qqa_dispatch.h"
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // NVTX ranges (header-only v3): create / run / evaluate in nsys / ncu timelines
 
 #include <algorithm>
 #include <cmath>
@@ -21,6 +22,12 @@
 namespace {
 
 thread_local std::string g_last_error;
+
+// RAII NVTX range around an entry point (SURVEY.md §5 tracing).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(int status, const std::string& msg) {
   g_last_error = msg;
@@ -802,6 +809,7 @@ int qqa_workspace_bytes(const qqa_graph* g, const qqa_config* cfg, size_t* bytes
 
 int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void* d_workspace,
                size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx("qqa_create");
   if (!out) return fail(QQA_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   Shape s;
@@ -1044,6 +1052,7 @@ int qqa_share_comm(qqa_handle* h, qqa_handle* donor) {
 }
 
 int qqa_run(qqa_handle* h, const float* gamma_host, int64_t n_steps) {
+  NvtxRange nvtx("qqa_run");
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   int st = set_device(h);
   if (st) return st;
@@ -1103,6 +1112,7 @@ int qqa_loopback_sync_init(qqa_handle** hs, int G) {
 }
 
 int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps) {
+  NvtxRange nvtx("qqa_loopback_run");
   int st = check_loopback(hs, G);
   if (st) return st;
   if ((st = set_device(hs[0]))) return st;
@@ -1117,6 +1127,7 @@ int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_
 }
 
 int qqa_run_linear(qqa_handle* h, float gmin, float gmax, int64_t total_steps, int64_t t0, int64_t t1) {
+  NvtxRange nvtx("qqa_run_linear");
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   if (total_steps < 1 || t0 < 0 || t1 < t0 || t1 > total_steps)
     return fail(QQA_ERR_INVALID_ARG, "need 0 <= t0 <= t1 <= total_steps, total_steps >= 1");
@@ -1276,6 +1287,7 @@ extern "C" {
 
 int qqa_round_evaluate(qqa_handle* h, qqa_replica_result* per_replica, int32_t* best_replica,
                        double* best_energy, uint8_t* best_x) {
+  NvtxRange nvtx("qqa_round_evaluate");
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   int st = set_device(h);
   if (st) return st;
@@ -1340,6 +1352,7 @@ int qqa_n_groups(qqa_handle* h, int32_t* n_groups) {
 
 int qqa_round_evaluate_groups(qqa_handle* h, int64_t* counts, double* energy, int32_t* best_replica,
                               double* best_energy, uint8_t* best_x) {
+  NvtxRange nvtx("qqa_round_evaluate_groups");
   if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
   int st = set_device(h);
   if (st) return st;
