@@ -50,7 +50,11 @@ def _case(k):
     return problem, g, gor, S, hp, steps, sb, gmin
 
 
-@pytest.mark.parametrize("k", range(24))
+N_FUZZ = int(__import__("os").environ.get("QQA_FUZZ_CASES", "24"))
+N_FUZZ_K = int(__import__("os").environ.get("QQA_FUZZ_CASES_K", "8"))
+
+
+@pytest.mark.parametrize("k", range(N_FUZZ))
 def test_random_configuration(Q, monkeypatch, k):
     problem, g, gor, S, hp, steps, sb, gmin = _case(k)
     if sb:
@@ -76,7 +80,7 @@ def test_random_configuration(Q, monkeypatch, k):
         assert np.array_equal(res.counts, counts) and np.array_equal(res.best_replica, best)
 
 
-@pytest.mark.parametrize("k", range(8))
+@pytest.mark.parametrize("k", range(N_FUZZ_K))
 def test_random_colouring_configuration(Q, k):
     r = np.random.default_rng(5000 + k)
     K = int(r.integers(2, 17))
