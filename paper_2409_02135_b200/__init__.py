@@ -5,7 +5,8 @@ this package only marshals arguments. Importing it fails loudly when the
 shared library has not been built -- there is no CPU fallback.
 """
 from ._lib import LIB_PATH, QQAError, header_functions, lib  # noqa: F401
+from .graph import csr_from_edges, read_edge_list  # noqa: F401
 from .solver import GroupResult, Result, Solver, loopback_run, loopback_sync_init, make_config, workspace_bytes  # noqa: F401,E501
 
 __all__ = ["Solver", "Result", "GroupResult", "make_config", "workspace_bytes", "loopback_sync_init", "loopback_run",
-           "QQAError", "LIB_PATH"]
+           "csr_from_edges", "read_edge_list", "QQAError", "LIB_PATH"]
