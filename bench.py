@@ -192,7 +192,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "q13", "k8"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "t1", "q13", "k8"])
     ap.add_argument("--map", default=None, choices=["sigmoid", "clamp"],
                     help="override the map (clamp = the paper's sensitive transition, NEXT-1)")
     ap.add_argument("--temperature", type=float, default=None, help="Langevin T (NEXT-2; the paper: 0.001)")

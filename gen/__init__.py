@@ -284,6 +284,13 @@ def workload(name: str, n_instances: int | None = None) -> Workload:
     if name == "c5":
         return Workload("c5", "mis", [random_regular(1_000_000, 20, 5)], [5], S=64, steps=3000,
                         recipe="MIS, random 20-regular N=1,000,000 (seed 5); S=64; 3000 steps")
+    if name == "t1":   # the paper's own Table 1 batch size (128 graphs, Table 12), not a BASELINE.json config
+        k_n = 128 if n_instances is None else n_instances
+        sizes = [700 + splitmix64(8000 + k) % 101 for k in range(k_n)]
+        gs = [erdos_renyi(n, 0.15, 8000 + k) for k, n in enumerate(sizes)]
+        return Workload("t1", "mis", gs, [8000], S=100, steps=3000,
+                        recipe="MIS, 128 x ER G(N, 0.15), N = 700 + splitmix64(8000+k) mod 101, one batched handle; "
+                               "S=100; 3000 steps (Table 1's ER-[700-800] setting: 128 graphs, S=100, 3000 steps)")
     # NEXT-4 (K-ary) workloads -- not BASELINE.json configs; measurement cases of the colouring path
     if name == "q13":
         return Workload("q13", "coloring", [queens(13, 13)], [13], S=1000, steps=3000, lr=0.01, n_colors=13,
