@@ -198,6 +198,7 @@ def main():
     ap.add_argument("--temperature", type=float, default=None, help="Langevin T (NEXT-2; the paper: 0.001)")
     ap.add_argument("--alpha", type=int, default=None, help="override the alpha-entropy exponent (the paper: 4, P:244)")
     ap.add_argument("--lr", type=float, default=None, help="override the AdamW learning rate (the paper: 1, 0.1 or 0.01, P:670)")
+    ap.add_argument("--replicas", type=int, default=None, help="override S (diagnostics: per-rank work of a sharded run)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--anneal-steps", type=int, default=None, help="override T (diagnostics only)")
     ap.add_argument("--cpu-sample-steps", type=int, default=60, help="annealing steps of the cpu_baseline sample "
@@ -220,6 +221,8 @@ def main():
     if args.lr is not None:
         w.lr = args.lr
         args_lr_override[0] = args.lr
+    if args.replicas is not None:
+        w.S = args.replicas
     if args.impl == "reference":
         run_reference(args, w)
         return
