@@ -79,6 +79,8 @@ def _declare(lib):
         "qqa_profile": (ctypes.c_int, [H, ctypes.c_int]),
         "qqa_profile_read": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
         "qqa_launch_count": (ctypes.c_int, [H, ctypes.POINTER(i64)]),
+        "qqa_step_path": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_int)]),
+        "qqa_replica_block": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_int)]),
         "qqa_destroy": (ctypes.c_int, [H]),
     }
     for name, (res, args) in sigs.items():

@@ -50,7 +50,7 @@ int fail(int status, const std::string& msg) {
 
 constexpr size_t kAlign = 256;
 constexpr int kSchedCap = 4096;   // steps per persistent launch (device table of per-step scalars)
-constexpr double kL2BlockBudget = 256.0 * 1024 * 1024;  // p larger than this is replica-blocked (measured)
+constexpr double kL2BlockBudget = 128.0 * 1024 * 1024;  // p larger than this is replica-blocked (measured)
 size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Shape {
@@ -1486,6 +1486,18 @@ int qqa_profile_read(qqa_handle* h, double* step_kernel_ms, int64_t* step_launch
 int qqa_launch_count(qqa_handle* h, int64_t* launches) {
   if (!h || !launches) return fail(QQA_ERR_INVALID_ARG, "handle or launches is NULL");
   *launches = h->launches;
+  return QQA_OK;
+}
+
+int qqa_step_path(qqa_handle* h, int* path) {
+  if (!h || !path) return fail(QQA_ERR_INVALID_ARG, "handle or path is NULL");
+  *path = h->s.kary ? QQA_PATH_KARY : use_persistent(h, 2) ? QQA_PATH_PERSISTENT : QQA_PATH_STEP;
+  return QQA_OK;
+}
+
+int qqa_replica_block(qqa_handle* h, int* SB) {
+  if (!h || !SB) return fail(QQA_ERR_INVALID_ARG, "handle or SB is NULL");
+  *SB = h->s.kary ? 0 : h->s.SB;
   return QQA_OK;
 }
 

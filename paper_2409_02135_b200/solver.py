@@ -208,6 +208,20 @@ class Solver:
         check(lib.qqa_launch_count(self._h, ctypes.byref(k)))
         return int(k.value)
 
+    STEP_PATHS = ("step", "persistent", "kary")
+
+    def step_path(self) -> str:
+        """The step kernel a run of >= 2 steps uses: 'step', 'persistent' or 'kary' (qqa_step_path)."""
+        k = ctypes.c_int(0)
+        check(lib.qqa_step_path(self._h, ctypes.byref(k)))
+        return self.STEP_PATHS[k.value]
+
+    def replica_block(self) -> int:
+        """SB of the replica-blocked layout [B][n+1][SB] (0 for colouring)."""
+        k = ctypes.c_int(0)
+        check(lib.qqa_replica_block(self._h, ctypes.byref(k)))
+        return int(k.value)
+
     def close(self):
         if self._h:
             check(lib.qqa_destroy(self._h))
