@@ -252,8 +252,10 @@ QQA_API int qqa_launch_count(qqa_handle* h, int64_t* launches);
 /* Which step kernel a qqa_run of >= 2 steps uses (fixed at create / attach). Host-only.
  *   QQA_PATH_STEP        one k_finalize + k_step launch per annealing step
  *   QQA_PATH_PERSISTENT  k_run: one cooperative launch per <= 4096 steps (one GPU, p in L2)
- *   QQA_PATH_KARY        k_step_K (graph colouring) */
-enum { QQA_PATH_STEP = 0, QQA_PATH_PERSISTENT = 1, QQA_PATH_KARY = 2 };
+ *   QQA_PATH_KARY        k_step_K (graph colouring)
+ *   QQA_PATH_CLUSTER     k_run_cluster: the whole anneal in one thread-block cluster's shared memory
+ *                        (one GPU, n * S_p <= 32768) */
+enum { QQA_PATH_STEP = 0, QQA_PATH_PERSISTENT = 1, QQA_PATH_KARY = 2, QQA_PATH_CLUSTER = 3 };
 QQA_API int qqa_step_path(qqa_handle* h, int* path);
 /* Replica block SB of the layout [B][n+1][SB] (0 for colouring). Host-only. */
 QQA_API int qqa_replica_block(qqa_handle* h, int* SB);

@@ -50,6 +50,7 @@ int fail(int status, const std::string& msg) {
 
 constexpr size_t kAlign = 256;
 constexpr int kSchedCap = 4096;   // steps per persistent launch (device table of per-step scalars)
+constexpr int64_t kClusterMaxElems = 1 << 15;  // n S_p up to this runs in one thread-block cluster (k_run_cluster)
 constexpr double kL2BlockBudget = 128.0 * 1024 * 1024;  // p larger than this is replica-blocked (measured)
 size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -305,6 +306,9 @@ struct qqa_handle {
   long long* wsums = nullptr;  // [S_total][2] evaluation weight sums (fixed point 2^24)
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
   int run_cta = 256;           // threads per CTA of k_run (1024: contiguous rows per SM)
+  int cluster_cs = 0;          // k_run_cluster: CTAs per cluster (0: not available for this handle)
+  int cluster_rows = 0;        // rows per CTA of the cluster
+  size_t cluster_smem = 0;
   int cur = 0;   // p / c buffer of the current step (mod 2)
   int scur = 0;  // sums buffer of the current step (mod 3)
   int64_t step = 0;
@@ -640,10 +644,86 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
   return QQA_OK;
 }
 
+// One-cluster path (k_run_cluster): one GPU, unblocked, n S_p <= kClusterMaxElems. QQA_CLUSTER=0/1
+// overrides; an explicit QQA_PERSISTENT selects k_run / k_step instead.
+bool use_cluster(const qqa_handle* h, int64_t n_steps) {
+  if (h->cluster_cs <= 0 || h->comm || n_steps < 2) return false;
+  if (const char* env = std::getenv("QQA_CLUSTER")) return std::atoi(env) != 0;
+  return std::getenv("QQA_PERSISTENT") == nullptr;
+}
+
+int do_steps_cluster(qqa_handle* h, const float* gamma, int64_t n_steps) {
+  const qqa_config& c = h->cfg;
+  qqa::RunParams R{};
+  qqa::StepParams& P = R.P;
+  P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
+  P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
+  P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
+  P.row_begin = 0; P.row_end = h->s.n;
+  P.problem = problem_kind(c.problem);
+  P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
+  P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
+  P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
+  P.eps = c.eps;
+  P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
+  P.ns = (float)std::sqrt(2.0 * (double)c.lr * (double)c.temperature);
+  P.S_total_u = (unsigned long long)h->s.S_total;
+  P.off = c.replica_offset;
+  R.c[0] = h->c[0]; R.c[1] = h->c[1];
+  R.sums[0] = h->sums[0]; R.sums[1] = h->sums[1]; R.sums[2] = h->sums[2];
+  R.p[0] = h->p[0]; R.p[1] = h->p[1];
+  R.nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);
+  R.S_total = (double)h->s.S_total;
+  R.sched = h->sched;
+  R.rows_cta = h->cluster_rows;
+  const qqa::RunKernel kc = qqa::cluster_kernel(step_mode(c, h->s.weighted));
+  std::vector<float4> tab((size_t)std::min<int64_t>(n_steps, kSchedCap));
+  for (int64_t k0 = 0; k0 < n_steps; k0 += kSchedCap) {
+    const int nk = (int)std::min<int64_t>(kSchedCap, n_steps - k0);
+    for (int j = 0; j < nk; ++j) {   // the same host double -> fp32 scalars as the other paths
+      const int64_t t = h->step + j + 1;
+      tab[j] = make_float4((float)(-2.0 * (double)c.alpha * (double)gamma[k0 + j]),
+                           (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t))),
+                           (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t))), 0.0f);
+    }
+    QQA_CUDA(cudaMemcpyAsync(h->sched, tab.data(), (size_t)nk * sizeof(float4), cudaMemcpyHostToDevice, h->stream));
+    R.t0 = h->step;
+    R.nsteps = nk;
+    R.cur0 = h->cur;
+    R.scur0 = h->scur;
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(h->cluster_cs);
+    lc.blockDim = dim3(1024);
+    lc.dynamicSmemBytes = h->cluster_smem;
+    lc.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = h->cluster_cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int st;
+    if ((st = record_start(h))) return st;
+    QQA_CUDA(cudaLaunchKernelEx(&lc, kc, R));
+    h->launches++;
+    if (h->profiling) {   // one launch = nk steps
+      QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
+      h->ev_used += 2;
+      h->prof_launches += nk;
+    }
+    h->cur = (h->cur + nk) & 1;
+    h->scur = (int)((h->scur + nk) % 3);
+    h->step += nk;
+  }
+  return QQA_OK;
+}
+
 int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (n_steps < 0) return fail(QQA_ERR_INVALID_ARG, "n_steps < 0");
   if (n_steps > 0 && !gamma) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
   if (h->s.kary) return do_steps_kary(h, gamma, n_steps);
+  if (use_cluster(h, n_steps)) return do_steps_cluster(h, gamma, n_steps);
   if (use_persistent(h, n_steps)) return do_steps_persistent(h, gamma, n_steps);
   StepKernel ks;
   InitKernel ki;
@@ -979,6 +1059,42 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     }
     h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
     if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
+    if (s.B == 1 && !s.weighted && cfg->problem != QQA_MAXCLIQUE_SPARSE && s.n > 0 &&
+        (int64_t)s.n * s.S_p <= kClusterMaxElems) {   // tiny problem: one thread-block cluster (k_run_cluster)
+      const qqa::RunKernel kc = qqa::cluster_kernel(step_mode(*cfg, s.weighted));
+      for (int cs : {16, 8}) {
+        if (!kc) break;
+        const int rows = next_pow2((s.n + cs - 1) / cs);   // power of two: owner = j >> log2(rows)
+        const size_t smem = qqa::cluster_smem_bytes(rows, s.S_p);
+        if (smem > 200 * 1024) continue;
+        if (cudaFuncSetAttribute((const void*)kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            (cs > 8 && cudaFuncSetAttribute((const void*)kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                           cudaSuccess)) {
+          (void)cudaGetLastError();
+          continue;
+        }
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(cs);
+        lc.blockDim = dim3(1024);
+        lc.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)kc, &lc) != cudaSuccess || nclusters < 1) {
+          (void)cudaGetLastError();
+          continue;
+        }
+        h->cluster_cs = cs;
+        h->cluster_rows = rows;
+        h->cluster_smem = smem;
+        break;
+      }
+    }
   }
   if ((st = launch_init(h, false, nullptr))) return cleanup(st);
   QQA_CUDA_C(cudaStreamSynchronize(h->stream));
@@ -1491,7 +1607,8 @@ int qqa_launch_count(qqa_handle* h, int64_t* launches) {
 
 int qqa_step_path(qqa_handle* h, int* path) {
   if (!h || !path) return fail(QQA_ERR_INVALID_ARG, "handle or path is NULL");
-  *path = h->s.kary ? QQA_PATH_KARY : use_persistent(h, 2) ? QQA_PATH_PERSISTENT : QQA_PATH_STEP;
+  *path = h->s.kary ? QQA_PATH_KARY : use_cluster(h, 2) ? QQA_PATH_CLUSTER
+                                    : use_persistent(h, 2) ? QQA_PATH_PERSISTENT : QQA_PATH_STEP;
   return QQA_OK;
 }
 

@@ -38,6 +38,9 @@ RunKernel run_kernel_m9(int lanes, int vpl, int cta);
 RunKernel run_kernel_m10(int lanes, int vpl, int cta);
 RunKernel run_kernel_m11(int lanes, int vpl, int cta);
 
+// k_run_cluster<MODE> (MODE 0..3, compiled in k_cluster.cu); nullptr otherwise.
+RunKernel cluster_kernel(int mode);
+
 // K-ary kernels for KP in {4, 8, 12, 16}; false otherwise.
 bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);
 }  // namespace qqa

@@ -580,6 +580,7 @@ struct RunParams {
   long long t0;                         // Adam steps taken before this launch
   int nsteps, cur0, scur0;
   double S_total;
+  int rows_cta;                         // k_run_cluster: rows per CTA of the cluster
 };
 
 // CT (CTA threads): 1024 = one CTA per SM (32 warps) owning a CONTIGUOUS row range, so an SM
@@ -622,6 +623,135 @@ __global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 2 ? 2 : QQA_STEP
     cg::this_grid().sync();
   }
   if (bad) atomicOr(P.flag, 1);
+}
+
+// Tiny problems (c1: n S_p = 4096): the whole anneal in ONE thread-block cluster, all state in
+// shared memory. CTA r of the cluster owns rows [r R, (r+1) R) (R = rows_cta): their theta / m / v,
+// both p buffers, shift and fixed-point sums live in its shared memory; a neighbour row owned by
+// another CTA is read through distributed shared memory (mapa). Per step: the CTA finalizes its
+// rows' (mu, STD), __syncthreads, one thread per element gathers (CSR order, skipping the trailing
+// sentinel entries: + 0 leaves the sum unchanged), updates and adds its fixed-point terms into the
+// row's sums (shared int64 atomics: exact, order-free), then one cluster barrier publishes p_next.
+// No global memory traffic between the first load and the final write-back, no grid barrier.
+// Same buffers in and out as k_run (p / c ping-pong, sums mod 3), bit-identical.
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) k_run_cluster(const RunParams R) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const StepParams& P = R.P;
+  const int RC = R.rows_cta, SP = P.SB, S = P.S_local, n = P.n;   // RC a power of two
+  const int rsh = __ffs(RC) - 1;
+  const int r0 = (int)cl.block_rank() * RC;
+  const int nr = max(0, min(RC, n - r0));
+  const int tid = threadIdx.x, nt = blockDim.x;
+  extern __shared__ float4 smem_f4[];
+  float* sth = reinterpret_cast<float*>(smem_f4);      // [RC][SP] each
+  float* smm = sth + (size_t)RC * SP;
+  float* svv = smm + (size_t)RC * SP;
+  float* spb[2] = {svv + (size_t)RC * SP, svv + 2 * (size_t)RC * SP};
+  long long* ssum = reinterpret_cast<long long*>(svv + 3 * (size_t)RC * SP);   // [2 buffers][2][RC]
+  float* sc = reinterpret_cast<float*>(ssum + 4 * (size_t)RC);                // [RC]
+  float2* sms = reinterpret_cast<float2*>(sc + ((RC + 1) & ~1));              // [RC]
+  {
+    const float* pg = R.p[R.cur0 & 1];
+    for (int e = tid; e < nr * SP; e += nt) {
+      const size_t g = (size_t)r0 * SP + e;
+      sth[e] = P.theta[g]; smm[e] = P.m[g]; svv[e] = P.v[g]; spb[0][e] = pg[g];
+    }
+    const long long* sg = R.sums[R.scur0];
+    for (int r = tid; r < nr; r += nt) {
+      sc[r] = R.c[R.cur0 & 1][r0 + r];
+      ssum[r] = sg[r0 + r];
+      ssum[RC + r] = sg[n + r0 + r];
+    }
+  }
+  cl.sync();
+  bool bad = false;
+  for (int j = 0; j < R.nsteps; ++j) {
+    const float4 sch = R.sched[j];
+    const unsigned long long t = (unsigned long long)(R.t0 + j + 1);
+    const StepVar V{nullptr, nullptr, nullptr, nullptr, sch.x, sch.y, sch.z,
+                    R.nbase + t * (unsigned long long)n * P.S_total_u};
+    long long* scur = ssum + (size_t)(j & 1) * 2 * RC;
+    long long* snext = ssum + (size_t)((j + 1) & 1) * 2 * RC;
+    for (int r = tid; r < nr; r += nt) {   // (mu_i, STD_i) of the current p; shift of the next sums
+      float mu, sd;
+      finalize_stats(sc[r], scur[r], scur[RC + r], R.S_total, mu, sd);
+      sms[r] = make_float2(mu, sd);
+      sc[r] = mu;
+      snext[r] = 0;
+      snext[RC + r] = 0;
+    }
+    __syncthreads();
+    const float* pc = spb[j & 1];
+    float* pn = spb[(j + 1) & 1];
+    // S a power of two <= 32: a row's S elements are S adjacent lanes of one warp (nt is a multiple
+    // of 32), so its fixed-point terms are shuffle-reduced and stored by one lane; else atomics.
+    const bool lanes_row = (S & (S - 1)) == 0 && S <= 32;
+    for (int base = 0; base < nr * S; base += nt) {
+      const int e = base + tid;
+      const bool live = e < nr * S;
+      const int r = live ? e / S : 0, s = e - r * S, i = r0 + r;
+      long long D = 0, D2 = 0;
+      if (live) {
+        float q = 0.0f;   // CSR order, 4 neighbour rows per round (DSMEM loads first, then the adds);
+                          // the sentinel n of the row padding contributes +0, which leaves q unchanged
+        for (int k = __ldg(P.rowptr_pad + i), k1 = __ldg(P.rowptr_pad + i + 1); k < k1; k += 4) {
+          const int4 j4 = __ldg(reinterpret_cast<const int4*>(P.colidx_pad + k));
+          const int js[4] = {j4.x, j4.y, j4.z, j4.w};
+          float vals[4];
+  #pragma unroll
+          for (int u = 0; u < 4; ++u)
+            vals[u] = (js[u] < n) ? cl.map_shared_rank(pc, js[u] >> rsh)[(size_t)(js[u] & (RC - 1)) * SP + s] : 0.0f;
+  #pragma unroll
+          for (int u = 0; u < 4; ++u) q = fadd(q, vals[u]);
+        }
+        const int at = r * SP + s;
+        const float degf = (P.problem == kMAXCUT) ? (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i)) : 0.0f;
+        const float z = (MODE & kModeNoise) ? noise_of(V.nkey + (unsigned long long)i * P.S_total_u, P.off + s) : 0.0f;
+        float th = sth[at], mm = smm[at], vv = svv[at];
+        const float pi = (MODE & kModeClamp) ? th : pc[at];
+        const float2 st = sms[r];
+        const float pv = update_element<MODE>(P, V, q, degf, pi, st.x, st.y, th, mm, vv, z, bad);
+        sth[at] = th; smm[at] = mm; svv[at] = vv; pn[at] = pv;
+        stat_terms(pv, st.x, D, D2);
+      }
+      if (lanes_row) {
+        for (int off = S / 2; off > 0; off >>= 1) {
+          D += __shfl_xor_sync(0xffffffffu, D, off, S);
+          D2 += __shfl_xor_sync(0xffffffffu, D2, off, S);
+        }
+        if (live && s == 0) { snext[r] = D; snext[RC + r] = D2; }
+      } else if (live) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(snext + r), (unsigned long long)D);
+        atomicAdd(reinterpret_cast<unsigned long long*>(snext + RC + r), (unsigned long long)D2);
+      }
+    }
+    cl.sync();   // p_next of every CTA written; every read of p_cur done
+  }
+  {  // write back in the k_run buffer convention
+    const int cf = (R.cur0 + R.nsteps) & 1;
+    float* pg = R.p[cf];
+    const float* pl = spb[R.nsteps & 1];
+    for (int e = tid; e < nr * SP; e += nt) {
+      const size_t g = (size_t)r0 * SP + e;
+      P.theta[g] = sth[e]; P.m[g] = smm[e]; P.v[g] = svv[e]; pg[g] = pl[e];
+    }
+    long long* sg = R.sums[(R.scur0 + R.nsteps) % 3];
+    const long long* sl = ssum + (size_t)(R.nsteps & 1) * 2 * RC;
+    for (int r = tid; r < nr; r += nt) {
+      R.c[cf][r0 + r] = sc[r];
+      sg[r0 + r] = sl[r];
+      sg[n + r0 + r] = sl[RC + r];
+    }
+  }
+  if (bad) atomicOr(P.flag, 1);
+}
+
+// Shared memory of k_run_cluster for rows_cta rows of SP columns.
+__host__ __device__ inline size_t cluster_smem_bytes(int rows_cta, int SP) {
+  return (size_t)rows_cta * SP * 5 * sizeof(float) + (size_t)rows_cta * 4 * sizeof(long long) +
+         (size_t)((rows_cta + 1) & ~1) * sizeof(float) + (size_t)rows_cta * sizeof(float2);
 }
 
 // ------------------------------------------------------------------- K1

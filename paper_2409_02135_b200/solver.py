@@ -208,10 +208,10 @@ class Solver:
         check(lib.qqa_launch_count(self._h, ctypes.byref(k)))
         return int(k.value)
 
-    STEP_PATHS = ("step", "persistent", "kary")
+    STEP_PATHS = ("step", "persistent", "kary", "cluster")
 
     def step_path(self) -> str:
-        """The step kernel a run of >= 2 steps uses: 'step', 'persistent' or 'kary' (qqa_step_path)."""
+        """The step kernel a run of >= 2 steps uses: 'step', 'persistent', 'cluster' or 'kary' (qqa_step_path)."""
         k = ctypes.c_int(0)
         check(lib.qqa_step_path(self._h, ctypes.byref(k)))
         return self.STEP_PATHS[k.value]

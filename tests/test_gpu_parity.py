@@ -395,7 +395,7 @@ def test_persistent_cta_layouts_identical(Q, monkeypatch, cta):
         assert np.array_equal(a.get_state()[k], b.get_state()[k]), k
 
 
-@pytest.mark.parametrize("name,path,SB", [("c1", "persistent", 16), ("c3", "persistent", 256), ("c4", "persistent", 512),
+@pytest.mark.parametrize("name,path,SB", [("c1", "cluster", 16), ("c3", "persistent", 256), ("c4", "persistent", 512),
                                           ("c5", "step", 32), ("q13", "kary", 0)])
 def test_step_path_and_replica_block(Q, name, path, SB):
     """Kernel selection of bench.py's workloads: c5's p (256 MB) exceeds the 128 MB
@@ -405,3 +405,51 @@ def test_step_path_and_replica_block(Q, name, path, SB):
     hp = {k: v for k, v in w.hparams().items() if k != "problem"}
     sol = Q.Solver(g.rowptr, g.colidx, Q.make_config(w.problem, S_total=w.S, seed=w.seeds[0], **hp))
     assert sol.step_path() == path and sol.replica_block() == SB
+
+
+@pytest.mark.parametrize("problem,n,S,mp,T", [("mis", 256, 16, "sigmoid", 0.0), ("maxcut", 300, 100, "clamp", 0.001),
+                                              ("maxclique", 60, 24, "sigmoid", 0.001), ("mis", 1000, 32, "clamp", 0.0),
+                                              ("mis", 7, 3, "sigmoid", 0.0), ("maxcut", 2000, 13, "sigmoid", 0.001)])
+def test_cluster_equals_launch_per_step(Q, monkeypatch, problem, n, S, mp, T):
+    """The one-cluster shared-memory anneal (k_run_cluster: rows spread over the cluster's CTAs,
+    neighbour rows through distributed shared memory, one cluster barrier per step) is bit-identical
+    to one k_finalize + k_step launch per step, across a schedule-table chunk (4096 steps)."""
+    g = gen.erdos_renyi(n, 0.5, 12) if problem == "maxclique" else gen.erdos_renyi(n, min(0.5, 6.0 / n), 12)
+    steps = 4100 if (n, S) == (256, 16) else 300
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("QQA_CLUSTER", flag)
+        monkeypatch.setenv("QQA_PERSISTENT", "0")
+        sol = gpu(Q, g, problem, S, 4, map=mp, temperature=T, comm=0.3)
+        assert sol.step_path() == ("cluster" if flag == "1" else "step")
+        sol.profile(True)
+        l0 = sol.launch_count()
+        sol.run_linear(-2.0, 0.1, steps)
+        launches = sol.launch_count() - l0
+        assert sol.profile_read()[1] == steps
+        out.append((sol.get_state(), sol.get_stats(), launches, sol.round_evaluate()))
+    (a, sa, la, ra), (b, sb, lb, rb) = out
+    for k in ("theta", "m", "v", "p"):
+        assert np.array_equal(a[k], b[k]), k
+    for k in ("c", "sumD", "sumD2"):
+        assert np.array_equal(sa[k], sb[k]), k
+    assert ra.best_replica == rb.best_replica and np.array_equal(ra.best_x, rb.best_x)
+    assert la == (steps + 4095) // 4096 and lb == 2 * steps
+
+
+def test_cluster_then_resume_on_other_paths(Q, monkeypatch):
+    """Buffers after a cluster run follow the k_run convention: continuing on k_step, or through a
+    checkpoint, gives the uninterrupted result."""
+    g = gen.random_regular(256, 3, 1)
+    a = gpu(Q, g, "mis", 16, 9)
+    assert a.step_path() == "cluster"
+    a.run_linear(-2.0, 0.1, 400, 0, 150)
+    monkeypatch.setenv("QQA_CLUSTER", "0")
+    monkeypatch.setenv("QQA_PERSISTENT", "0")
+    a.run_linear(-2.0, 0.1, 400, 150, 151)     # one step: launch-per-step path
+    monkeypatch.delenv("QQA_CLUSTER")
+    monkeypatch.delenv("QQA_PERSISTENT")
+    a.run_linear(-2.0, 0.1, 400, 151, 400)
+    st = oracle.run(g, ocfg("mis", 16, 9), oracle.schedule(-2.0, 0.1, 400))
+    assert_state_equal(a, st)
+    assert_stats_equal(a, st)
