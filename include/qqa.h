@@ -254,7 +254,7 @@ QQA_API int qqa_launch_count(qqa_handle* h, int64_t* launches);
  *   QQA_PATH_PERSISTENT  k_run: one cooperative launch per <= 4096 steps (one GPU, p in L2)
  *   QQA_PATH_KARY        k_step_K (graph colouring)
  *   QQA_PATH_CLUSTER     k_run_cluster: the whole anneal in one thread-block cluster's shared memory
- *                        (one GPU, n * S_p <= 32768) */
+ *                        (one GPU, n * S_p <= 32768 and padded nnz * S_p <= 2^19) */
 enum { QQA_PATH_STEP = 0, QQA_PATH_PERSISTENT = 1, QQA_PATH_KARY = 2, QQA_PATH_CLUSTER = 3 };
 QQA_API int qqa_step_path(qqa_handle* h, int* path);
 /* Replica block SB of the layout [B][n+1][SB] (0 for colouring). Host-only. */

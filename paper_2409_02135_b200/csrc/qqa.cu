@@ -50,7 +50,8 @@ int fail(int status, const std::string& msg) {
 
 constexpr size_t kAlign = 256;
 constexpr int kSchedCap = 4096;   // steps per persistent launch (device table of per-step scalars)
-constexpr int64_t kClusterMaxElems = 1 << 15;  // n S_p up to this runs in one thread-block cluster (k_run_cluster)
+constexpr int64_t kClusterMaxElems = 1 << 15;   // n S_p up to this runs in one thread-block cluster (k_run_cluster)
+constexpr int64_t kClusterMaxGather = 1 << 19;  // ... if its DSMEM gather (padded nnz x S_p values per step) is small
 constexpr double kL2BlockBudget = 128.0 * 1024 * 1024;  // p larger than this is replica-blocked (measured)
 size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -1060,7 +1061,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
     if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
     if (s.B == 1 && !s.weighted && cfg->problem != QQA_MAXCLIQUE_SPARSE && s.n > 0 &&
-        (int64_t)s.n * s.S_p <= kClusterMaxElems) {   // tiny problem: one thread-block cluster (k_run_cluster)
+        (int64_t)s.n * s.S_p <= kClusterMaxElems && s.nnz_pad * s.S_p <= kClusterMaxGather) {   // tiny: one cluster
       const qqa::RunKernel kc = qqa::cluster_kernel(step_mode(*cfg, s.weighted));
       for (int cs : {16, 8}) {
         if (!kc) break;
