@@ -706,7 +706,16 @@ int do_steps_cluster(qqa_handle* h, const float* gamma, int64_t n_steps) {
     lc.numAttrs = 1;
     int st;
     if ((st = record_start(h))) return st;
-    QQA_CUDA(cudaLaunchKernelEx(&lc, kc, R));
+    const cudaError_t le = cudaLaunchKernelEx(&lc, kc, R);
+    if (le == cudaErrorClusterOutOfResources || le == cudaErrorLaunchOutOfResources ||
+        le == cudaErrorInvalidClusterSize) {
+      // the cluster cannot be placed now (e.g. a shared GPU): the remaining steps run on the other
+      // (bit-identical) paths and the handle stops using k_run_cluster
+      (void)cudaGetLastError();
+      h->cluster_cs = 0;
+      return do_steps(h, gamma + k0, n_steps - k0);
+    }
+    QQA_CUDA(le);
     h->launches++;
     if (h->profiling) {   // one launch = nk steps
       QQA_CUDA(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
