@@ -707,7 +707,7 @@ int do_steps_cluster(qqa_handle* h, const float* gamma, int64_t n_steps) {
     int st;
     if ((st = record_start(h))) return st;
     const cudaError_t le = cudaLaunchKernelEx(&lc, kc, R);
-    if (le == cudaErrorClusterOutOfResources || le == cudaErrorLaunchOutOfResources ||
+    if (le == cudaErrorLaunchOutOfResources || le == cudaErrorCooperativeLaunchTooLarge ||
         le == cudaErrorInvalidClusterSize) {
       // the cluster cannot be placed now (e.g. a shared GPU): the remaining steps run on the other
       // (bit-identical) paths and the handle stops using k_run_cluster
