@@ -159,7 +159,7 @@ def run_reference(args, w):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                              "cpu": model},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 args_lr_override = [None]
@@ -187,7 +187,21 @@ def workload_config(w, world):
                   if state_bytes > 132e6 else "state fits L2 (no flush)"}
 
 
+# The driver reads ONE JSON line from stdout. Libraries may print there (NCCL prints its version line
+# on stdout), so for the whole run file descriptor 1 points at stderr and only the result line is
+# written to the original stdout.
+_RESULT_FD = None
+
+
+def emit(line: dict) -> None:
+    os.write(_RESULT_FD if _RESULT_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _RESULT_FD
+    sys.stdout.flush()
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -198,6 +212,11 @@ def main():
     ap.add_argument("--temperature", type=float, default=None, help="Langevin T (NEXT-2; the paper: 0.001)")
     ap.add_argument("--alpha", type=int, default=None, help="override the alpha-entropy exponent (the paper: 4, P:244)")
     ap.add_argument("--lr", type=float, default=None, help="override the AdamW learning rate (the paper: 1, 0.1 or 0.01, P:670)")
+    ap.add_argument("--exchange", choices=["auto", "fused", "nccl"], default="auto",
+                    help="N > 1: per-step statistics exchange -- fused peer-memory exchange inside the step "
+                         "kernel (auto: after a bit-exact self-check against NCCL) or the NCCL all-reduce")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="diagnostics: run the N > 1 code path (process group, NCCL communicator, exchange) at N = 1")
     ap.add_argument("--replicas", type=int, default=None, help="override S (diagnostics: per-rank work of a sharded run)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--anneal-steps", type=int, default=None, help="override T (diagnostics only)")
@@ -238,8 +257,14 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    sharded = world > 1 or args.force_dist   # the multi-GPU code path (--force-dist: also at N = 1)
+    if sharded:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29541")
+            dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     offset, S_l = qdist.shard(w.S, world, rank)
     (g, gor), seed = w.batched(), w.seeds[0]
     hp = {k: v for k, v in w.hparams().items() if k != "problem"}
@@ -247,7 +272,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize(dev)
 
@@ -255,8 +280,59 @@ def main():
         return qdist.max_over_ranks(x, device=dev)
 
     sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
-    if world > 1:
+    exchange, xptrs, exchange_probe = None, None, None
+    if sharded:
         qdist.attach(sol, rank, world)
+        exchange = "nccl all-reduce (4-chunk overlap)"
+        if args.exchange != "nccl" and not w.n_colors:
+            try:
+                xptrs = qdist.attach_exchange(sol, rank, world)
+                ok_attach = 1
+            except Exception as e:   # no symmetric memory / peer mapping here: stay on NCCL
+                print(f"fused exchange unavailable: {e!r}", file=sys.stderr)
+                ok_attach = 0
+            t_ok = torch.tensor([ok_attach], dtype=torch.int32, device=dev)
+            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+            if int(t_ok.item()) == 0:
+                if xptrs is not None:   # this rank attached, another did not: back to a plain NCCL handle
+                    sol.close()
+                    sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
+                    qdist.attach(sol, rank, world)
+                xptrs = None
+            else:
+                exchange = "fused peer-memory exchange in k_step_x"
+        if xptrs is not None and args.exchange == "auto":   # bit-exact self-check against NCCL, agreed by all ranks
+            ref = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
+            ref.share_comm(sol)
+            for s in (sol, ref):
+                s.reset()
+                s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 3)
+            a, b = sol.get_state(), ref.get_state()
+            ok = all(np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)) for k in ("theta", "m", "v", "p"))
+            ok = ok and np.array_equal(sol.get_stats()["sumD2"], ref.get_stats()["sumD2"])
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:   # both exact: keep the faster one (max over ranks, 5 steps each)
+                def probe(s):
+                    s.reset()
+                    barrier()
+                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a0.record(stream)
+                    s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 5)
+                    a1.record(stream)
+                    barrier()
+                    return max_over_ranks(a0.elapsed_time(a1)) / 5
+                exchange_probe = {"fused_ms_per_step": probe(sol), "nccl_ms_per_step": probe(ref)}
+                if exchange_probe["nccl_ms_per_step"] < exchange_probe["fused_ms_per_step"]:
+                    sol.close()
+                    sol, xptrs = ref, None
+                    exchange = "nccl all-reduce (4-chunk overlap; faster than the fused exchange here)"
+                else:
+                    ref.close()
+            else:
+                sol.close()
+                sol, xptrs = ref, None
+                exchange = "nccl all-reduce (4-chunk overlap; fused exchange failed its self-check)"
 
     def evaluate(s):
         if gor is not None:   # batch: every instance's best replica (NEXT-3)
@@ -314,8 +390,10 @@ def main():
 
         def e2e_step():
             s = Q.Solver(rp, ci, cfg, device=dev, stream=stream, workspace=ws, group_of_row=gp)
-            if world > 1:
+            if sharded:
                 s.share_comm(sol)
+                if xptrs is not None:   # re-attach the (now idle) exchange buffers of the timed handle
+                    s.attach_exchange(xptrs, rank, world)
             s.run_linear(w.gamma_min, w.gamma_max, w.steps)
             r = (s.round_evaluate_groups(want_x=True, want_counts=True) if gp is not None
                  else s.round_evaluate(want_x=True, want_replicas=True))
@@ -350,7 +428,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(w, world),
+                "config": dict(workload_config(w, world), **({"exchange": exchange} if exchange else {}),
+                               **({"exchange_probe": exchange_probe} if exchange_probe else {})),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
                              # the DRAM bytes ncu measured per launch over the same launch time: the byte
@@ -358,15 +437,17 @@ def main():
                              "traffic_achieved": (traffic / avg_kernel_s / 1e9) if traffic else None,
                              "traffic_frac": (traffic / avg_kernel_s / 1e9 / peak) if traffic else None,
                              "kernel": ("qqa::k_step_K (fused K-ary gather + gradient + AdamW + normalise + stats)"
-                                        if w.n_colors else "qqa::k_step (fused gather + gradient + AdamW + stats)"),
+                                        if w.n_colors else
+                                        "qqa::k_step_x (fused gather + gradient + AdamW + stats + peer exchange)"
+                                        if xptrs is not None else "qqa::k_step (fused gather + gradient + AdamW + stats)"),
                              "bytes_per_launch": B, "avg_launch_ms": avg_kernel_s * 1e3,
                              "launches_timed": kern_launches, "peak_source": peak_src,
                              "step_kernel_share": kern_ms / t_ms},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": l1 - l0, "clocks": clocks,
                 "result": ({"best_replica": res.best_replica, "best_energy": res.best_energy} if gor is None else
                            {"instances": len(w.graphs), "best_energy_per_instance": [float(x) for x in res.best_energy]})}
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        emit(line)
+    if sharded:
         dist.destroy_process_group()
 
 

@@ -194,6 +194,22 @@ QQA_API int qqa_share_comm(qqa_handle* h, qqa_handle* donor);
  * reset / set_state); qqa_loopback_run then runs n_steps in lockstep, adding the int64 sums of all
  * shards after every step -- exactly the per-step NCCL all-reduce -- so the shards reproduce one
  * handle holding all S_total replicas bit for bit. No kernel waits on another. (sync) */
+/* Fused statistics exchange over peer memory, replacing the per-step NCCL all-reduce
+ * of Eq. 10's sums: rank r owns rows [r ceil(n/G), (r+1) ceil(n/G)) of the int64 sums; each step
+ * kernel adds its replicas' terms of row i directly into the OWNER's buffer (atomics at the owner,
+ * over NVLink, issued as rows complete) and reads row i's total from the owner at the next step;
+ * step boundaries are an arrival-counter barrier in the same buffers. Bit-identical to the NCCL
+ * path (exact integer sums).
+ *   qqa_exchange_bytes: size of one rank's exchange buffer (device memory, 256-byte aligned, caller-
+ *     owned, e.g. torch symmetric memory), identical on every rank.
+ *   qqa_attach_exchange: peer_bufs[r] = rank r's exchange buffer as mapped in THIS process (its own
+ *     at r = rank); every rank calls it (collectively when a communicator is attached, which stays
+ *     in use for init and evaluation). Zeroes this rank's buffer and re-initialises the replicas.
+ *     Without a communicator (shards emulated on one device) call qqa_loopback_sync_init next.
+ *   Supported: binary problems without edge weights or the printed clique (else UNSUPPORTED). A peer
+ *   that never arrives is reported as QQA_ERR_COMM at the next synchronising call (no hang). */
+QQA_API int qqa_exchange_bytes(qqa_handle* h, size_t* bytes);
+QQA_API int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks);
 QQA_API int qqa_loopback_sync_init(qqa_handle** hs, int G);
 QQA_API int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps);
 
@@ -253,9 +269,10 @@ QQA_API int qqa_launch_count(qqa_handle* h, int64_t* launches);
  *   QQA_PATH_STEP        one k_finalize + k_step launch per annealing step
  *   QQA_PATH_PERSISTENT  k_run: one cooperative launch per <= 4096 steps (one GPU, p in L2)
  *   QQA_PATH_KARY        k_step_K (graph colouring)
+ *   QQA_PATH_EXCHANGE    k_step_x: sharded replicas with the fused statistics exchange (qqa_attach_exchange)
  *   QQA_PATH_CLUSTER     k_run_cluster: the whole anneal in one thread-block cluster's shared memory
  *                        (one GPU, n * S_p <= 32768 and padded nnz * S_p <= 2^19) */
-enum { QQA_PATH_STEP = 0, QQA_PATH_PERSISTENT = 1, QQA_PATH_KARY = 2, QQA_PATH_CLUSTER = 3 };
+enum { QQA_PATH_STEP = 0, QQA_PATH_PERSISTENT = 1, QQA_PATH_KARY = 2, QQA_PATH_CLUSTER = 3, QQA_PATH_EXCHANGE = 4 };
 QQA_API int qqa_step_path(qqa_handle* h, int* path);
 /* Replica block SB of the layout [B][n+1][SB] (0 for colouring). Host-only. */
 QQA_API int qqa_replica_block(qqa_handle* h, int* SB);

@@ -80,6 +80,8 @@ def _declare(lib):
         "qqa_profile_read": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
         "qqa_launch_count": (ctypes.c_int, [H, ctypes.POINTER(i64)]),
         "qqa_step_path": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_int)]),
+        "qqa_exchange_bytes": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_size_t)]),
+        "qqa_attach_exchange": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.c_int]),
         "qqa_replica_block": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_int)]),
         "qqa_destroy": (ctypes.c_int, [H]),
     }

@@ -25,6 +25,17 @@ StepKernel step_for(int lanes, int vpl) {
 }
 
 template <int M>
+XStepKernel xstep_for(int lanes, int vpl) {
+  if (M & (kModeSparseClique | kModeWeighted)) return nullptr;   // fused exchange: modes 0-3
+#define QQA_XCASE(L, V) \
+  if (lanes == L && vpl == V) return k_step_x<L, V, (M & 3)>;
+  QQA_XCASE(1, 1) QQA_XCASE(2, 1) QQA_XCASE(4, 1) QQA_XCASE(8, 1) QQA_XCASE(16, 1)
+  QQA_XCASE(32, 1) QQA_XCASE(32, 2) QQA_XCASE(32, 4)
+#undef QQA_XCASE
+  return nullptr;
+}
+
+template <int M>
 RunKernel run_kernel_for(int lanes, int vpl, int cta) {
   if (M & kModeSparseClique) return nullptr;   // its column sums need a pass between steps: no k_run
   return (cta == 1024 && vpl == 1) ? run_for<M, 1024>(lanes, vpl) : run_for<M, 256>(lanes, vpl);

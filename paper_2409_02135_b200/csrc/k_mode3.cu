@@ -4,4 +4,5 @@
 namespace qqa {
 StepKernel step_kernel_m3(int lanes, int vpl) { return step_for<3>(lanes, vpl); }
 RunKernel run_kernel_m3(int lanes, int vpl, int cta) { return run_kernel_for<3>(lanes, vpl, cta); }
+XStepKernel xstep_kernel_m3(int lanes, int vpl) { return xstep_for<3>(lanes, vpl); }
 }  // namespace qqa

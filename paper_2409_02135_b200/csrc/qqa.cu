@@ -307,6 +307,14 @@ struct qqa_handle {
   long long* wsums = nullptr;  // [S_total][2] evaluation weight sums (fixed point 2^24)
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
   int run_cta = 256;           // threads per CTA of k_run (1024: contiguous rows per SM)
+  // fused statistics exchange over peer memory (qqa_attach_exchange; k_step_x instead of k_step + NCCL)
+  bool xmode = false;
+  int xrank = 0, xG = 1;
+  long long* xsums[qqa::kMaxRanks][3] = {};     // every rank's sums buffers, mapped in this process
+  unsigned long long* xflag[qqa::kMaxRanks] = {};
+  unsigned int* xticket = nullptr;
+  unsigned long long xsync = 0;                  // barriers so far (each adds G arrivals to every counter)
+  long long* ws_sums[3] = {nullptr, nullptr, nullptr};   // the workspace's own sums (get_stats scratch)
   int cluster_cs = 0;          // k_run_cluster: CTAs per cluster (0: not available for this handle)
   int cluster_rows = 0;        // rows per CTA of the cluster
   size_t cluster_smem = 0;
@@ -451,6 +459,45 @@ int launch_init_kary(qqa_handle* h, bool use_given, const float* c_given) {
   return QQA_OK;
 }
 
+qqa::XParams make_xparams(const qqa_handle* h, int sa, int sb, int sz, int a, int b) {
+  qqa::XParams X{};
+  for (int r = 0; r < h->xG; ++r) {
+    X.peer_cur[r] = h->xsums[r][sa];
+    X.peer_next[r] = h->xsums[r][sb];
+    X.peer_flag[r] = h->xflag[r];
+  }
+  X.zero = h->xsums[h->xrank][sz];
+  X.flag = h->xflag[h->xrank];
+  X.ticket = h->xticket;
+  X.c_cur = h->c[a];
+  X.c_next = h->c[b];
+  X.expect = (unsigned long long)h->xG * h->xsync;
+  X.rank = h->xrank;
+  X.G = h->xG;
+  X.rows_per_rank = std::max(1, (h->s.n + h->xG - 1) / h->xG);
+  return X;
+}
+
+// This rank's arrival at an exchange barrier (after the initial statistics are complete).
+int x_arrive(qqa_handle* h) {
+  const qqa::XParams X = make_xparams(h, h->scur, h->scur, h->scur, h->cur, h->cur);
+  qqa::k_x_arrive<<<1, 32, 0, h->stream>>>(X);
+  QQA_CUDA(cudaGetLastError());
+  h->launches++;
+  h->xsync++;
+  return QQA_OK;
+}
+
+qqa::XStepKernel pick_xstep(int lanes, int vpl, int mode) {
+  switch (mode) {
+    case 0: return qqa::xstep_kernel_m0(lanes, vpl);
+    case 1: return qqa::xstep_kernel_m1(lanes, vpl);
+    case 2: return qqa::xstep_kernel_m2(lanes, vpl);
+    case 3: return qqa::xstep_kernel_m3(lanes, vpl);
+    default: return nullptr;
+  }
+}
+
 int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   if (h->s.kary) return launch_init_kary(h, use_given, c_given);
   StepKernel ks;
@@ -477,6 +524,12 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
   }
   if (h->comm) {
     QQA_NCCL(ncclAllReduce(h->sums[0], h->sums[0], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
+  }
+  h->cur = 0;
+  h->scur = 0;
+  if (h->xmode && h->comm) {   // every rank's sums[0] holds the totals: first exchange barrier
+    int st;
+    if ((st = x_arrive(h))) return st;
   }
   if (h->cfg.problem == QQA_MAXCLIQUE_SPARSE) {
     int st;
@@ -569,7 +622,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps);
 // one-GPU, unblocked problems of up to 2^24 replica-variables (L2-resident / launch-bound);
 // QQA_PERSISTENT=0/1 overrides. Bit-identical to the launch-per-step path.
 bool use_persistent(const qqa_handle* h, int64_t n_steps) {
-  if (h->grid_run <= 0 || h->comm || h->s.B != 1 || h->s.kary || h->s.n == 0 || n_steps < 2 ||
+  if (h->grid_run <= 0 || h->comm || h->xmode || h->s.B != 1 || h->s.kary || h->s.n == 0 || n_steps < 2 ||
       h->cfg.problem == QQA_MAXCLIQUE_SPARSE)   // its column sums need a pass between steps
     return false;
   if (const char* env = std::getenv("QQA_PERSISTENT")) return std::atoi(env) != 0;
@@ -648,7 +701,7 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
 // One-cluster path (k_run_cluster): one GPU, unblocked, n S_p <= kClusterMaxElems. QQA_CLUSTER=0/1
 // overrides; an explicit QQA_PERSISTENT selects k_run / k_step instead.
 bool use_cluster(const qqa_handle* h, int64_t n_steps) {
-  if (h->cluster_cs <= 0 || h->comm || n_steps < 2) return false;
+  if (h->cluster_cs <= 0 || h->comm || h->xmode || n_steps < 2) return false;
   if (const char* env = std::getenv("QQA_CLUSTER")) return std::atoi(env) != 0;
   return std::getenv("QQA_PERSISTENT") == nullptr;
 }
@@ -729,10 +782,58 @@ int do_steps_cluster(qqa_handle* h, const float* gamma, int64_t n_steps) {
   return QQA_OK;
 }
 
+// Fused-exchange steps: one k_step_x launch per step (it waits for the previous step's barrier,
+// finalizes from the owners' sums, adds into the owners' next sums and arrives); no NCCL, no k_finalize.
+int do_steps_x(qqa_handle* h, const float* gamma, int64_t n_steps) {
+  const qqa_config& c = h->cfg;
+  const qqa::XStepKernel kx = pick_xstep(h->s.lanes, h->s.vpl, step_mode(c, h->s.weighted));
+  if (!kx) return fail(QQA_ERR_UNSUPPORTED, "no fused-exchange kernel for this mode");
+  qqa::StepParams P{};
+  P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
+  P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
+  P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
+  P.off = c.replica_offset;
+  P.row_begin = 0; P.row_end = h->s.n;
+  P.problem = problem_kind(c.problem);
+  P.alpha = c.alpha; P.lam = c.penalty; P.comm = c.comm;
+  P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
+  P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
+  P.eps = c.eps;
+  P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
+  P.ns = (float)std::sqrt(2.0 * (double)c.lr * (double)c.temperature);
+  P.S_total_u = (unsigned long long)h->s.S_total;
+  const uint64_t nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);
+  for (int64_t k = 0; k < n_steps; ++k) {
+    const int64_t t = h->step + 1;
+    P.var.nkey = nbase + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total;
+    P.var.kt = (float)(-2.0 * (double)c.alpha * (double)gamma[k]);
+    P.var.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
+    P.var.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
+    const int a = h->cur, b = h->cur ^ 1;
+    const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
+    P.var.p_cur = h->p[a]; P.var.p_next = h->p[b];
+    if (h->s.n > 0) {
+      const qqa::XParams X = make_xparams(h, sa, sb, sz, a, b);
+      int st;
+      if ((st = record_start(h))) return st;
+      kx<<<h->grid_step, 256, 0, h->stream>>>(P, X);
+      QQA_CUDA(cudaGetLastError());
+      h->launches++;
+      h->xsync++;
+      if ((st = record_end(h))) return st;
+    }
+    h->cur = b;
+    h->scur = sb;
+    h->step = t;
+  }
+  return QQA_OK;
+}
+
 int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (n_steps < 0) return fail(QQA_ERR_INVALID_ARG, "n_steps < 0");
   if (n_steps > 0 && !gamma) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
   if (h->s.kary) return do_steps_kary(h, gamma, n_steps);
+  if (h->xmode) return do_steps_x(h, gamma, n_steps);
   if (use_cluster(h, n_steps)) return do_steps_cluster(h, gamma, n_steps);
   if (use_persistent(h, n_steps)) return do_steps_persistent(h, gamma, n_steps);
   StepKernel ks;
@@ -1233,6 +1334,8 @@ int qqa_loopback_sync_init(qqa_handle** hs, int G) {
   if (st) return st;
   if ((st = set_device(hs[0]))) return st;
   if ((st = loopback_reduce(hs, G))) return st;
+  for (int r = 0; r < G; ++r)   // fused-exchange shards: the totals are in place, first barrier
+    if (hs[r]->xmode && (st = x_arrive(hs[r]))) return st;
   QQA_CUDA(cudaStreamSynchronize(hs[0]->stream));
   return QQA_OK;
 }
@@ -1246,7 +1349,7 @@ int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_
   for (int64_t k = 0; k < n_steps; ++k) {
     for (int r = 0; r < G; ++r)   // one launch-per-step step of every shard (n_steps = 1: no k_run)
       if ((st = do_steps(hs[r], gamma_host + k, 1))) return st;
-    if ((st = loopback_reduce(hs, G))) return st;
+    if (!hs[0]->xmode && (st = loopback_reduce(hs, G))) return st;   // fused shards exchanged in-kernel
   }
   QQA_CUDA(cudaStreamSynchronize(hs[0]->stream));
   return QQA_OK;
@@ -1403,6 +1506,7 @@ int finish_eval(qqa_handle* h) {
     ncclCommGetAsyncError(h->comm, &async_err);
     if (async_err != ncclSuccess) return fail(QQA_ERR_COMM, ncclGetErrorString(async_err));
   }
+  if (flag & 4) return fail(QQA_ERR_COMM, "fused exchange: a peer rank never arrived at a step barrier");
   if (flag & 1) return fail(QQA_ERR_NONFINITE, "a non-finite theta appeared during the run");
   return QQA_OK;
 }
@@ -1548,10 +1652,18 @@ int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2) {
   if (st) return st;
   const size_t n = (size_t)h->s.n * (h->s.kary ? h->s.K : 1);   // statistics entries
   if (c && n) QQA_CUDA(cudaMemcpyAsync(c, h->c[h->cur], n * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  const long long* sums = h->sums[h->scur];
+  if (h->xmode && n && (sumD || sumD2)) {   // owner rows hold the totals: gather them into the scratch
+    const qqa::XParams X = make_xparams(h, h->scur, h->scur, h->scur, h->cur, h->cur);
+    qqa::k_x_gather<<<std::max(1, std::min((int)((n + 255) / 256), h->sm_count * 8)), 256, 0, h->stream>>>(
+        X, (int)n, h->ws_sums[0]);
+    QQA_CUDA(cudaGetLastError());
+    sums = h->ws_sums[0];
+  }
   if (sumD && n)
-    QQA_CUDA(cudaMemcpyAsync(sumD, h->sums[h->scur], n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    QQA_CUDA(cudaMemcpyAsync(sumD, sums, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   if (sumD2 && n)
-    QQA_CUDA(cudaMemcpyAsync(sumD2, h->sums[h->scur] + n, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    QQA_CUDA(cudaMemcpyAsync(sumD2, sums + n, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   QQA_CUDA(cudaStreamSynchronize(h->stream));
   return QQA_OK;
 }
@@ -1615,9 +1727,55 @@ int qqa_launch_count(qqa_handle* h, int64_t* launches) {
   return QQA_OK;
 }
 
+int qqa_exchange_bytes(qqa_handle* h, size_t* bytes) {
+  if (!h || !bytes) return fail(QQA_ERR_INVALID_ARG, "handle or bytes is NULL");
+  *bytes = 6 * (size_t)h->s.n * sizeof(long long) + 256;   // sums [3][2][n], arrival counter, ticket
+  return QQA_OK;
+}
+
+int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks) {
+  if (!h || !peer_bufs) return fail(QQA_ERR_INVALID_ARG, "handle or peer_bufs is NULL");
+  if (nranks < 1 || nranks > qqa::kMaxRanks || rank < 0 || rank >= nranks)
+    return fail(QQA_ERR_INVALID_ARG, "need 1 <= nranks <= 8 and 0 <= rank < nranks");
+  if (h->s.kary || step_mode(h->cfg, h->s.weighted) > 3)
+    return fail(QQA_ERR_UNSUPPORTED, "the fused exchange supports the binary problems without edge weights or the printed clique");
+  if ((int64_t)h->s.S_local * nranks != h->s.S_total || h->cfg.replica_offset != rank * h->s.S_local)
+    return fail(QQA_ERR_INVALID_ARG, "sharding must be S_total = nranks * S_local and replica_offset = rank * S_local");
+  if (h->comm && (h->rank != rank || h->nranks != nranks))
+    return fail(QQA_ERR_INVALID_ARG, "rank / nranks differ from the attached communicator");
+  if (!pick_xstep(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted)))
+    return fail(QQA_ERR_UNSUPPORTED, "no fused-exchange kernel for this replica layout");
+  int st = set_device(h);
+  if (st) return st;
+  const size_t n2 = 2 * (size_t)h->s.n;
+  for (int r = 0; r < nranks; ++r) {
+    if (!peer_bufs[r] || peer_bufs[r] % 256) return fail(QQA_ERR_INVALID_ARG, "peer buffer NULL or not 256-byte aligned");
+    long long* base = reinterpret_cast<long long*>(peer_bufs[r]);
+    for (int k = 0; k < 3; ++k) h->xsums[r][k] = base + k * n2;
+    h->xflag[r] = reinterpret_cast<unsigned long long*>(base + 3 * n2);
+  }
+  if (!h->xmode)
+    for (int k = 0; k < 3; ++k) h->ws_sums[k] = h->sums[k];
+  h->xticket = reinterpret_cast<unsigned int*>(h->xflag[rank] + 1);
+  QQA_CUDA(cudaMemsetAsync(h->xsums[rank][0], 0, 3 * n2 * sizeof(long long) + 256, h->stream));
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  for (int k = 0; k < 3; ++k) h->sums[k] = h->xsums[rank][k];
+  h->xmode = true;
+  h->xrank = rank;
+  h->xG = nranks;
+  h->xsync = 0;
+  h->comm_chunks = 1;
+  h->step = 0;
+  // re-initialise into the exchange buffers; with a communicator the all-reduced totals end with the
+  // first barrier arrival, without one (emulated shards) qqa_loopback_sync_init completes them
+  if ((st = launch_init(h, false, nullptr))) return st;
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  return QQA_OK;
+}
+
 int qqa_step_path(qqa_handle* h, int* path) {
   if (!h || !path) return fail(QQA_ERR_INVALID_ARG, "handle or path is NULL");
-  *path = h->s.kary ? QQA_PATH_KARY : use_cluster(h, 2) ? QQA_PATH_CLUSTER
+  *path = h->s.kary ? QQA_PATH_KARY : h->xmode ? QQA_PATH_EXCHANGE : use_cluster(h, 2) ? QQA_PATH_CLUSTER
                                     : use_persistent(h, 2) ? QQA_PATH_PERSISTENT : QQA_PATH_STEP;
   return QQA_OK;
 }

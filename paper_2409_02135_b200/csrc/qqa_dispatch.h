@@ -7,6 +7,7 @@
 namespace qqa {
 using StepKernel = void (*)(const StepParams);
 using RunKernel = void (*)(const RunParams);
+using XStepKernel = void (*)(const StepParams, const XParams);
 using StepKKernel = void (*)(const StepKParams);
 using InitKKernel = void (*)(const InitKParams);
 using PackKKernel = void (*)(const float*, uint8_t*, int, int, int);
@@ -37,6 +38,12 @@ RunKernel run_kernel_m8(int lanes, int vpl, int cta);
 RunKernel run_kernel_m9(int lanes, int vpl, int cta);
 RunKernel run_kernel_m10(int lanes, int vpl, int cta);
 RunKernel run_kernel_m11(int lanes, int vpl, int cta);
+
+// k_step_x<lanes, vpl, MODE> (fused statistics exchange), MODE 0..3; nullptr otherwise.
+XStepKernel xstep_kernel_m0(int lanes, int vpl);
+XStepKernel xstep_kernel_m1(int lanes, int vpl);
+XStepKernel xstep_kernel_m2(int lanes, int vpl);
+XStepKernel xstep_kernel_m3(int lanes, int vpl);
 
 // k_run_cluster<MODE> (MODE 0..3, compiled in k_cluster.cu); nullptr otherwise.
 RunKernel cluster_kernel(int mode);

@@ -409,7 +409,7 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
 // One work item (replica block b, variable i) of the step: gather, update, statistics.
 template <int LANES, int VPL, int MODE>
 __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
-                                          unsigned gmask, float mu, float sd, bool& bad) {
+                                          unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false) {
       const int SB8 = P.SB >> 3;
       const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
       const float* __restrict__ pc = V.p_cur + blk;
@@ -544,7 +544,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         st8_stream(P.v + at, vv);
         st8_pnext(V.p_next + at, pn);
       }
-      publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, V.sums_next, V.sums_zero);
+      publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, force_atomic ? 2 : P.B, V.sums_next, V.sums_zero);
 }
 
 template <int LANES, int VPL, int MODE>
@@ -561,6 +561,101 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
     }
   if (bad) atomicOr(P.flag, 1);
 }
+
+// ---------------------------------------------- fused statistics exchange (G GPUs, no NCCL per step)
+// Each rank owns a contiguous range of rows of the int64 statistic sums. In the step epilogue every
+// rank adds its replicas' fixed-point terms of row i straight into row i of the OWNER's buffer (peer
+// memory over NVLink, `atomicAdd` performed at the owner), so the exchange overlaps the step tile by
+// tile; the next step reads row i's total from the owner (one 16-byte peer load per row) and finalizes
+// (mu_i, STD_i) in registers. Step boundaries are a flag barrier in peer memory: the last CTA of a
+// rank's step kernel (ticket counter) releases +1 into every rank's arrival counter, and a step
+// kernel starts once its own counter reaches G x (barriers so far). The sums are exact integers, so
+// the result is bit-identical to the NCCL all-reduce path and to one GPU.
+constexpr int kMaxRanks = 8;
+struct XParams {
+  long long* peer_cur[kMaxRanks];       // every rank's sums buffer of this step (owner rows hold totals)
+  long long* peer_next[kMaxRanks];      // every rank's sums buffer of the next step (zeroed owner rows)
+  long long* zero;                      // this rank's buffer two steps ahead (owned rows zeroed here)
+  unsigned long long* flag;             // this rank's arrival counter
+  unsigned long long* peer_flag[kMaxRanks];
+  unsigned int* ticket;                 // this rank's CTA ticket (0 between launches)
+  const float* c_cur;                   // shift of the current sums (every rank keeps all rows)
+  float* c_next;
+  unsigned long long expect;            // arrivals to wait for = G x barriers before this step
+  int rank, G, rows_per_rank;
+};
+
+__device__ __forceinline__ void x_wait(const XParams& X, int* err) {
+  if (threadIdx.x == 0) {
+    long long spins = 0;
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(X.flag) : "memory");
+      if (v >= X.expect) break;
+      __nanosleep(128);
+      if (++spins > (1ll << 25)) { atomicOr(err, 4); break; }   // a peer never arrived: report, do not hang
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void x_arrive_all(const XParams& X) {
+  __threadfence_system();
+  for (int r = 0; r < X.G; ++r)
+    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(X.peer_flag[r]) : "memory");
+}
+
+// The last CTA of the launch (ticket) releases this rank's arrival into every rank's counter.
+__device__ __forceinline__ void x_signal(const XParams& X) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();   // this CTA's peer additions, ordered before the ticket
+    const unsigned t = atomicAdd(X.ticket, 1u);
+    if (t == gridDim.x - 1) {
+      *X.ticket = 0;
+      x_arrive_all(X);
+    }
+  }
+}
+
+template <int LANES, int VPL, int MODE>
+__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
+  const int lane = threadIdx.x & (LANES - 1);
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  x_wait(X, P.flag);
+  bool bad = false;
+  for (int b = 0; b < P.B; ++b)
+    for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
+      const int own = min(i / X.rows_per_rank, X.G - 1);
+      const long long* sc = X.peer_cur[own];
+      float mu, sd;
+      finalize_stats(X.c_cur[i], sc[i], sc[P.n + i], P.S_total, mu, sd);   // the k_finalize arithmetic
+      if (b == 0 && lane == 0) X.c_next[i] = mu;
+      StepVar V = P.var;
+      V.sums_next = X.peer_next[own];
+      V.sums_zero = (own == X.rank) ? X.zero : nullptr;
+      step_item<LANES, VPL, MODE>(P, V, b, i, lane, gmask, mu, sd, bad, true);
+    }
+  if (bad) atomicOr(P.flag, 1);
+  x_signal(X);
+}
+
+#ifndef QQA_INST_ONLY
+// One barrier arrival of this rank (after the initial statistics, outside a step kernel).
+__global__ void k_x_arrive(const XParams X) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) x_arrive_all(X);
+}
+// Owner rows of the current sums -> a local [2][n] copy (qqa_get_stats).
+__global__ void k_x_gather(const XParams X, int n, long long* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const long long* sc = X.peer_cur[min(i / X.rows_per_rank, X.G - 1)];
+    out[i] = sc[i];
+    out[n + i] = sc[n + i];
+  }
+}
+#endif
 
 // Persistent form for small / L2-resident problems (one replica block, one GPU): ONE
 // cooperative launch runs nsteps annealing steps with a grid barrier between them. A

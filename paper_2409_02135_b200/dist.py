@@ -36,6 +36,27 @@ def attach(solver, rank: int, world: int, group=None) -> None:
     solver.attach_comm(uid, rank, world)
 
 
+def attach_exchange(solver, rank: int, world: int, group=None):
+    """Collective: the fused statistics exchange over peer memory. Every rank's
+    exchange buffer comes from torch symmetric memory, whose rendezvous maps all of them into every
+    process; the library gets the peer pointers. Call after ``attach`` (the communicator stays in use
+    for init and evaluation). Returns the peer pointers (the buffer is kept alive by ``solver``; another
+    handle of the same shape may re-attach to them once ``solver`` is idle)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+
+    nbytes = solver.exchange_bytes()
+    buf = symm.empty(nbytes, dtype=torch.uint8, device=solver.device)
+    grp = group if group is not None else dist.group.WORLD
+    hdl = symm.rendezvous(buf, grp.group_name)
+    ptrs = list(hdl.buffer_ptrs)
+    if len(ptrs) != world or ptrs[rank] != buf.data_ptr():
+        raise RuntimeError("symmetric-memory rendezvous returned an unexpected peer map")
+    solver.attach_exchange(ptrs, rank, world, keep=(buf, hdl))
+    return ptrs
+
+
 def max_over_ranks(x: float, device=None, group=None) -> float:
     import torch
     import torch.distributed as dist

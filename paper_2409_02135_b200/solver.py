@@ -189,6 +189,19 @@ class Solver:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         check(lib.qqa_attach_comm(self._h, buf, rank, nranks))
 
+    def exchange_bytes(self) -> int:
+        """Bytes of this rank's fused-exchange buffer (qqa_exchange_bytes)."""
+        out = ctypes.c_size_t(0)
+        check(lib.qqa_exchange_bytes(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    def attach_exchange(self, peer_ptrs, rank: int, nranks: int, keep=None):
+        """Fused statistics exchange over peer memory (qqa_attach_exchange): peer_ptrs[r] = rank r's
+        exchange buffer (device pointer mapped in this process). ``keep`` holds the buffers alive."""
+        arr = (ctypes.c_uint64 * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+        check(lib.qqa_attach_exchange(self._h, arr, rank, nranks))
+        self._exchange_keep = keep
+
     def share_comm(self, donor: "Solver"):
         """Join donor's communicator (no new NCCL bootstrap); collective over its ranks."""
         check(lib.qqa_share_comm(self._h, donor._h))
@@ -208,10 +221,11 @@ class Solver:
         check(lib.qqa_launch_count(self._h, ctypes.byref(k)))
         return int(k.value)
 
-    STEP_PATHS = ("step", "persistent", "kary", "cluster")
+    STEP_PATHS = ("step", "persistent", "kary", "cluster", "exchange")
 
     def step_path(self) -> str:
-        """The step kernel a run of >= 2 steps uses: 'step', 'persistent', 'cluster' or 'kary' (qqa_step_path)."""
+        """The step kernel a run of >= 2 steps uses: 'step', 'persistent', 'cluster', 'exchange' or 'kary'
+        (qqa_step_path)."""
         k = ctypes.c_int(0)
         check(lib.qqa_step_path(self._h, ctypes.byref(k)))
         return self.STEP_PATHS[k.value]
