@@ -291,9 +291,7 @@ def main():
             except Exception as e:   # no symmetric memory / peer mapping here: stay on NCCL
                 print(f"fused exchange unavailable: {e!r}", file=sys.stderr)
                 ok_attach = 0
-            t_ok = torch.tensor([ok_attach], dtype=torch.int32, device=dev)
-            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
-            if int(t_ok.item()) == 0:
+            if not qdist.all_ranks(ok_attach == 1, device=dev):
                 if xptrs is not None:   # this rank attached, another did not: back to a plain NCCL handle
                     sol.close()
                     sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
@@ -310,9 +308,7 @@ def main():
             a, b = sol.get_state(), ref.get_state()
             ok = all(np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)) for k in ("theta", "m", "v", "p"))
             ok = ok and np.array_equal(sol.get_stats()["sumD2"], ref.get_stats()["sumD2"])
-            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if int(flag.item()) == 1:   # both exact: keep the faster one (max over ranks, 5 steps each)
+            if qdist.all_ranks(ok, device=dev):   # both exact: keep the faster one (max over ranks, 5 steps each)
                 def probe(s):
                     s.reset()
                     barrier()
@@ -323,7 +319,7 @@ def main():
                     barrier()
                     return max_over_ranks(a0.elapsed_time(a1)) / 5
                 exchange_probe = {"fused_ms_per_step": probe(sol), "nccl_ms_per_step": probe(ref)}
-                if exchange_probe["nccl_ms_per_step"] < exchange_probe["fused_ms_per_step"]:
+                if qdist.pick_exchange(exchange_probe["fused_ms_per_step"], exchange_probe["nccl_ms_per_step"]) == "nccl":
                     sol.close()
                     sol, xptrs = ref, None
                     exchange = "nccl all-reduce (4-chunk overlap; faster than the fused exchange here)"

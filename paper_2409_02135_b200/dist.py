@@ -57,6 +57,25 @@ def attach_exchange(solver, rank: int, world: int, group=None):
     return ptrs
 
 
+def all_ranks(flag: bool, device=None, group=None) -> bool:
+    """True iff ``flag`` holds on every rank (MIN all-reduce): how the ranks agree on using the fused
+    exchange (every rank attached it, and its self-check was bit-exact everywhere)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return bool(flag)
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(int(t.item()))
+
+
+def pick_exchange(fused_ms: float, nccl_ms: float) -> str:
+    """'fused' unless the NCCL path was faster; both times are already maxima over ranks, so every rank
+    picks the same."""
+    return "nccl" if nccl_ms < fused_ms else "fused"
+
+
 def max_over_ranks(x: float, device=None, group=None) -> float:
     import torch
     import torch.distributed as dist

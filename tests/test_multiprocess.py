@@ -58,6 +58,13 @@ def _worker(rank, world, port, out_dir):
         assert uid == bytes(range(128))
         # max over ranks
         assert qdist.max_over_ranks(float(rank + 1)) == float(world)
+        # exchange choice of bench.py at N > 1: every rank must agree
+        assert qdist.all_ranks(True) is True
+        assert qdist.all_ranks(rank == 0) is False          # one rank's failed attach / self-check
+        fused_ms = qdist.max_over_ranks(1.0 + rank)           # the probe times are maxima over ranks
+        nccl_ms = qdist.max_over_ranks(1.5)
+        assert qdist.pick_exchange(fused_ms, nccl_ms) == "nccl"
+        assert qdist.pick_exchange(1.0, 1.5) == "fused"
         # shards tile [0, S)
         cover = torch.zeros(S, dtype=torch.int64)
         cover[off:off + S_l] = 1
