@@ -395,15 +395,15 @@ def test_persistent_cta_layouts_identical(Q, monkeypatch, cta):
         assert np.array_equal(a.get_state()[k], b.get_state()[k]), k
 
 
-@pytest.mark.parametrize("name,path,SB", [("c1", "cluster", 16), ("c3", "persistent", 256), ("c4", "persistent", 512),
+@pytest.mark.parametrize("name,path,SB", [("c1", "cluster", 16), ("c2", "persistent", 104), ("t1", "persistent", 104), ("c3", "persistent", 256), ("c4", "persistent", 512),
                                           ("c5", "step", 32), ("q13", "kary", 0)])
 def test_step_path_and_replica_block(Q, name, path, SB):
     """Kernel selection of bench.py's workloads: c5's p (256 MB) exceeds the 128 MB
     block budget, so its 64 replicas run as two blocks of 32 (measured faster than unblocked)."""
     w = gen.workload(name)
-    g = w.graphs[0]
+    (g, gor) = w.batched()                      # bench.py's handle: the batch of a multi-instance workload
     hp = {k: v for k, v in w.hparams().items() if k != "problem"}
-    sol = Q.Solver(g.rowptr, g.colidx, Q.make_config(w.problem, S_total=w.S, seed=w.seeds[0], **hp))
+    sol = Q.Solver(g.rowptr, g.colidx, Q.make_config(w.problem, S_total=w.S, seed=w.seeds[0], **hp), group_of_row=gor)
     assert sol.step_path() == path and sol.replica_block() == SB
 
 
