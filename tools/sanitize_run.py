@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
 """Small run through every kernel path of libqqa.so, for compute-sanitizer:
-create (validate, pad), init, launch-per-step and persistent steps, blocked layout, clamp / noise,
-batches, weights, K-ary colouring, the printed clique relaxation, loopback shards, checkpoint /
-resume and every evaluation kernel."""
+create (validate, pad), init, launch-per-step, persistent and one-cluster steps, blocked layout, clamp /
+noise, batches, weights, K-ary colouring, the printed clique relaxation, loopback shards (NCCL-style and
+fused exchange), checkpoint / resume and every evaluation kernel."""
 import os
 import sys
 
@@ -59,6 +59,18 @@ def main():
     Q.loopback_sync_init(shards)
     Q.loopback_run(shards, gam[:10])
     for s in shards:
+        s.round_evaluate()
+    # fused statistics exchange (k_step_x) on emulated shards, each with its own exchange buffer
+    import torch
+    shards = [Q.Solver(g.rowptr, g.colidx, Q.make_config("maxcut", S_total=24, seed=9, replica_offset=r * 8, S_local=8,
+                                                         temperature=0.001)) for r in range(3)]
+    bufs = [torch.empty(sh.exchange_bytes(), dtype=torch.uint8, device=sh.device) for sh in shards]
+    for r, sh in enumerate(shards):
+        sh.attach_exchange([b.data_ptr() for b in bufs], r, 3, keep=bufs)
+    Q.loopback_sync_init(shards)
+    Q.loopback_run(shards, gam[:10])
+    for s in shards:
+        s.get_stats()
         s.round_evaluate()
     print("sanitize_run ok")
 
