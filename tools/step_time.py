@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Per-step kernel time of one workload (A/B helper): python tools/step_time.py c5 [steps]
-Environment variables (QQA_TMA, QQA_TMA_SB, QQA_BLOCK_REPLICAS, ...) select the variant."""
+Environment variables (QQA_BLOCK_REPLICAS, QQA_PERSISTENT, QQA_CLUSTER, QQA_LIB_PATH, ...) select the variant."""
 import os
 import sys
 
