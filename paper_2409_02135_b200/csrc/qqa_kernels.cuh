@@ -409,7 +409,8 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
 // One work item (replica block b, variable i) of the step: gather, update, statistics.
 template <int LANES, int VPL, int MODE>
 __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
-                                          unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false) {
+                                          unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false,
+                                          long long* sums_dst = nullptr, long long* zero_dst = nullptr) {
       const int SB8 = P.SB >> 3;
       const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
       const float* __restrict__ pc = V.p_cur + blk;
@@ -544,7 +545,10 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         st8_stream(P.v + at, vv);
         st8_pnext(V.p_next + at, pn);
       }
-      publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, force_atomic ? 2 : P.B, V.sums_next, V.sums_zero);
+      if (force_atomic)   // fused exchange: the owner's buffers (atomics across ranks and blocks)
+        publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, 2, sums_dst, zero_dst);
+      else
+        publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, V.sums_next, V.sums_zero);
 }
 
 template <int LANES, int VPL, int MODE>
@@ -633,10 +637,8 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
       float mu, sd;
       finalize_stats(X.c_cur[i], sc[i], sc[P.n + i], P.S_total, mu, sd);   // the k_finalize arithmetic
       if (b == 0 && lane == 0) X.c_next[i] = mu;
-      StepVar V = P.var;
-      V.sums_next = X.peer_next[own];
-      V.sums_zero = (own == X.rank) ? X.zero : nullptr;
-      step_item<LANES, VPL, MODE>(P, V, b, i, lane, gmask, mu, sd, bad, true);
+      step_item<LANES, VPL, MODE>(P, P.var, b, i, lane, gmask, mu, sd, bad, true, X.peer_next[own],
+                                  (own == X.rank) ? X.zero : nullptr);
     }
   if (bad) atomicOr(P.flag, 1);
   x_signal(X);
