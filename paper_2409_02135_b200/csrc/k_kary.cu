@@ -16,4 +16,11 @@ bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKerne
 #undef QQA_KCASE
   return false;
 }
+
+StepKKernel kary_quad_kernel(int KP, int mode) {
+  const bool noise = (mode & kModeNoise) != 0;
+  if (KP == 12) return noise ? k_step_Kq<12, kModeNoise> : k_step_Kq<12, 0>;
+  if (KP == 16) return noise ? k_step_Kq<16, kModeNoise> : k_step_Kq<16, 0>;
+  return nullptr;
+}
 }  // namespace qqa

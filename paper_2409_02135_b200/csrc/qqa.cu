@@ -316,6 +316,8 @@ struct qqa_handle {
   unsigned long long xsync = 0;                  // barriers so far (each adds G arrivals to every counter)
   long long* ws_sums[3] = {nullptr, nullptr, nullptr};   // the workspace's own sums (get_stats scratch)
   int cluster_cs = 0;          // k_run_cluster: CTAs per cluster (0: not available for this handle)
+  qqa::StepKKernel kq = nullptr;    // K-ary colour-quad step (KP 12 / 16), nullptr: k_step_K
+  int grid_kq = 0;
   int cluster_rows = 0;        // rows per CTA of the cluster
   size_t cluster_smem = 0;
   int cur = 0;   // p / c buffer of the current step (mod 2)
@@ -603,7 +605,10 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
       h->launches++;
       int st;
       if ((st = record_start(h))) return st;
-      ks<<<h->grid_step, 256, 0, h->stream>>>(P);
+      if (h->kq)
+        h->kq<<<h->grid_kq, 256, 0, h->stream>>>(P);
+      else
+        ks<<<h->grid_step, 256, 0, h->stream>>>(P);
       QQA_CUDA(cudaGetLastError());
       h->launches++;
       if ((st = record_end(h))) return st;
@@ -1144,6 +1149,14 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     if (!pick_kary(s.KP, step_mode(*cfg, s.weighted), ks, ki, kp)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no K-ary kernel"));
     const int64_t chunks = (s.S_local + s.LK - 1) / s.LK;   // work item = (variable, replica chunk)
     if ((st = grid_for((const void*)ks, h->sm_count, (int64_t)s.n * chunks, s.LK, h->grid_step))) return cleanup(st);
+    {  // colour quads for KP 12 / 16 (QQA_KARY_QUAD=0 keeps k_step_K)
+      const char* env = std::getenv("QQA_KARY_QUAD");
+      h->kq = (env && std::atoi(env) == 0) ? nullptr : qqa::kary_quad_kernel(s.KP, step_mode(*cfg, s.weighted));
+      if (h->kq) {
+        const int64_t qitems = (int64_t)s.n * ((s.S_local + qqa::kQuadReps - 1) / qqa::kQuadReps);
+        if ((st = grid_for((const void*)h->kq, h->sm_count, qitems, 32, h->grid_kq))) return cleanup(st);
+      }
+    }
     if ((st = grid_for((const void*)ki, h->sm_count, (int64_t)s.n * s.S_local, 1, h->grid_init))) return cleanup(st);
     const int64_t nk = (int64_t)s.n * s.K;
     h->grid_fin = (int)std::max<int64_t>(1, std::min<int64_t>((nk + 255) / 256, (int64_t)h->sm_count * 8));

@@ -1334,6 +1334,146 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(co
   if (bad) atomicOr(P.flag, 1);
 }
 
+// K-ary step with colour quads (KP = 12 / 16; small graphs with many replicas, e.g. queen13-13 at
+// S = 1000): a thread owns 4 colours (one float4) of one replica, the 4 lanes of a replica hold its
+// colours, a warp covers 8 replicas. Four times the threads of k_step_K per (variable, replica) and a
+// quarter of the registers, so many more gathers are in flight. Same arithmetic: CSR-order float4
+// gather, the per-colour update, the normaliser Z summed in colour order by passing the running sum
+// from lane to lane, per-colour statistics reduced over the warp's 8 replicas (u64 atomics across
+// chunks). Bit-identical to k_step_K.
+constexpr int kQuadReps = 8;   // replicas per warp
+#ifndef QQA_KQ_U
+#define QQA_KQ_U 4               // neighbour rows in flight per lane (measured: 4 at 5 CTAs/SM)
+#endif
+#ifndef QQA_KQ_MINB
+#define QQA_KQ_MINB 5
+#endif
+template <int KP, int MODE>
+__global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams P) {
+  constexpr int U = QQA_KQ_U;                            // neighbour rows in flight per lane
+  constexpr int NQ = KP / 4;                             // quads holding colours (3 or 4)
+  const int lane = threadIdx.x & 31;
+  const int rq = lane >> 2, q = lane & 3;                // replica in the chunk, colour quad
+  const int warps_cta = blockDim.x >> 5;
+  const int nch = (P.S + kQuadReps - 1) / kQuadReps;
+  const long long items = (long long)P.n * nch;
+  bool bad = false;
+  for (long long it = (long long)blockIdx.x * warps_cta + (threadIdx.x >> 5); it < items;
+       it += (long long)gridDim.x * warps_cta) {
+    const int i = (int)(it / nch), ch = (int)(it - (long long)i * nch);
+    const int r = ch * kQuadReps + rq;
+    const bool rep = r < P.S;                            // a live replica (all 4 lanes)
+    const bool live = rep && q < NQ;                     // ... and a quad holding colours
+    const int k0 = 4 * q;
+    float w[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float cl4[4] = {0.0f, 0.0f, 0.0f, 0.0f};             // Clamp(w) of this quad's colours
+    float mm[4], vv2[4];
+    size_t at = 0;
+    if (live) {
+      const int e0 = __ldg(P.rowptr + i), e1 = __ldg(P.rowptr + i + 1);
+      float4 qa = make_float4(0.0f, 0.0f, 0.0f, 0.0f);   // q_k = sum_j p_j[r][k], CSR order
+      const float* base = P.p_cur + (size_t)r * KP + k0;
+      int e = e0;
+      for (; e + U <= e1; e += U) {
+        float4 pj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          pj[u] = __ldg(reinterpret_cast<const float4*>(base + (size_t)__ldg(P.colidx + e + u) * P.S * KP));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float2 lo = __fadd2_rn(make_float2(qa.x, qa.y), make_float2(pj[u].x, pj[u].y));
+          const float2 hi = __fadd2_rn(make_float2(qa.z, qa.w), make_float2(pj[u].z, pj[u].w));
+          qa = make_float4(lo.x, lo.y, hi.x, hi.y);
+        }
+      }
+      for (; e < e1; ++e) {
+        const float4 pj = __ldg(reinterpret_cast<const float4*>(base + (size_t)__ldg(P.colidx + e) * P.S * KP));
+        qa = make_float4(fadd(qa.x, pj.x), fadd(qa.y, pj.y), fadd(qa.z, pj.z), fadd(qa.w, pj.w));
+      }
+      const float qv[4] = {qa.x, qa.y, qa.z, qa.w};
+      const unsigned long long rkey = P.nkey + (unsigned long long)i * (unsigned long long)P.K * P.S_total_u;
+      at = ((size_t)i * P.S + r) * KP + k0;
+      const float4 w4 = *reinterpret_cast<const float4*>(P.p_cur + at);
+      const float4 m4 = *reinterpret_cast<const float4*>(P.m + at);
+      const float4 v4 = *reinterpret_cast<const float4*>(P.v + at);
+      w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+      mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
+      vv2[0] = v4.x; vv2[1] = v4.y; vv2[2] = v4.z; vv2[3] = v4.w;
+      float xi = 0.0f, xi_odd = 0.0f;                    // colours pair up (k even, k + 1) on one noise hash
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int k = k0 + c;
+        if (k >= P.K) continue;
+        if (MODE & kModeNoise) {
+          if ((c & 1) == 0)
+            gauss_pair_c(mix64(rkey + (unsigned long long)k * P.S_total_u + (unsigned long long)r), xi, xi_odd);
+          else
+            xi = xi_odd;
+        }
+        const float pi = w[c];
+        const float2 st = P.ms[(size_t)i * P.K + k];
+        const float e1f = fsub(fmul(P.Kf, pi), 1.0f);
+        float ep = e1f;
+        for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e1f);          // (K p - 1)^(alpha-1)
+        const float ent = fmul(P.kt, ep);
+        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
+        const float g = fadd(fadd(qv[c], ent), com);
+        const float t1 = fmul(pi, P.at);
+        mm[c] = fadd(fmul(P.b1, mm[c]), fmul(P.c1, g));
+        vv2[c] = fadd(fmul(P.b2, vv2[c]), fmul(fmul(P.c2, g), g));
+        const float den = fadd(fmul(__fsqrt_rn(vv2[c]), P.rt), P.eps);
+        float x = fsub(t1, fmul(P.st, fdiv(mm[c], den)));
+        if (MODE & kModeNoise) x = fadd(x, fmul(P.ns, xi));
+        bad |= !isfinite(x);
+        w[c] = x;
+        cl4[c] = clamp01(x);
+      }
+    }
+    // Z = ((c_0 + c_1) + c_2) + ... over the K colours in order: the running sum passes from quad to quad
+    float Z = 0.0f;
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+      if (q == qq)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (k0 + c < P.K) Z = fadd(Z, cl4[c]);
+      Z = __shfl_sync(0xffffffffu, Z, (lane & ~3) + qq);
+    }
+    if (live) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        w[c] = (k0 + c < P.K) ? ((Z > 0.0f) ? fdiv(cl4[c], Z) : P.unif) : 0.0f;
+      *reinterpret_cast<float4*>(P.m + at) = make_float4(mm[0], mm[1], mm[2], mm[3]);
+      *reinterpret_cast<float4*>(P.v + at) = make_float4(vv2[0], vv2[1], vv2[2], vv2[3]);
+      *reinterpret_cast<float4*>(P.p_next + at) = make_float4(w[0], w[1], w[2], w[3]);
+    }
+    // fixed-point statistics per colour: reduce over the warp's replicas (lanes of the same quad)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = k0 + c;
+      long long D = 0, D2 = 0;
+      if (live && k < P.K) stat_terms(w[c], P.ms[(size_t)i * P.K + k].x, D, D2);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        D += __shfl_xor_sync(0xffffffffu, D, off);
+        D2 += __shfl_xor_sync(0xffffffffu, D2, off);
+      }
+      if (rq == 0 && q < NQ && k < P.K) {
+        const size_t ik = (size_t)i * P.K + k, nk = (size_t)P.n * P.K;
+        if (nch == 1) {
+          P.sums_next[ik] = D;
+          P.sums_next[nk + ik] = D2;
+        } else {
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + ik), (unsigned long long)D);
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + nk + ik), (unsigned long long)D2);
+          if (ch == 0) { P.sums_zero[ik] = 0; P.sums_zero[nk + ik] = 0; }
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(P.flag, 1);
+}
+
 // K1 for K-ary: W_0 = 1/K + U(lo, hi) keyed (seed, i K + k, global s), P_0 = normalise(W_0),
 // m = v = 0; or (use_given) P_0 as given. Sums of P_0 with shift c (1/K or c_given), u64 atomics.
 struct InitKParams {

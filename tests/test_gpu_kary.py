@@ -126,3 +126,23 @@ def test_invalid_colouring_configs(Q):
     with pytest.raises(Q.QQAError) as e:
         Q.Solver(U.rowptr, U.colidx, Q.make_config("coloring", S_total=8, n_colors=4), group_of_row=gor)
     assert e.value.status == 6
+
+
+@pytest.mark.parametrize("K,S,T,steps", [(13, 1000, 0.0, 40), (10, 37, 0.002, 60), (16, 8, 0.0, 30), (9, 100, 0.001, 4100)])
+def test_colour_quad_kernel_equals_k_step_K(Q, monkeypatch, K, S, T, steps):
+    """k_step_Kq (4 colours per thread, 8 replicas per warp; KP = 12 / 16) is bit-identical to k_step_K,
+    including noise pairs, ragged replica chunks and a schedule longer than one run() call."""
+    g = gen.queens(7, 7)
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("QQA_KARY_QUAD", flag)
+        sol = Q.Solver(g.rowptr, g.colidx, Q.make_config("coloring", S_total=S, seed=3, n_colors=K, lr=0.01,
+                                                         temperature=T, comm=0.3))
+        sol.run_linear(-2.0, 0.1, steps)
+        out.append((sol.get_state(), sol.get_stats(), sol.round_evaluate()))
+    (a, sa, ra), (b, sb, rb) = out
+    for f in ("theta", "m", "v", "p"):
+        assert np.array_equal(a[f].view(np.uint32), b[f].view(np.uint32)), f
+    for f in ("c", "sumD", "sumD2"):
+        assert np.array_equal(sa[f], sb[f]), f
+    assert ra.best_replica == rb.best_replica
