@@ -5,9 +5,10 @@
 
 namespace qqa {
 template <int M, int CT>
-RunKernel run_for(int lanes, int vpl) {
+RunKernel run_for(int lanes, int vpl, bool full) {
 #define QQA_RCASE(L, V) \
-  if (lanes == L && vpl == V) return k_run<L, V, M, (V == 1 ? CT : 256)>;
+  if (lanes == L && vpl == V) \
+    return full ? k_run<L, V, M, (V == 1 ? CT : 256), true> : k_run<L, V, M, (V == 1 ? CT : 256), false>;
   QQA_RCASE(1, 1) QQA_RCASE(2, 1) QQA_RCASE(4, 1) QQA_RCASE(8, 1) QQA_RCASE(16, 1)
   QQA_RCASE(32, 1) QQA_RCASE(32, 2) QQA_RCASE(32, 4)
 #undef QQA_RCASE
@@ -15,9 +16,9 @@ RunKernel run_for(int lanes, int vpl) {
 }
 
 template <int M>
-StepKernel step_for(int lanes, int vpl) {
+StepKernel step_for(int lanes, int vpl, bool full) {
 #define QQA_SCASE(L, V) \
-  if (lanes == L && vpl == V) return k_step<L, V, M>;
+  if (lanes == L && vpl == V) return full ? k_step<L, V, M, true> : k_step<L, V, M, false>;
   QQA_SCASE(1, 1) QQA_SCASE(2, 1) QQA_SCASE(4, 1) QQA_SCASE(8, 1) QQA_SCASE(16, 1)
   QQA_SCASE(32, 1) QQA_SCASE(32, 2) QQA_SCASE(32, 4)
 #undef QQA_SCASE
@@ -36,8 +37,8 @@ XStepKernel xstep_for(int lanes, int vpl) {
 }
 
 template <int M>
-RunKernel run_kernel_for(int lanes, int vpl, int cta) {
+RunKernel run_kernel_for(int lanes, int vpl, int cta, bool full) {
   if (M & kModeSparseClique) return nullptr;   // its column sums need a pass between steps: no k_run
-  return (cta == 1024 && vpl == 1) ? run_for<M, 1024>(lanes, vpl) : run_for<M, 256>(lanes, vpl);
+  return (cta == 1024 && vpl == 1) ? run_for<M, 1024>(lanes, vpl, full) : run_for<M, 256>(lanes, vpl, full);
 }
 }  // namespace qqa

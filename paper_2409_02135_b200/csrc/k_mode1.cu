@@ -2,7 +2,7 @@
 #include "k_mode.cuh"
 
 namespace qqa {
-StepKernel step_kernel_m1(int lanes, int vpl) { return step_for<1>(lanes, vpl); }
-RunKernel run_kernel_m1(int lanes, int vpl, int cta) { return run_kernel_for<1>(lanes, vpl, cta); }
+StepKernel step_kernel_m1(int lanes, int vpl, bool full) { return step_for<1>(lanes, vpl, full); }
+RunKernel run_kernel_m1(int lanes, int vpl, int cta, bool full) { return run_kernel_for<1>(lanes, vpl, cta, full); }
 XStepKernel xstep_kernel_m1(int lanes, int vpl) { return xstep_for<1>(lanes, vpl); }
 }  // namespace qqa

@@ -2,6 +2,6 @@
 #include "k_mode.cuh"
 
 namespace qqa {
-StepKernel step_kernel_m10(int lanes, int vpl) { return step_for<10>(lanes, vpl); }
-RunKernel run_kernel_m10(int lanes, int vpl, int cta) { return run_kernel_for<10>(lanes, vpl, cta); }
+StepKernel step_kernel_m10(int lanes, int vpl, bool full) { return step_for<10>(lanes, vpl, full); }
+RunKernel run_kernel_m10(int lanes, int vpl, int cta, bool full) { return run_kernel_for<10>(lanes, vpl, cta, full); }
 }  // namespace qqa

@@ -121,6 +121,9 @@ Layout make_layout(const Shape& s) {
 
 int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
 
+// Every lane of a step-kernel group holds a vector of the replica block (k_step / k_run FULL variant).
+bool full_lanes(const Shape& s) { return s.SB / 8 == s.lanes * s.vpl; }
+
 int check_config(const qqa_config* c) {
   if (!c) return fail(QQA_ERR_INVALID_ARG, "config is NULL");
   if (c->problem < 0 || c->problem > 4)
@@ -359,20 +362,20 @@ InitKernel init_for() { return qqa::k_init<L, V>; }
 // run_cta: 1024 (contiguous rows per SM) or 256 threads per CTA of the persistent kernel (VPL 1 only).
 // The k_step / k_run instantiations live in k_mode<mode>.cu (compiled in parallel).
 bool pick_kernels(int lanes, int vpl, int mode, StepKernel& ks, InitKernel& ki, RunKernel* kr = nullptr,
-                  int run_cta = 256) {
+                  int run_cta = 256, bool full = false) {
   switch (mode) {
-    case 0: ks = qqa::step_kernel_m0(lanes, vpl); if (kr) *kr = qqa::run_kernel_m0(lanes, vpl, run_cta); break;
-    case 1: ks = qqa::step_kernel_m1(lanes, vpl); if (kr) *kr = qqa::run_kernel_m1(lanes, vpl, run_cta); break;
-    case 2: ks = qqa::step_kernel_m2(lanes, vpl); if (kr) *kr = qqa::run_kernel_m2(lanes, vpl, run_cta); break;
-    case 3: ks = qqa::step_kernel_m3(lanes, vpl); if (kr) *kr = qqa::run_kernel_m3(lanes, vpl, run_cta); break;
-    case 4: ks = qqa::step_kernel_m4(lanes, vpl); if (kr) *kr = qqa::run_kernel_m4(lanes, vpl, run_cta); break;
-    case 5: ks = qqa::step_kernel_m5(lanes, vpl); if (kr) *kr = qqa::run_kernel_m5(lanes, vpl, run_cta); break;
-    case 6: ks = qqa::step_kernel_m6(lanes, vpl); if (kr) *kr = qqa::run_kernel_m6(lanes, vpl, run_cta); break;
-    case 7: ks = qqa::step_kernel_m7(lanes, vpl); if (kr) *kr = qqa::run_kernel_m7(lanes, vpl, run_cta); break;
-    case 8: ks = qqa::step_kernel_m8(lanes, vpl); if (kr) *kr = qqa::run_kernel_m8(lanes, vpl, run_cta); break;
-    case 9: ks = qqa::step_kernel_m9(lanes, vpl); if (kr) *kr = qqa::run_kernel_m9(lanes, vpl, run_cta); break;
-    case 10: ks = qqa::step_kernel_m10(lanes, vpl); if (kr) *kr = qqa::run_kernel_m10(lanes, vpl, run_cta); break;
-    case 11: ks = qqa::step_kernel_m11(lanes, vpl); if (kr) *kr = qqa::run_kernel_m11(lanes, vpl, run_cta); break;
+    case 0: ks = qqa::step_kernel_m0(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m0(lanes, vpl, run_cta, full); break;
+    case 1: ks = qqa::step_kernel_m1(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m1(lanes, vpl, run_cta, full); break;
+    case 2: ks = qqa::step_kernel_m2(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m2(lanes, vpl, run_cta, full); break;
+    case 3: ks = qqa::step_kernel_m3(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m3(lanes, vpl, run_cta, full); break;
+    case 4: ks = qqa::step_kernel_m4(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m4(lanes, vpl, run_cta, full); break;
+    case 5: ks = qqa::step_kernel_m5(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m5(lanes, vpl, run_cta, full); break;
+    case 6: ks = qqa::step_kernel_m6(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m6(lanes, vpl, run_cta, full); break;
+    case 7: ks = qqa::step_kernel_m7(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m7(lanes, vpl, run_cta, full); break;
+    case 8: ks = qqa::step_kernel_m8(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m8(lanes, vpl, run_cta, full); break;
+    case 9: ks = qqa::step_kernel_m9(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m9(lanes, vpl, run_cta, full); break;
+    case 10: ks = qqa::step_kernel_m10(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m10(lanes, vpl, run_cta, full); break;
+    case 11: ks = qqa::step_kernel_m11(lanes, vpl, full); if (kr) *kr = qqa::run_kernel_m11(lanes, vpl, run_cta, full); break;
     default: ks = nullptr; if (kr) *kr = nullptr; break;
   }
   ki = nullptr;
@@ -638,7 +641,7 @@ int do_steps_persistent(qqa_handle* h, const float* gamma, int64_t n_steps) {
   StepKernel ks;
   InitKernel ki;
   RunKernel kr = nullptr;
-  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), ks, ki, &kr, h->run_cta);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), ks, ki, &kr, h->run_cta, full_lanes(h->s));
   const qqa_config& c = h->cfg;
   qqa::RunParams R{};
   qqa::StepParams& P = R.P;
@@ -843,7 +846,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (use_persistent(h, n_steps)) return do_steps_persistent(h, gamma, n_steps);
   StepKernel ks;
   InitKernel ki;
-  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), ks, ki);
+  pick_kernels(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), ks, ki, nullptr, 256, full_lanes(h->s));
   const qqa_config& c = h->cfg;
   qqa::StepParams P{};
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
@@ -1168,7 +1171,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     // fills every SM with a 1024-thread CTA (measured: profiles/r1_design_iterations.md)
     h->run_cta = (s.vpl == 1 && (int64_t)s.n * s.lanes >= (int64_t)h->sm_count * 1024) ? 1024 : 256;
     if (const char* env = std::getenv("QQA_RUN_CTA")) h->run_cta = (std::atoi(env) == 1024 && s.vpl == 1) ? 1024 : 256;
-    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg, s.weighted), ks, ki, &kr, h->run_cta))
+    if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg, s.weighted), ks, ki, &kr, h->run_cta, full_lanes(s)))
       return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
     if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
     {  // persistent kernel: every CTA must be co-resident (cooperative launch)

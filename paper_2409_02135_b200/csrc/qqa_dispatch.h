@@ -14,30 +14,30 @@ using PackKKernel = void (*)(const float*, uint8_t*, int, int, int);
 
 // k_step<lanes, vpl, MODE> and k_run<lanes, vpl, MODE, cta> (cta 1024 only for vpl 1); nullptr if
 // no kernel exists for (lanes, vpl). MODE bit 2 (printed clique) has no k_run.
-StepKernel step_kernel_m0(int lanes, int vpl);
-StepKernel step_kernel_m1(int lanes, int vpl);
-StepKernel step_kernel_m2(int lanes, int vpl);
-StepKernel step_kernel_m3(int lanes, int vpl);
-StepKernel step_kernel_m4(int lanes, int vpl);
-StepKernel step_kernel_m5(int lanes, int vpl);
-StepKernel step_kernel_m6(int lanes, int vpl);
-StepKernel step_kernel_m7(int lanes, int vpl);
-StepKernel step_kernel_m8(int lanes, int vpl);    // 8-11: weighted graphs (+ clamp / noise)
-StepKernel step_kernel_m9(int lanes, int vpl);
-StepKernel step_kernel_m10(int lanes, int vpl);
-StepKernel step_kernel_m11(int lanes, int vpl);
-RunKernel run_kernel_m0(int lanes, int vpl, int cta);
-RunKernel run_kernel_m1(int lanes, int vpl, int cta);
-RunKernel run_kernel_m2(int lanes, int vpl, int cta);
-RunKernel run_kernel_m3(int lanes, int vpl, int cta);
-RunKernel run_kernel_m4(int lanes, int vpl, int cta);   // nullptr: modes 4-7 run launch-per-step
-RunKernel run_kernel_m5(int lanes, int vpl, int cta);
-RunKernel run_kernel_m6(int lanes, int vpl, int cta);
-RunKernel run_kernel_m7(int lanes, int vpl, int cta);
-RunKernel run_kernel_m8(int lanes, int vpl, int cta);
-RunKernel run_kernel_m9(int lanes, int vpl, int cta);
-RunKernel run_kernel_m10(int lanes, int vpl, int cta);
-RunKernel run_kernel_m11(int lanes, int vpl, int cta);
+StepKernel step_kernel_m0(int lanes, int vpl, bool full);
+StepKernel step_kernel_m1(int lanes, int vpl, bool full);
+StepKernel step_kernel_m2(int lanes, int vpl, bool full);
+StepKernel step_kernel_m3(int lanes, int vpl, bool full);
+StepKernel step_kernel_m4(int lanes, int vpl, bool full);
+StepKernel step_kernel_m5(int lanes, int vpl, bool full);
+StepKernel step_kernel_m6(int lanes, int vpl, bool full);
+StepKernel step_kernel_m7(int lanes, int vpl, bool full);
+StepKernel step_kernel_m8(int lanes, int vpl, bool full);    // 8-11: weighted graphs (+ clamp / noise)
+StepKernel step_kernel_m9(int lanes, int vpl, bool full);
+StepKernel step_kernel_m10(int lanes, int vpl, bool full);
+StepKernel step_kernel_m11(int lanes, int vpl, bool full);
+RunKernel run_kernel_m0(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m1(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m2(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m3(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m4(int lanes, int vpl, int cta, bool full);   // nullptr: modes 4-7 run launch-per-step
+RunKernel run_kernel_m5(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m6(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m7(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m8(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m9(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m10(int lanes, int vpl, int cta, bool full);
+RunKernel run_kernel_m11(int lanes, int vpl, int cta, bool full);
 
 // k_step_x<lanes, vpl, MODE> (fused statistics exchange), MODE 0..3; nullptr otherwise.
 XStepKernel xstep_kernel_m0(int lanes, int vpl);

@@ -31,22 +31,23 @@ def _get(usage, mangled):
 
 
 def test_headline_c5_kernel_fits_four_ctas(usage):
-    """c5 runs k_step<4,1,0> (two replica blocks of 32): 64 registers, at most the 8-byte spill it has
-    around the division slow-path calls (measured: a 16-byte spill cost 6 % on c5)."""
-    reg, stack = _get(usage, "_ZN3qqa6k_stepILi4ELi1ELi0EEEvNS_10StepParamsE")     # k_step<4,1,0>
+    """c5 runs k_step<4,1,0,FULL> (two replica blocks of 32, every lane holds a vector): 64 registers, at
+    most the 8-byte spill it has around the division slow-path calls (a 16-byte spill cost 6 % on c5)."""
+    reg, stack = _get(usage, "_ZN3qqa6k_stepILi4ELi1ELi0ELb1EEEvNS_10StepParamsE")     # k_step<4,1,0,FULL>
     assert reg <= 64 and stack <= 8
 
 
 def test_unblocked_64_replica_kernel_has_no_spills(usage):
-    reg, stack = _get(usage, "_ZN3qqa6k_stepILi8ELi1ELi0EEEvNS_10StepParamsE")     # k_step<8,1,0>
+    reg, stack = _get(usage, "_ZN3qqa6k_stepILi8ELi1ELi0ELb0EEEvNS_10StepParamsE")     # k_step<8,1,0>
     assert reg <= 64 and stack == 0
 
 
 @pytest.mark.parametrize("lanes", [1, 2, 4, 8, 16, 32])
 @pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_step_kernels_keep_64_registers(usage, lanes, mode):
-    reg, stack = _get(usage, f"_ZN3qqa6k_stepILi{lanes}ELi1ELi{mode}EEEvNS_10StepParamsE")
-    assert reg <= 64 and stack <= 64
+    for full in (0, 1):
+        reg, stack = _get(usage, f"_ZN3qqa6k_stepILi{lanes}ELi1ELi{mode}ELb{full}EEEvNS_10StepParamsE")
+        assert reg <= 64 and stack <= 64
 
 
 @pytest.mark.parametrize("kp,cap", [(4, 64), (8, 64), (12, 80), (16, 80)])
