@@ -493,12 +493,12 @@ int x_arrive(qqa_handle* h) {
   return QQA_OK;
 }
 
-qqa::XStepKernel pick_xstep(int lanes, int vpl, int mode) {
+qqa::XStepKernel pick_xstep(int lanes, int vpl, int mode, bool full) {
   switch (mode) {
-    case 0: return qqa::xstep_kernel_m0(lanes, vpl);
-    case 1: return qqa::xstep_kernel_m1(lanes, vpl);
-    case 2: return qqa::xstep_kernel_m2(lanes, vpl);
-    case 3: return qqa::xstep_kernel_m3(lanes, vpl);
+    case 0: return qqa::xstep_kernel_m0(lanes, vpl, full);
+    case 1: return qqa::xstep_kernel_m1(lanes, vpl, full);
+    case 2: return qqa::xstep_kernel_m2(lanes, vpl, full);
+    case 3: return qqa::xstep_kernel_m3(lanes, vpl, full);
     default: return nullptr;
   }
 }
@@ -794,7 +794,7 @@ int do_steps_cluster(qqa_handle* h, const float* gamma, int64_t n_steps) {
 // finalizes from the owners' sums, adds into the owners' next sums and arrives); no NCCL, no k_finalize.
 int do_steps_x(qqa_handle* h, const float* gamma, int64_t n_steps) {
   const qqa_config& c = h->cfg;
-  const qqa::XStepKernel kx = pick_xstep(h->s.lanes, h->s.vpl, step_mode(c, h->s.weighted));
+  const qqa::XStepKernel kx = pick_xstep(h->s.lanes, h->s.vpl, step_mode(c, h->s.weighted), full_lanes(h->s));
   if (!kx) return fail(QQA_ERR_UNSUPPORTED, "no fused-exchange kernel for this mode");
   qqa::StepParams P{};
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
@@ -1759,7 +1759,7 @@ int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int 
     return fail(QQA_ERR_INVALID_ARG, "sharding must be S_total = nranks * S_local and replica_offset = rank * S_local");
   if (h->comm && (h->rank != rank || h->nranks != nranks))
     return fail(QQA_ERR_INVALID_ARG, "rank / nranks differ from the attached communicator");
-  if (!pick_xstep(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted)))
+  if (!pick_xstep(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), full_lanes(h->s)))
     return fail(QQA_ERR_UNSUPPORTED, "no fused-exchange kernel for this replica layout");
   int st = set_device(h);
   if (st) return st;

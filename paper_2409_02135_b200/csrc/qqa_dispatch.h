@@ -40,10 +40,10 @@ RunKernel run_kernel_m10(int lanes, int vpl, int cta, bool full);
 RunKernel run_kernel_m11(int lanes, int vpl, int cta, bool full);
 
 // k_step_x<lanes, vpl, MODE> (fused statistics exchange), MODE 0..3; nullptr otherwise.
-XStepKernel xstep_kernel_m0(int lanes, int vpl);
-XStepKernel xstep_kernel_m1(int lanes, int vpl);
-XStepKernel xstep_kernel_m2(int lanes, int vpl);
-XStepKernel xstep_kernel_m3(int lanes, int vpl);
+XStepKernel xstep_kernel_m0(int lanes, int vpl, bool full);
+XStepKernel xstep_kernel_m1(int lanes, int vpl, bool full);
+XStepKernel xstep_kernel_m2(int lanes, int vpl, bool full);
+XStepKernel xstep_kernel_m3(int lanes, int vpl, bool full);
 
 // k_run_cluster<MODE> (MODE 0..3, compiled in k_cluster.cu); nullptr otherwise.
 RunKernel cluster_kernel(int mode);

@@ -624,7 +624,7 @@ __device__ __forceinline__ void x_signal(const XParams& X) {
   }
 }
 
-template <int LANES, int VPL, int MODE>
+template <int LANES, int VPL, int MODE, bool FULL>
 __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
   const int lane = threadIdx.x & (LANES - 1);
   const unsigned gmask = group_mask<LANES>();
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
       float mu, sd;
       finalize_stats(X.c_cur[i], sc[i], sc[P.n + i], P.S_total, mu, sd);   // the k_finalize arithmetic
       if (b == 0 && lane == 0) X.c_next[i] = mu;
-      step_item<LANES, VPL, MODE>(P, P.var, b, i, lane, gmask, mu, sd, bad, true, X.peer_next[own],
+      step_item<LANES, VPL, MODE, FULL>(P, P.var, b, i, lane, gmask, mu, sd, bad, true, X.peer_next[own],
                                   (own == X.rank) ? X.zero : nullptr);
     }
   if (bad) atomicOr(P.flag, 1);
