@@ -47,9 +47,17 @@ def attach_exchange(solver, rank: int, world: int, group=None):
     import torch.distributed._symmetric_memory as symm
 
     nbytes = solver.exchange_bytes()
-    buf = symm.empty(nbytes, dtype=torch.uint8, device=solver.device)
     grp = group if group is not None else dist.group.WORLD
-    hdl = symm.rendezvous(buf, grp.group_name)
+    try:
+        buf = symm.empty(nbytes, dtype=torch.uint8, device=solver.device)
+        ok = True
+    except Exception:
+        buf, ok = None, False
+    # agree before the (collective) rendezvous: a rank that could not allocate must not leave the
+    # others waiting in it
+    if not all_ranks(ok, device=solver.device, group=group):
+        raise RuntimeError("symmetric memory unavailable on at least one rank")
+    hdl = symm.rendezvous(buf, grp)
     ptrs = list(hdl.buffer_ptrs)
     if len(ptrs) != world or ptrs[rank] != buf.data_ptr():
         raise RuntimeError("symmetric-memory rendezvous returned an unexpected peer map")
