@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define QQA_ABI_VERSION 5
+#define QQA_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define QQA_API __attribute__((visibility("default")))
@@ -86,7 +86,8 @@ typedef enum {
                          for the complement as QQA_MAXCLIQUE does. No batches.                 */
   QQA_COLORING = 3    /* graph colouring with K = n_colors colours (NEXT-4, App. B):
                          every variable is a row of K probabilities, s_K entropy, map
-                         Clamp-then-normalise, AdamW on the probabilities,
+                         Clamp-then-normalise, AdamW on the probabilities with the
+                         gradient through the map (kary_grad),
                          x = argmax_k, energy = #{(i<j) in E : x_i = x_j}. The
                          map field is ignored; state arrays are [n][S_local][K]; no batches */
 } qqa_problem;
@@ -109,6 +110,10 @@ typedef struct {
                              counter-based Box-Muller draw keyed (seed, Adam step, variable,
                              global replica): identical for every sharding               */
   int32_t n_colors;       /* K, 2..16, for QQA_COLORING (ignored otherwise)                 */
+  int32_t kary_grad;      /* QQA_COLORING: 1 = the gradient through the Clamp-normalise map,
+                             g_k - sum_k' g_k' p_k' (reading R33: the chain rule at W = P, which
+                             reproduces Table 4 on the small queens graphs); 0 = dR/dP itself
+                             (reading R29). Ignored for the binary problems              */
 } qqa_config;
 
 /* Undirected simple graph as symmetric CSR, host memory, copied at create.

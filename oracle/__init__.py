@@ -46,7 +46,7 @@ class OcCfg(ctypes.Structure):
                 ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("init_lo", ctypes.c_float), ("init_hi", ctypes.c_float),
                 ("seed", ctypes.c_uint64), ("S", ctypes.c_int32), ("threads", ctypes.c_int32),
-                ("map", ctypes.c_int32), ("temperature", ctypes.c_float)]
+                ("map", ctypes.c_int32), ("temperature", ctypes.c_float), ("kary_grad", ctypes.c_int32)]
 
 
 MAP_SIGMOID, MAP_CLAMP = 0, 1
@@ -123,11 +123,12 @@ def _L():
 
 def make_cfg(problem="mis", S=16, seed=1, threads=1, alpha=2, penalty=2.0, comm=0.1, lr=1.0,
              beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, init_lo=-0.01, init_hi=0.01,
-             map="sigmoid", temperature=0.0) -> OcCfg:
+             map="sigmoid", temperature=0.0, kary_grad=1) -> OcCfg:
     pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
     mid = MAPS[map] if isinstance(map, str) else int(map)
     return OcCfg(pid, int(alpha), penalty, comm, lr, beta1, beta2, eps, weight_decay,
-                 init_lo, init_hi, seed & 0xFFFFFFFFFFFFFFFF, int(S), int(threads), mid, float(temperature))
+                 init_lo, init_hi, seed & 0xFFFFFFFFFFFFFFFF, int(S), int(threads), mid, float(temperature),
+                 int(kary_grad))
 
 
 def threshold(map="sigmoid") -> float:

@@ -67,6 +67,7 @@ typedef struct {
     int32_t threads;     /* OpenMP threads for the row loop (<=1: serial) */
     int32_t map;         /* 0 sigmoid (theta is the parameter), 1 clamp (p is the parameter) */
     float temperature;   /* Langevin T; 0 = no noise */
+    int32_t kary_grad;   /* K-ary: 1 = gradient through the map, g - <g, p> (reading R33); 0 = dR/dP (R29) */
 } oc_cfg;
 
 enum { OC_MAP_SIGMOID = 0, OC_MAP_CLAMP = 1 };
@@ -653,14 +654,23 @@ static int update_row_K(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, 
             for (int32_t k = 0; k < K; ++k) q[k] = q[k] + pj[k];
         }
         const size_t at_s = (size_t)s * K;        /* offset of (s, 0) inside row i */
-        for (int32_t k = 0; k < K; ++k) {
+        for (int32_t k = 0; k < K; ++k) {         /* g_k = dR/dp_k, into q[k] */
             const float pi = pp[at_s + k];
             const float e = Kf * pi - 1.0f;
             float ep = e;
             for (int32_t a = 2; a < cf->alpha; ++a) ep = ep * e;       /* (K p - 1)^(alpha-1) */
             const float ent = kt * ep;
             const float com = (sd[k] >= 1e-6f) ? (-ac) * ((pi - mu[k]) / sd[k]) : 0.0f;
-            const float g = (q[k] + ent) + com;
+            q[k] = (q[k] + ent) + com;
+        }
+        if (cf->kary_grad) {                      /* through the map: g - <g, p>, <g, p> in colour order */
+            float gb = 0.0f;
+            for (int32_t k = 0; k < K; ++k) gb = gb + q[k] * pp[at_s + k];
+            for (int32_t k = 0; k < K; ++k) q[k] = q[k] - gb;
+        }
+        for (int32_t k = 0; k < K; ++k) {
+            const float pi = pp[at_s + k];
+            const float g = q[k];
             float t1 = pi * at;
             const float m1 = b1 * mm[at_s + k] + c1 * g;
             const float v1 = b2 * vv[at_s + k] + (c2 * g) * g;

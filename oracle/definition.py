@@ -397,6 +397,14 @@ def grad_K(A, P, gamma, alpha, comm) -> np.ndarray:
     return obj + gamma * ent + com
 
 
+def grad_K_map(A, P, gamma, alpha, comm) -> np.ndarray:
+    """The K-ary gradient through the map (reading R33): with W = P on the simplex (the sensitive
+    transition replaces W by sigma(W) every step), d sigma_k' / d W_k = delta_kk' - P_k' inside the clamp
+    range, so dR/dW = g - <g, P> per (variable, replica) row, g = dR/dP (grad_K)."""
+    g = grad_K(A, P, gamma, alpha, comm)
+    return g - (g * P).sum(axis=2, keepdims=True)
+
+
 def clamp_normalize(W: np.ndarray) -> np.ndarray:
     """sigma(W_ik) = Clamp(W_ik) / sum_k' Clamp(W_ik'); a row whose clamps are all 0 maps
     to the uniform 1/K (reading R27: the paper leaves 0/0 undefined)."""
@@ -434,16 +442,18 @@ def gauss_noise_K(seed: int, t: int, n: int, S_total: int, K: int) -> np.ndarray
 
 
 def run_K(A, P0, gammas, alpha=2, comm=0.1, lr=1.0, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.01,
-          m0=None, v0=None, t0=0, temperature=0.0, seed=0):
-    """K-ary PQQA, fp64: AdamW on P with dR/dP, (+ noise), then P <- clamp_normalize(P') (Eq. 11 with
-    the K-ary map of P:672-676). P0 is the (already normalised) starting point. Returns (P, m, v)."""
+          m0=None, v0=None, t0=0, temperature=0.0, seed=0, through_map=True):
+    """K-ary PQQA, fp64: AdamW on the parameter W = P with the gradient through the map (grad_K_map,
+    reading R33; through_map=False: dR/dP itself, reading R29), (+ noise), then P <- clamp_normalize(P')
+    (the sensitive transition with the K-ary map of P:672-676). P0 is the (already normalised) starting
+    point. Returns (P, m, v)."""
     P = np.array(P0, dtype=np.float64)
     m = np.zeros_like(P) if m0 is None else np.array(m0, dtype=np.float64)
     v = np.zeros_like(P) if v0 is None else np.array(v0, dtype=np.float64)
     n, S, K = P.shape
     for k, gamma in enumerate(gammas):
         t = t0 + k + 1
-        g = grad_K(A, P, float(gamma), alpha, comm)
+        g = (grad_K_map if through_map else grad_K)(A, P, float(gamma), alpha, comm)
         P, m, v = adamw_step(P, m, v, g, t, lr, beta1, beta2, eps, wd)
         if temperature > 0.0:
             P = P + np.sqrt(2.0 * lr * temperature) * gauss_noise_K(seed, t, n, S, K)

@@ -34,7 +34,8 @@ class Config(ctypes.Structure):
                 ("init_lo", ctypes.c_float), ("init_hi", ctypes.c_float),
                 ("seed", ctypes.c_uint64),
                 ("S_total", ctypes.c_int32), ("replica_offset", ctypes.c_int32), ("S_local", ctypes.c_int32),
-                ("map", ctypes.c_int32), ("temperature", ctypes.c_float), ("n_colors", ctypes.c_int32)]
+                ("map", ctypes.c_int32), ("temperature", ctypes.c_float), ("n_colors", ctypes.c_int32),
+                ("kary_grad", ctypes.c_int32)]
 
 
 class Graph(ctypes.Structure):

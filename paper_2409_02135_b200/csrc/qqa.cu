@@ -145,6 +145,7 @@ int check_config(const qqa_config* c) {
     return fail(QQA_ERR_INVALID_ARG, "map must be 0 (sigmoid) or 1 (clamp)");
   if (!(c->temperature >= 0.0f) || !std::isfinite(c->temperature))
     return fail(QQA_ERR_INVALID_ARG, "temperature must be finite and >= 0");
+  if (c->kary_grad != 0 && c->kary_grad != 1) return fail(QQA_ERR_INVALID_ARG, "kary_grad must be 0 or 1");
   return QQA_OK;
 }
 
@@ -580,6 +581,7 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
   P.rowptr = h->rowptr; P.colidx = h->colidx; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = s.n; P.S = s.S_local; P.K = s.K; P.L = s.LK;
   P.Kf = (float)s.K; P.comm = c.comm; P.alpha = c.alpha;
+  P.kgrad = c.kary_grad;
   P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);
   P.b2 = c.beta2; P.c2 = (float)(1.0 - (double)c.beta2);
   P.eps = c.eps;

@@ -1185,6 +1185,7 @@ struct StepKParams {
   long long* __restrict__ sums_zero;    // [2][n K] buffer of the step after next (zeroed here)
   int* __restrict__ flag;
   int n, S, K, L;
+  int kgrad;                            // 1: gradient through the map, g - <g, p> (reading R33)
   float Kf, comm, b1, c1, b2, c2, eps, unif;   // unif = (float)(1/K)
   int alpha;
   float kt, at, st, rt, ns;
@@ -1278,6 +1279,26 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(co
       ld_colours<KP>(P.p_cur + at, w);
       ld_colours<KP>(P.m + at, mm);
       ld_colours<KP>(P.v + at, vv2);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {              // g_k = dR/dp_k (into q[k])
+        if (k >= P.K) continue;
+        const float pi = w[k];
+        const float2 st = P.ms[(size_t)i * P.K + k];
+        const float e = fsub(fmul(P.Kf, pi), 1.0f);
+        float ep = e;
+        for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);            // (K p - 1)^(alpha-1)
+        const float ent = fmul(P.kt, ep);
+        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
+        q[k] = fadd(fadd(q[k], ent), com);
+      }
+      if (P.kgrad) {                              // through the map: g - <g, p>, <g, p> in colour order
+        float gb = 0.0f;
+#pragma unroll
+        for (int k = 0; k < KP; ++k)
+          if (k < P.K) gb = fadd(gb, fmul(q[k], w[k]));
+#pragma unroll
+        for (int k = 0; k < KP; ++k) q[k] = fsub(q[k], gb);
+      }
       float xi = 0.0f, xi_odd = 0.0f;              // colours pair up (k even, k + 1) on one noise hash
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
@@ -1289,13 +1310,7 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(co
             xi = xi_odd;
         }
         const float pi = w[k];
-        const float2 st = P.ms[(size_t)i * P.K + k];
-        const float e = fsub(fmul(P.Kf, pi), 1.0f);
-        float ep = e;
-        for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);            // (K p - 1)^(alpha-1)
-        const float ent = fmul(P.kt, ep);
-        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
-        const float g = fadd(fadd(q[k], ent), com);
+        const float g = q[k];
         const float t1 = fmul(pi, P.at);
         mm[k] = fadd(fmul(P.b1, mm[k]), fmul(P.c1, g));
         vv2[k] = fadd(fmul(P.b2, vv2[k]), fmul(fmul(P.c2, g), g));
@@ -1370,6 +1385,7 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
     float w[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     float cl4[4] = {0.0f, 0.0f, 0.0f, 0.0f};             // Clamp(w) of this quad's colours
     float mm[4], vv2[4];
+    float qv[4] = {0.0f, 0.0f, 0.0f, 0.0f};             // q, then the gradient g of this quad's colours
     size_t at = 0;
     if (live) {
       const int e0 = __ldg(P.rowptr + i), e1 = __ldg(P.rowptr + i + 1);
@@ -1392,8 +1408,7 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
         const float4 pj = __ldg(reinterpret_cast<const float4*>(base + (size_t)__ldg(P.colidx + e) * P.S * KP));
         qa = make_float4(fadd(qa.x, pj.x), fadd(qa.y, pj.y), fadd(qa.z, pj.z), fadd(qa.w, pj.w));
       }
-      const float qv[4] = {qa.x, qa.y, qa.z, qa.w};
-      const unsigned long long rkey = P.nkey + (unsigned long long)i * (unsigned long long)P.K * P.S_total_u;
+      qv[0] = qa.x; qv[1] = qa.y; qv[2] = qa.z; qv[3] = qa.w;
       at = ((size_t)i * P.S + r) * KP + k0;
       const float4 w4 = *reinterpret_cast<const float4*>(P.p_cur + at);
       const float4 m4 = *reinterpret_cast<const float4*>(P.m + at);
@@ -1401,6 +1416,37 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
       w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
       mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
       vv2[0] = v4.x; vv2[1] = v4.y; vv2[2] = v4.z; vv2[3] = v4.w;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {               // g_k = dR/dp_k (into qv[c])
+        const int k = k0 + c;
+        if (k >= P.K) continue;
+        const float pi = w[c];
+        const float2 st = P.ms[(size_t)i * P.K + k];
+        const float e1f = fsub(fmul(P.Kf, pi), 1.0f);
+        float ep = e1f;
+        for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e1f);          // (K p - 1)^(alpha-1)
+        const float ent = fmul(P.kt, ep);
+        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
+        qv[c] = fadd(fadd(qv[c], ent), com);
+      }
+    }
+    // through the map (reading R33): g - <g, p>, <g, p> summed in colour order -- the running sum
+    // passes from quad to quad as the normaliser's does below
+    if (P.kgrad) {
+      float gb = 0.0f;
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        if (q == qq && live)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (k0 + c < P.K) gb = fadd(gb, fmul(qv[c], w[c]));
+        gb = __shfl_sync(0xffffffffu, gb, (lane & ~3) + qq);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) qv[c] = fsub(qv[c], gb);
+    }
+    if (live) {
+      const unsigned long long rkey = P.nkey + (unsigned long long)i * (unsigned long long)P.K * P.S_total_u;
       float xi = 0.0f, xi_odd = 0.0f;                    // colours pair up (k even, k + 1) on one noise hash
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -1413,13 +1459,7 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
             xi = xi_odd;
         }
         const float pi = w[c];
-        const float2 st = P.ms[(size_t)i * P.K + k];
-        const float e1f = fsub(fmul(P.Kf, pi), 1.0f);
-        float ep = e1f;
-        for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e1f);          // (K p - 1)^(alpha-1)
-        const float ent = fmul(P.kt, ep);
-        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
-        const float g = fadd(fadd(qv[c], ent), com);
+        const float g = qv[c];
         const float t1 = fmul(pi, P.at);
         mm[c] = fadd(fmul(P.b1, mm[c]), fmul(P.c1, g));
         vv2[c] = fadd(fmul(P.b2, vv2[c]), fmul(fmul(P.c2, g), g));

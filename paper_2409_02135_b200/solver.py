@@ -16,7 +16,7 @@ from ._lib import Config, Graph, ReplicaResult, check, lib
 
 DEFAULTS = dict(alpha=2, penalty=2.0, comm=0.1, lr=1.0, beta1=0.9, beta2=0.999, eps=1e-8,
                 weight_decay=0.01, init_lo=-0.01, init_hi=0.01, map="sigmoid", temperature=0.0,
-                n_colors=0)
+                n_colors=0, kary_grad=1)
 
 
 def make_config(problem="mis", S_total=16, seed=1, replica_offset=0, S_local=None, **hp) -> Config:
@@ -27,7 +27,7 @@ def make_config(problem="mis", S_total=16, seed=1, replica_offset=0, S_local=Non
     return Config(pid, int(kw["alpha"]), kw["penalty"], kw["comm"], kw["lr"], kw["beta1"], kw["beta2"],
                   kw["eps"], kw["weight_decay"], kw["init_lo"], kw["init_hi"], seed & 0xFFFFFFFFFFFFFFFF,
                   int(S_total), int(replica_offset), int(S_total if S_local is None else S_local),
-                  mid, float(kw["temperature"]), int(kw["n_colors"]))
+                  mid, float(kw["temperature"]), int(kw["n_colors"]), int(kw["kary_grad"]))
 
 
 def _as_graph(rowptr: np.ndarray, colidx: np.ndarray, group_of_row: np.ndarray | None = None,

@@ -60,9 +60,11 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("kary_grad", [1, 0])   # gradient through the map (R33, default) / dR/dP (R29)
 @pytest.mark.parametrize("case", range(len(CASES)))
-def test_fifty_steps_parity(Q, case):
+def test_fifty_steps_parity(Q, case, kary_grad):
     mk, K, S, hp = CASES[case]
+    hp = dict(hp, kary_grad=kary_grad)
     g = mk()
     gam = oracle.schedule(-2.0, 0.1, 1000)[:50]
     sol = gpu(Q, g, K, S, 11, **hp)
@@ -128,8 +130,9 @@ def test_invalid_colouring_configs(Q):
     assert e.value.status == 6
 
 
+@pytest.mark.parametrize("kary_grad", [1, 0])
 @pytest.mark.parametrize("K,S,T,steps", [(13, 1000, 0.0, 40), (10, 37, 0.002, 60), (16, 8, 0.0, 30), (9, 100, 0.001, 4100)])
-def test_colour_quad_kernel_equals_k_step_K(Q, monkeypatch, K, S, T, steps):
+def test_colour_quad_kernel_equals_k_step_K(Q, monkeypatch, K, S, T, steps, kary_grad):
     """k_step_Kq (4 colours per thread, 8 replicas per warp; KP = 12 / 16) is bit-identical to k_step_K,
     including noise pairs, ragged replica chunks and a schedule longer than one run() call."""
     g = gen.queens(7, 7)
@@ -137,7 +140,7 @@ def test_colour_quad_kernel_equals_k_step_K(Q, monkeypatch, K, S, T, steps):
     for flag in ("1", "0"):
         monkeypatch.setenv("QQA_KARY_QUAD", flag)
         sol = Q.Solver(g.rowptr, g.colidx, Q.make_config("coloring", S_total=S, seed=3, n_colors=K, lr=0.01,
-                                                         temperature=T, comm=0.3))
+                                                         temperature=T, comm=0.3, kary_grad=kary_grad))
         sol.run_linear(-2.0, 0.1, steps)
         out.append((sol.get_state(), sol.get_stats(), sol.round_evaluate()))
     (a, sa, ra), (b, sb, rb) = out
@@ -146,3 +149,14 @@ def test_colour_quad_kernel_equals_k_step_K(Q, monkeypatch, K, S, T, steps):
     for f in ("c", "sumD", "sumD2"):
         assert np.array_equal(sa[f], sb[f]), f
     assert ra.best_replica == rb.best_replica
+
+
+def test_gradient_through_the_map_reaches_table_4_on_small_queens(Q):
+    """Reading R33 on the GPU path: queen6-6 (7 colours), queen7-7 (7), queen8-8 (9) and queen9-9 (10)
+    coloured without a conflict, as Table 4 reports for PQQA."""
+    for (r, K) in [(6, 7), (7, 7), (8, 9), (9, 10)]:
+        g = gen.queens(r, r)
+        sol = Q.Solver(g.rowptr, g.colidx, Q.make_config("coloring", S_total=256, seed=1, n_colors=K, lr=0.1,
+                                                         temperature=0.001))
+        sol.run_linear(-2.0, 0.1, 3000)
+        assert int(sol.round_evaluate().best_energy) == 0, (r, K)

@@ -95,16 +95,48 @@ def test_clamp_normalize_properties():
     assert np.allclose(oracle.normalize_K(w[0]), np.clip(w[0], 0, 1) / np.clip(w[0], 0, 1).sum(), atol=1e-7)
 
 
-def test_first_step_closed_form_K():
-    """Adam from m = v = 0: P_1 = normalise(P_0 (1 - lr wd) - lr g / (|g| + eps))."""
+@pytest.mark.parametrize("through_map", [True, False])
+def test_first_step_closed_form_K(through_map):
+    """Adam from m = v = 0: P_1 = normalise(P_0 (1 - lr wd) - lr g / (|g| + eps)), g the gradient
+    through the map (R33) or dR/dP (R29)."""
     g = gen.queens(4, 4)
     A = D.dense_adjacency(g.n, g.rowptr, g.colidx)
     P0 = D.clamp_normalize(D.init_W_K(g.n, 6, 4, 9))
     lr, wd, gam = 0.1, 0.01, -1.0
-    G = D.grad_K(A, P0, gam, 2, 0.2)
+    G = (D.grad_K_map if through_map else D.grad_K)(A, P0, gam, 2, 0.2)
     want = D.clamp_normalize(P0 * (1 - lr * wd) - lr * G / (np.abs(G) + 1e-8))
-    got, _, _ = D.run_K(A, P0, [gam], alpha=2, comm=0.2, lr=lr, wd=wd)
+    got, _, _ = D.run_K(A, P0, [gam], alpha=2, comm=0.2, lr=lr, wd=wd, through_map=through_map)
     assert np.allclose(got, want, atol=1e-12)
+
+
+@pytest.mark.parametrize("alpha,comm,gamma", [(2, 0.0, -1.0), (4, 0.3, 0.5)])
+def test_grad_K_map_is_the_chain_rule_through_the_map(alpha, comm, gamma):
+    """Reading R33 pinned by central finite differences: at W = P (on the simplex, inside the clamp
+    range) dR/dW of R(clamp_normalize(W)) equals g - <g, P> per (variable, replica) row."""
+    g = gen.queens(4, 4)
+    A = D.dense_adjacency(g.n, g.rowptr, g.colidx)
+    rng = np.random.default_rng(3)
+    P = rng.dirichlet(np.full(5, 4.0), (g.n, 3))            # interior points, rows sum to 1
+    G = D.grad_K_map(A, P, gamma, alpha, comm)
+    h = 1e-6
+    for (i, s_, k) in [(0, 0, 0), (3, 1, 2), (7, 2, 4), (15, 0, 3)]:
+        Wp, Wm = P.copy(), P.copy()
+        Wp[i, s_, k] += h
+        Wm[i, s_, k] -= h
+        fd = (D.R_hat_K(A, D.clamp_normalize(Wp), gamma, alpha, comm)
+              - D.R_hat_K(A, D.clamp_normalize(Wm), gamma, alpha, comm)) / (2 * h)
+        assert abs(fd - G[i, s_, k]) <= 1e-5 * max(1.0, abs(fd)), (i, s_, k, fd, G[i, s_, k])
+
+
+def test_gradient_through_the_map_reproduces_table_4_small_queens():
+    """Evidence for R33 (Table 4): the gradient through the map colours queen6-6 with 7
+    colours and queen7-7 with 7 without a conflict, where dR/dP (R29) leaves conflicts."""
+    for (r, K) in [(6, 7), (7, 7)]:
+        gq = gen.queens(r, r)
+        st = oracle.run_K(gq, oracle.make_cfg("mis", S=64, seed=1, lr=0.1, threads=4, temperature=0.001), K,
+                          oracle.schedule(-2.0, 0.1, 2000))
+        _, energy, best, _ = oracle.evaluate_K(gq, st.P)
+        assert energy[best] == 0
 
 
 def test_gamma_negative_limit_is_simplex_centre():
