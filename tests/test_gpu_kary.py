@@ -128,6 +128,10 @@ def test_invalid_colouring_configs(Q):
     with pytest.raises(Q.QQAError) as e:
         Q.Solver(U.rowptr, U.colidx, Q.make_config("coloring", S_total=8, n_colors=4), group_of_row=gor)
     assert e.value.status == 6
+    for kg in (-1, 2):
+        with pytest.raises(Q.QQAError) as e:
+            gpu(Q, g, 4, 8, 1, kary_grad=kg)
+        assert e.value.status == 1
 
 
 @pytest.mark.parametrize("kary_grad", [1, 0])
