@@ -73,20 +73,22 @@ typedef struct {
 enum { OC_MAP_SIGMOID = 0, OC_MAP_CLAMP = 1 };
 
 /* ------------------------------------------------------------ sigmoid ---- */
-/* E = exp(-a) for 0 <= a <= 87, in fp32: a = k ln2 + r, exp(r) by Taylor. */
+/* E = exp(-a) for 0 <= a <= 87, in fp32: a = k ln2 + r, exp(r) by Taylor. The reduction and the
+ * Horner steps are fused multiply-adds (fmaf: one rounding, IEEE-exact on every platform, the GPU's
+ * __fmaf_rn), the contract of DESIGN.md §3 item 2. */
 float oc_exp_neg(float a) {
     const float x = -a;
     const float kf = rintf(x * 1.44269504088896341f);       /* nearest k */
-    const float r = (x - kf * 0.693145751953125f)             /* ln2 hi (exact products) */
-                    - kf * 1.428606765330187e-6f;              /* ln2 lo */
+    const float r = fmaf(-kf, 1.428606765330187e-6f,          /* ln2 lo */
+                         fmaf(-kf, 0.693145751953125f, x));   /* ln2 hi */
     float P = 1.0f / 5040.0f;                                  /* 1/7! */
-    P = P * r + 1.0f / 720.0f;
-    P = P * r + 1.0f / 120.0f;
-    P = P * r + 1.0f / 24.0f;
-    P = P * r + 1.0f / 6.0f;
-    P = P * r + 1.0f / 2.0f;
-    P = P * r + 1.0f;
-    P = P * r + 1.0f;
+    P = fmaf(P, r, 1.0f / 720.0f);
+    P = fmaf(P, r, 1.0f / 120.0f);
+    P = fmaf(P, r, 1.0f / 24.0f);
+    P = fmaf(P, r, 1.0f / 6.0f);
+    P = fmaf(P, r, 1.0f / 2.0f);
+    P = fmaf(P, r, 1.0f);
+    P = fmaf(P, r, 1.0f);
     int k = (int)kf;                                           /* in [-126, 0] */
     union { uint32_t u; float f; } two_k;
     two_k.u = (uint32_t)(k + 127) << 23;

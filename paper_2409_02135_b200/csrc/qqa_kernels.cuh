@@ -56,19 +56,20 @@ __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b)
 __device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
 
 // exp(-a) for 0 <= a <= 87: a = k ln2 + r (Cody-Waite), exp(r) by the degree-7
-// Taylor polynomial in Horner form, times 2^k built from bits.
+// Taylor polynomial in Horner form, times 2^k built from bits. Reduction and Horner steps are
+// explicit fused multiply-adds (__fmaf_rn == C fmaf, one rounding; DESIGN.md §3 item 2).
 __device__ __forceinline__ float exp_neg_c(float a) {
   const float x = -a;
   const float kf = rintf(fmul(x, 1.44269504088896341f));
-  const float r = fsub(fsub(x, fmul(kf, 0.693145751953125f)), fmul(kf, 1.428606765330187e-6f));
+  const float r = __fmaf_rn(-kf, 1.428606765330187e-6f, __fmaf_rn(-kf, 0.693145751953125f, x));
   float P = 1.0f / 5040.0f;
-  P = fadd(fmul(P, r), 1.0f / 720.0f);
-  P = fadd(fmul(P, r), 1.0f / 120.0f);
-  P = fadd(fmul(P, r), 1.0f / 24.0f);
-  P = fadd(fmul(P, r), 1.0f / 6.0f);
-  P = fadd(fmul(P, r), 0.5f);
-  P = fadd(fmul(P, r), 1.0f);
-  P = fadd(fmul(P, r), 1.0f);
+  P = __fmaf_rn(P, r, 1.0f / 720.0f);
+  P = __fmaf_rn(P, r, 1.0f / 120.0f);
+  P = __fmaf_rn(P, r, 1.0f / 24.0f);
+  P = __fmaf_rn(P, r, 1.0f / 6.0f);
+  P = __fmaf_rn(P, r, 0.5f);
+  P = __fmaf_rn(P, r, 1.0f);
+  P = __fmaf_rn(P, r, 1.0f);
   return fmul(P, __int_as_float((static_cast<int>(kf) + 127) << 23));
 }
 
