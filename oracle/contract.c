@@ -125,11 +125,11 @@ float oc_ln(float u) {
     const float f = m - 1.0f;
     const float s = f / (2.0f + f);
     const float z = s * s;
-    float P = 1.0f / 9.0f;
-    P = P * z + 1.0f / 7.0f;
-    P = P * z + 1.0f / 5.0f;
-    P = P * z + 1.0f / 3.0f;
-    P = P * z + 1.0f;
+    float P = 1.0f / 9.0f;                                     /* Horner steps as fmaf (one rounding) */
+    P = fmaf(P, z, 1.0f / 7.0f);
+    P = fmaf(P, z, 1.0f / 5.0f);
+    P = fmaf(P, z, 1.0f / 3.0f);
+    P = fmaf(P, z, 1.0f);
     const float lnm = 2.0f * (s * P);
     const float ef = (float)e;
     return (ef * 0.693145751953125f + lnm) + ef * 1.428606765330187e-6f;
@@ -144,16 +144,16 @@ void oc_cossin2pi(float x, float* c, float* sn) {
     const float r = y - k;
     const float a = r * 1.57079632679489662f;
     const float a2 = a * a;
-    float C = 1.0f / 40320.0f;
-    C = C * a2 - 1.0f / 720.0f;
-    C = C * a2 + 1.0f / 24.0f;
-    C = C * a2 - 0.5f;
-    C = C * a2 + 1.0f;
+    float C = 1.0f / 40320.0f;                                 /* Horner steps as fmaf (one rounding) */
+    C = fmaf(C, a2, -(1.0f / 720.0f));
+    C = fmaf(C, a2, 1.0f / 24.0f);
+    C = fmaf(C, a2, -0.5f);
+    C = fmaf(C, a2, 1.0f);
     float Sn = 1.0f / 362880.0f;
-    Sn = Sn * a2 - 1.0f / 5040.0f;
-    Sn = Sn * a2 + 1.0f / 120.0f;
-    Sn = Sn * a2 - 1.0f / 6.0f;
-    Sn = Sn * a2 + 1.0f;
+    Sn = fmaf(Sn, a2, -(1.0f / 5040.0f));
+    Sn = fmaf(Sn, a2, 1.0f / 120.0f);
+    Sn = fmaf(Sn, a2, -(1.0f / 6.0f));
+    Sn = fmaf(Sn, a2, 1.0f);
     Sn = Sn * a;
     const int q = ((int)k) & 3;
     *c = (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
@@ -167,24 +167,9 @@ float oc_sin2pi(float x) {
 }
 
 float oc_cos2pi(float x) {
-    const float y = 4.0f * x;
-    const float k = rintf(y);
-    const float r = y - k;
-    const float a = r * 1.57079632679489662f;
-    const float a2 = a * a;
-    float C = 1.0f / 40320.0f;
-    C = C * a2 - 1.0f / 720.0f;
-    C = C * a2 + 1.0f / 24.0f;
-    C = C * a2 - 0.5f;
-    C = C * a2 + 1.0f;
-    float Sn = 1.0f / 362880.0f;
-    Sn = Sn * a2 - 1.0f / 5040.0f;
-    Sn = Sn * a2 + 1.0f / 120.0f;
-    Sn = Sn * a2 - 1.0f / 6.0f;
-    Sn = Sn * a2 + 1.0f;
-    Sn = Sn * a;
-    const int q = ((int)k) & 3;
-    return (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;
+    float c, sn;
+    oc_cossin2pi(x, &c, &sn);
+    return c;
 }
 
 /* Two independent N(0, 1) from one 64-bit hash h by Box-Muller:

@@ -95,11 +95,11 @@ __device__ __forceinline__ float ln_c(float u) {
   const float f = fsub(m, 1.0f);
   const float sv = fdiv(f, fadd(2.0f, f));
   const float z = fmul(sv, sv);
-  float P = 1.0f / 9.0f;
-  P = fadd(fmul(P, z), 1.0f / 7.0f);
-  P = fadd(fmul(P, z), 1.0f / 5.0f);
-  P = fadd(fmul(P, z), 1.0f / 3.0f);
-  P = fadd(fmul(P, z), 1.0f);
+  float P = 1.0f / 9.0f;   // Horner steps as __fmaf_rn (== C fmaf)
+  P = __fmaf_rn(P, z, 1.0f / 7.0f);
+  P = __fmaf_rn(P, z, 1.0f / 5.0f);
+  P = __fmaf_rn(P, z, 1.0f / 3.0f);
+  P = __fmaf_rn(P, z, 1.0f);
   const float lnm = fmul(2.0f, fmul(sv, P));
   const float ef = (float)e;
   return fadd(fadd(fmul(ef, 0.693145751953125f), lnm), fmul(ef, 1.428606765330187e-6f));
@@ -113,16 +113,16 @@ __device__ __forceinline__ void cossin2pi_c(float x, float& cs, float& sn) {
   const float r = fsub(y, k);
   const float a = fmul(r, 1.57079632679489662f);
   const float a2 = fmul(a, a);
-  float C = 1.0f / 40320.0f;
-  C = fsub(fmul(C, a2), 1.0f / 720.0f);
-  C = fadd(fmul(C, a2), 1.0f / 24.0f);
-  C = fsub(fmul(C, a2), 0.5f);
-  C = fadd(fmul(C, a2), 1.0f);
+  float C = 1.0f / 40320.0f;   // Horner steps as __fmaf_rn (== C fmaf)
+  C = __fmaf_rn(C, a2, -(1.0f / 720.0f));
+  C = __fmaf_rn(C, a2, 1.0f / 24.0f);
+  C = __fmaf_rn(C, a2, -0.5f);
+  C = __fmaf_rn(C, a2, 1.0f);
   float Sn = 1.0f / 362880.0f;
-  Sn = fsub(fmul(Sn, a2), 1.0f / 5040.0f);
-  Sn = fadd(fmul(Sn, a2), 1.0f / 120.0f);
-  Sn = fsub(fmul(Sn, a2), 1.0f / 6.0f);
-  Sn = fadd(fmul(Sn, a2), 1.0f);
+  Sn = __fmaf_rn(Sn, a2, -(1.0f / 5040.0f));
+  Sn = __fmaf_rn(Sn, a2, 1.0f / 120.0f);
+  Sn = __fmaf_rn(Sn, a2, -(1.0f / 6.0f));
+  Sn = __fmaf_rn(Sn, a2, 1.0f);
   Sn = fmul(Sn, a);
   const int q = ((int)k) & 3;
   cs = (q == 0) ? C : (q == 1) ? -Sn : (q == 2) ? -C : Sn;

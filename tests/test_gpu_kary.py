@@ -160,7 +160,7 @@ def test_gradient_through_the_map_reaches_table_4_on_small_queens(Q):
     coloured without a conflict, as Table 4 reports for PQQA."""
     for (r, K) in [(6, 7), (7, 7), (8, 9), (9, 10)]:
         g = gen.queens(r, r)
-        sol = Q.Solver(g.rowptr, g.colidx, Q.make_config("coloring", S_total=256, seed=1, n_colors=K, lr=0.1,
+        sol = Q.Solver(g.rowptr, g.colidx, Q.make_config("coloring", S_total=1000, seed=1, n_colors=K, lr=0.1,
                                                          temperature=0.001))
         sol.run_linear(-2.0, 0.1, 3000)
         assert int(sol.round_evaluate().best_energy) == 0, (r, K)
