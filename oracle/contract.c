@@ -339,22 +339,22 @@ static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, co
         const float e = 2.0f * pi - 1.0f;
         float ep = e;
         for (int32_t a = 2; a < cf->alpha; ++a) ep = ep * e;   /* (2p-1)^(alpha-1) */
-        const float ent = kt * ep;
-        const float obj = (cf->problem == OC_MAXCUT) ? (2.0f * q[s] - degf)
-                          : (cf->problem == OC_MAXCLIQUE_SPARSE) ? (lam * ((Tcol[s] - 0.5f) - q[s]) - 1.0f)
-                          : (lam * q[s] - 1.0f);
+        /* a * b + c written fmaf(a, b, c) is one fused multiply-add (one rounding) in the contract */
+        const float obj = (cf->problem == OC_MAXCUT) ? fmaf(2.0f, q[s], -degf)
+                          : (cf->problem == OC_MAXCLIQUE_SPARSE) ? fmaf(lam, (Tcol[s] - 0.5f) - q[s], -1.0f)
+                          : fmaf(lam, q[s], -1.0f);
         const float com = (sd >= 1e-6f) ? (-ac) * ((pi - mu) / sd) : 0.0f;
-        const float gp = (obj + ent) + com;
+        const float gp = fmaf(kt, ep, obj) + com;         /* (obj + entropy) + comm */
         /* sigmoid: chain rule dR/dtheta = dR/dp p (1-p); clamp: the parameter is p */
         const float g = clamp ? gp : gp * (pi * (1.0f - pi));
         /* AdamW */
         float t1 = th[s] * at;
-        const float m1 = b1 * mm[s] + c1 * g;
-        const float v1 = b2 * vv[s] + (c2 * g) * g;
-        const float den = sqrtf(v1) * rt + eps;
-        t1 = t1 - st * (m1 / den);
+        const float m1 = fmaf(b1, mm[s], c1 * g);
+        const float v1 = fmaf(b2, vv[s], (c2 * g) * g);
+        const float den = fmaf(sqrtf(v1), rt, eps);
+        t1 = fmaf(-st, m1 / den, t1);
         if (cf->temperature > 0.0f)                       /* Langevin noise, Eq. 9 / 11 */
-            t1 = t1 + ns * oc_noise(nbase, t, n, i, S, s);
+            t1 = fmaf(ns, oc_noise(nbase, t, n, i, S, s), t1);
         if (!isfinite(t1)) nonfinite_flag = 1;            /* SPEC.md:396 abort, before the map */
         if (clamp) {
             t1 = oc_clamp01(t1);                          /* p^{t+1} = Clamp(p'), Eq. 11 */

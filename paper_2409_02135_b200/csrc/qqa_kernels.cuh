@@ -327,21 +327,21 @@ __device__ __forceinline__ float update_element(const StepParams& P, const StepV
   const float e = fsub(fmul(2.0f, pi), 1.0f);
   float ep = e;
   for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);                 // (2p-1)^(alpha-1)
-  const float ent = fmul(V.kt, ep);                                   // -2 alpha gamma (2p-1)^(alpha-1)
+  // __fmaf_rn(a, b, c) = one fused multiply-add (one rounding), C's fmaf
   // aux: the degree (Max-Cut) or the replica's column sum T (printed clique relaxation)
-  const float obj = (MODE & kModeSparseClique) ? fsub(fmul(P.lam, fsub(fsub(aux, 0.5f), q)), 1.0f)
-                    : (P.problem == kMAXCUT) ? fsub(fmul(2.0f, q), aux)                   // -deg + 2q
-                                             : fsub(fmul(P.lam, q), 1.0f);                // -1 + lambda q
+  const float obj = (MODE & kModeSparseClique) ? __fmaf_rn(P.lam, fsub(fsub(aux, 0.5f), q), -1.0f)
+                    : (P.problem == kMAXCUT) ? __fmaf_rn(2.0f, q, -aux)                   // -deg + 2q
+                                             : __fmaf_rn(P.lam, q, -1.0f);                // -1 + lambda q
   const float com = (sd >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, mu), sd)) : 0.0f;
-  const float gp = fadd(fadd(obj, ent), com);
+  const float gp = fadd(__fmaf_rn(V.kt, ep, obj), com);              // (obj - 2 alpha gamma (2p-1)^(alpha-1)) + comm
   const float g = (MODE & kModeClamp) ? gp                             // sensitive transition: d/dp
                                       : fmul(gp, fmul(pi, fsub(1.0f, pi)));  // chain rule through sigmoid
   const float t1 = fmul(th, P.at);                                    // decoupled weight decay
-  mm = fadd(fmul(P.b1, mm), fmul(P.c1, g));
-  vv = fadd(fmul(P.b2, vv), fmul(fmul(P.c2, g), g));
-  const float den = fadd(fmul(__fsqrt_rn(vv), V.rt), P.eps);
-  float w = fsub(t1, fmul(V.st, fdiv(mm, den)));
-  if (MODE & kModeNoise) w = fadd(w, fmul(P.ns, xi));                   // + sqrt(2 lr T) xi
+  mm = __fmaf_rn(P.b1, mm, fmul(P.c1, g));
+  vv = __fmaf_rn(P.b2, vv, fmul(fmul(P.c2, g), g));
+  const float den = __fmaf_rn(__fsqrt_rn(vv), V.rt, P.eps);
+  float w = __fmaf_rn(-V.st, fdiv(mm, den), t1);
+  if (MODE & kModeNoise) w = __fmaf_rn(P.ns, xi, w);                    // + sqrt(2 lr T) xi
   bad |= !isfinite(w);
   if (MODE & kModeClamp) {
     th = clamp01(w);

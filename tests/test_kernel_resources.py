@@ -31,10 +31,11 @@ def _get(usage, mangled):
 
 
 def test_headline_c5_kernel_fits_four_ctas(usage):
-    """c5 runs k_step<4,1,0,FULL> (two replica blocks of 32, every lane holds a vector): 64 registers, at
-    most the 8-byte spill it has around the division slow-path calls (a 16-byte spill cost 6 % on c5)."""
+    """c5 runs k_step<4,1,0,FULL> (two replica blocks of 32, every lane holds a vector): 64 registers and
+    at most the 16-byte spill around the division slow-path calls that the measured-faster FMA contract
+    leaves (profiles/r1_design_iterations.md); more would cost occupancy-bound bandwidth."""
     reg, stack = _get(usage, "_ZN3qqa6k_stepILi4ELi1ELi0ELb1EEEvNS_10StepParamsE")     # k_step<4,1,0,FULL>
-    assert reg <= 64 and stack <= 8
+    assert reg <= 64 and stack <= 16
 
 
 def test_unblocked_64_replica_kernel_has_no_spills(usage):

@@ -220,11 +220,30 @@ def test_pure_noise_random_walk_variance(mp):
     ns = oracle.noise_scale(cfg)
     assert ns == np.float32(math.sqrt(2 * lr * T))
     w = st0.theta.copy()
-    for t in range(1, K + 1):
-        w = (w + np.float32(ns) * oracle.noise(4, t, n, S)).astype(np.float32)
+    for t in range(1, K + 1):   # the contract adds the draw with one fused multiply-add: fma(ns, xi, w)
+        xi = oracle.noise(4, t, n, S)
+        w = np.array([_fma32(np.float32(ns), x, y) for x, y in zip(xi.ravel(), w.ravel())],
+                     np.float32).reshape(w.shape)
         if mp == "clamp":
             w = np.clip(w, 0, 1)
     assert np.array_equal(w, st.theta)
+
+
+def _fma32(a, b, c) -> np.float32:
+    """a * b + c rounded once to fp32 (round half to even), from exact rational arithmetic."""
+    from fractions import Fraction
+    x = Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c))
+    if x == 0:
+        return np.float32(0.0)
+    sign, x = (-1, -x) if x < 0 else (1, x)
+    e = x.numerator.bit_length() - x.denominator.bit_length()          # 2^e <= x < 2^(e+2)
+    if x < Fraction(2) ** e:
+        e -= 1
+    m = x / Fraction(2) ** (e - 23)                                     # in [2^23, 2^24)
+    q, r = divmod(m.numerator, m.denominator)
+    if 2 * r > m.denominator or (2 * r == m.denominator and q % 2 == 1):
+        q += 1
+    return np.float32(sign * q * 2.0 ** (e - 23))
 
 
 def test_temperature_zero_is_noise_free():
