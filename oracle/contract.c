@@ -646,9 +646,8 @@ static int update_row_K(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, 
             const float e = Kf * pi - 1.0f;
             float ep = e;
             for (int32_t a = 2; a < cf->alpha; ++a) ep = ep * e;       /* (K p - 1)^(alpha-1) */
-            const float ent = kt * ep;
             const float com = (sd[k] >= 1e-6f) ? (-ac) * ((pi - mu[k]) / sd[k]) : 0.0f;
-            q[k] = (q[k] + ent) + com;
+            q[k] = fmaf(kt, ep, q[k]) + com;                   /* (q + entropy) + comm, fused */
         }
         if (cf->kary_grad) {                      /* through the map: g - <g, p>, <g, p> in colour order */
             float gb = 0.0f;
@@ -659,16 +658,16 @@ static int update_row_K(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, 
             const float pi = pp[at_s + k];
             const float g = q[k];
             float t1 = pi * at;
-            const float m1 = b1 * mm[at_s + k] + c1 * g;
-            const float v1 = b2 * vv[at_s + k] + (c2 * g) * g;
-            const float den = sqrtf(v1) * rt + eps;
-            t1 = t1 - st * (m1 / den);
+            const float m1 = fmaf(b1, mm[at_s + k], c1 * g);
+            const float v1 = fmaf(b2, vv[at_s + k], (c2 * g) * g);
+            const float den = fmaf(sqrtf(v1), rt, eps);
+            t1 = fmaf(-st, m1 / den, t1);
             if (cf->temperature > 0.0f) {   /* colours pair up (k even, k + 1) on one hash */
                 const uint64_t key = nbase + (((uint64_t)t * (uint64_t)n + (uint64_t)i) * (uint64_t)K + (uint64_t)(k & ~1))
                                                  * (uint64_t)S + (uint64_t)s;
                 float zc, zs;
                 oc_gauss_pair_from_hash(mix64(key), &zc, &zs);
-                t1 = t1 + ns * ((k & 1) ? zs : zc);
+                t1 = fmaf(ns, (k & 1) ? zs : zc, t1);
             }
             if (!isfinite(t1)) bad = 1;
             w[k] = t1;

@@ -1288,9 +1288,8 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(co
         const float e = fsub(fmul(P.Kf, pi), 1.0f);
         float ep = e;
         for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);            // (K p - 1)^(alpha-1)
-        const float ent = fmul(P.kt, ep);
         const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
-        q[k] = fadd(fadd(q[k], ent), com);
+        q[k] = fadd(__fmaf_rn(P.kt, ep, q[k]), com);             // (q + entropy) + comm, fused
       }
       if (P.kgrad) {                              // through the map: g - <g, p>, <g, p> in colour order
         float gb = 0.0f;
@@ -1313,11 +1312,11 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(co
         const float pi = w[k];
         const float g = q[k];
         const float t1 = fmul(pi, P.at);
-        mm[k] = fadd(fmul(P.b1, mm[k]), fmul(P.c1, g));
-        vv2[k] = fadd(fmul(P.b2, vv2[k]), fmul(fmul(P.c2, g), g));
-        const float den = fadd(fmul(__fsqrt_rn(vv2[k]), P.rt), P.eps);
-        float x = fsub(t1, fmul(P.st, fdiv(mm[k], den)));
-        if (MODE & kModeNoise) x = fadd(x, fmul(P.ns, xi));
+        mm[k] = __fmaf_rn(P.b1, mm[k], fmul(P.c1, g));
+        vv2[k] = __fmaf_rn(P.b2, vv2[k], fmul(fmul(P.c2, g), g));
+        const float den = __fmaf_rn(__fsqrt_rn(vv2[k]), P.rt, P.eps);
+        float x = __fmaf_rn(-P.st, fdiv(mm[k], den), t1);
+        if (MODE & kModeNoise) x = __fmaf_rn(P.ns, xi, x);
         bad |= !isfinite(x);
         w[k] = x;
       }
@@ -1426,9 +1425,8 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
         const float e1f = fsub(fmul(P.Kf, pi), 1.0f);
         float ep = e1f;
         for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e1f);          // (K p - 1)^(alpha-1)
-        const float ent = fmul(P.kt, ep);
         const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
-        qv[c] = fadd(fadd(qv[c], ent), com);
+        qv[c] = fadd(__fmaf_rn(P.kt, ep, qv[c]), com);           // (q + entropy) + comm, fused
       }
     }
     // through the map (reading R33): g - <g, p>, <g, p> summed in colour order -- the running sum
@@ -1462,11 +1460,11 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
         const float pi = w[c];
         const float g = qv[c];
         const float t1 = fmul(pi, P.at);
-        mm[c] = fadd(fmul(P.b1, mm[c]), fmul(P.c1, g));
-        vv2[c] = fadd(fmul(P.b2, vv2[c]), fmul(fmul(P.c2, g), g));
-        const float den = fadd(fmul(__fsqrt_rn(vv2[c]), P.rt), P.eps);
-        float x = fsub(t1, fmul(P.st, fdiv(mm[c], den)));
-        if (MODE & kModeNoise) x = fadd(x, fmul(P.ns, xi));
+        mm[c] = __fmaf_rn(P.b1, mm[c], fmul(P.c1, g));
+        vv2[c] = __fmaf_rn(P.b2, vv2[c], fmul(fmul(P.c2, g), g));
+        const float den = __fmaf_rn(__fsqrt_rn(vv2[c]), P.rt, P.eps);
+        float x = __fmaf_rn(-P.st, fdiv(mm[c], den), t1);
+        if (MODE & kModeNoise) x = __fmaf_rn(P.ns, xi, x);
         bad |= !isfinite(x);
         w[c] = x;
         cl4[c] = clamp01(x);
