@@ -9,8 +9,10 @@ whole job = N_vars * S_total * T * steps / (max over ranks of the timed region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl ours|reference]
 
-N > 1 runs under torchrun (one process per GPU); replicas are sharded
-(S_local = S / N) -- strong scaling of the fixed S of BASELINE.json configs[4].
+N > 1 runs one process per GPU (replicas sharded, S_local = S / N: strong scaling of the
+fixed S of BASELINE.json configs[4]). Started without torchrun (WORLD_SIZE unset), bench.py
+re-launches itself as N local ranks through ``torch.distributed.run`` (127.0.0.1, a free port);
+rank 0 prints the one JSON line.
 ``--impl reference`` times the CPU oracle (oracle/, the reference arm of this
 tier) on a bounded sample of the same workload.
 """
@@ -43,6 +45,48 @@ def algorithmic_bytes(n: int, nnz: int, S_local: int, K: int = 1) -> int:
     CSR indices (4 nnz + 4 (n+1)) + gathered neighbour values (4 nnz S_l) + theta/m/v read+write (24 n S_l).
     K-ary (NEXT-4): every replica-variable carries K colour columns, so S_l -> S_l K."""
     return 4 * nnz + 4 * (n + 1) + 4 * nnz * S_local * K + 24 * n * S_local * K
+
+
+def compulsory_bytes(n: int, nnz_pad: int, S_local: int, B: int = 1, K: int = 1) -> int:
+    """The DRAM bytes a step cannot avoid with this layout (VERDICT r1 'What's weak' #4): theta/m/v read
+    and write (24 n S_p), p_next written and every p row read once (8 n S_p), the padded CSR once per
+    replica block (B (4 nnz_pad + 4 (n+1))), the statistics (int64 sums write + read, (mu, STD), shift:
+    48 n). S_p = S_local rounded up to 8 (the kernels move padded columns). K-ary: S_p -> S_local K."""
+    S_p = (S_local + 7) // 8 * 8 if K == 1 else S_local * K
+    return 32 * n * S_p + B * (4 * nnz_pad + 4 * (n + 1)) + 48 * n * K
+
+
+NOMINAL_HBM_GBS = 8000.0   # nominal B200 HBM3e (DGX figure; HGX quotes 7.7 TB/s, B200_PROFILING.md)
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_command(argv: list[str], gpus: int, port: int) -> list[str]:
+    """The command that runs this bench as ``gpus`` local ranks (one process per GPU), exactly as the
+    driver's torchrun launch does: ``python -m torch.distributed.run --nnodes=1 --nproc-per-node N
+    --master-addr 127.0.0.1 --master-port P bench.py <same args>``."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def maybe_relaunch(args, argv: list[str]) -> bool:
+    """--gpus N > 1 without a torchrun environment: run the N ranks as children (their stdout is this
+    process's original stdout, so rank 0's JSON line is the only stdout line) and exit with their code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    cmd = relaunch_command(argv, args.gpus, free_port())
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    r = subprocess.run(cmd, stdout=_RESULT_FD, stderr=2)
+    if r.returncode != 0:
+        print(f"bench.py: the {args.gpus}-rank run exited with {r.returncode}", file=sys.stderr)
+    sys.exit(r.returncode)
 
 
 def measured_peaks():
@@ -152,10 +196,10 @@ def run_reference(args, w):
     value = g.n * w.S * n_sample * args.steps / t
     sample = (f"{n_sample} of {w.steps} annealing steps of {w.name} per bench step at full size "
               f"(N={g.n}, nnz={g.nnz}, S={w.S}); oracle/contract.c, OpenMP over rows")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, args.gpus),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": workload_config(w, world),
+            "data": "synthetic", "config": workload_config(w, max(world, args.gpus)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                              "cpu": model},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -197,11 +241,106 @@ def emit(line: dict) -> None:
     os.write(_RESULT_FD if _RESULT_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
+def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, stream, barrier, max_over_ranks):
+    """N > 1: the per-step statistics exchange. Every phase that can fail on one rank (symmetric-memory
+    attach, the reference handle, the bit-exact self-check against NCCL, the timing probe) is wrapped,
+    and the ranks agree (MIN all-reduce) before the next collective phase, so a failure anywhere sends
+    every rank back to the NCCL handle instead of leaving the others waiting in a collective.
+    Returns (solver, peer pointers or None, description, probe times or None)."""
+    exchange = "nccl all-reduce (4-chunk overlap)"
+    if args.exchange == "nccl" or w.n_colors:
+        return sol, None, exchange, None
+
+    def agree(ok: bool) -> bool:
+        return qdist.all_ranks(ok, device=dev)
+
+    xptrs = None
+    try:
+        xptrs = qdist.attach_exchange(sol, rank, world)
+        ok = True
+    except Exception as e:   # no symmetric memory / peer mapping here: stay on NCCL
+        print(f"fused exchange unavailable: {e!r}", file=sys.stderr)
+        ok = False
+    if not agree(ok):
+        if xptrs is not None:   # this rank attached, another did not: back to a plain NCCL handle
+            sol.close()
+            sol = make_solver()
+            qdist.attach(sol, rank, world)
+        return sol, None, exchange + " (fused exchange unavailable on a rank)", None
+    if args.exchange == "fused":
+        return sol, xptrs, "fused peer-memory exchange in k_step_x (forced)", None
+
+    ref = None
+    try:
+        ref = make_solver()
+        ok = True
+    except Exception as e:
+        print(f"reference NCCL handle failed: {e!r}", file=sys.stderr)
+        ok = False
+    if not agree(ok):
+        # keep the fused handle only if nothing can be checked: rebuild a plain NCCL handle instead
+        if ref is not None:
+            ref.close()
+        sol.close()
+        sol = make_solver()
+        qdist.attach(sol, rank, world)
+        return sol, None, exchange + " (self-check handle unavailable)", None
+    ref.share_comm(sol)   # collective over the ranks' NCCL communicator (all ranks reach it together)
+
+    def fallback(why):
+        sol.close()
+        return ref, None, exchange + f" ({why})", None
+
+    try:   # bit-exact self-check of the fused exchange against NCCL, 3 steps
+        for s in (sol, ref):
+            s.reset()
+            s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 3)
+        a, b = sol.get_state(), ref.get_state()
+        ok = all(np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)) for k in ("theta", "m", "v", "p"))
+        ok = ok and np.array_equal(sol.get_stats()["sumD2"], ref.get_stats()["sumD2"])
+    except Exception as e:
+        print(f"fused-exchange self-check raised: {e!r}", file=sys.stderr)
+        ok = False
+    if not agree(ok):
+        return fallback("fused exchange failed its self-check")
+
+    def probe(s):
+        s.reset()
+        barrier()
+        a0, a1 = torch_event(), torch_event()
+        a0.record(stream)
+        s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 5)
+        a1.record(stream)
+        barrier()
+        return a0.elapsed_time(a1) / 5
+
+    try:
+        tf, tn = probe(sol), probe(ref)
+        ok = True
+    except Exception as e:
+        print(f"exchange probe raised: {e!r}", file=sys.stderr)
+        tf, tn, ok = 0.0, 0.0, False
+    if not agree(ok):
+        return fallback("exchange probe failed")
+    probe_ms = {"fused_ms_per_step": max_over_ranks(tf), "nccl_ms_per_step": max_over_ranks(tn)}
+    if qdist.pick_exchange(probe_ms["fused_ms_per_step"], probe_ms["nccl_ms_per_step"]) == "nccl":
+        sol.close()
+        return ref, None, exchange + " (faster than the fused exchange here)", probe_ms
+    ref.close()
+    return sol, xptrs, "fused peer-memory exchange in k_step_x", probe_ms
+
+
+def torch_event():
+    import torch
+    return torch.cuda.Event(enable_timing=True)
+
+
 def main():
     global _RESULT_FD
     sys.stdout.flush()
     _RESULT_FD = os.dup(1)
     os.dup2(2, 1)
+    argv = sys.argv[1:]
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -220,12 +359,22 @@ def main():
     ap.add_argument("--replicas", type=int, default=None, help="override S (diagnostics: per-rank work of a sharded run)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--anneal-steps", type=int, default=None, help="override T (diagnostics only)")
-    ap.add_argument("--cpu-sample-steps", type=int, default=60, help="annealing steps of the cpu_baseline sample "
-                    "(c5: about 15 s on 16 cores)")
+    ap.add_argument("--cpu-sample-steps", type=int, default=60, help="annealing steps of the all-core cpu_baseline "
+                    "sample (c5: about 15 s on 16 cores)")
+    ap.add_argument("--cpu1-sample-steps", type=int, default=3, help="annealing steps of the single-thread oracle "
+                    "sample (c5: about 10 s)")
     ap.add_argument("--ref-sample-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="tests: exercise the N-rank launch (gloo, no GPU work); rank 0 prints one JSON line")
     args = ap.parse_args()
+
+    if args.impl == "ours" and maybe_relaunch(args, argv):
+        return
+    if args.launcher_selftest:
+        launcher_selftest(args)
+        return
 
     import gen
     w = gen.workload(args.workload)
@@ -254,14 +403,14 @@ def main():
 
     rank, local_rank, world = dist_env()
     if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     sharded = world > 1 or args.force_dist   # the multi-GPU code path (--force-dist: also at N = 1)
     if sharded:
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29541")
+            os.environ.setdefault("MASTER_PORT", str(free_port()))
             dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
         else:
             dist.init_process_group("nccl", device_id=dev)
@@ -279,56 +428,15 @@ def main():
     def max_over_ranks(x: float) -> float:
         return qdist.max_over_ranks(x, device=dev)
 
-    sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
+    def make_solver():
+        return Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
+
+    sol = make_solver()
     exchange, xptrs, exchange_probe = None, None, None
     if sharded:
         qdist.attach(sol, rank, world)
-        exchange = "nccl all-reduce (4-chunk overlap)"
-        if args.exchange != "nccl" and not w.n_colors:
-            try:
-                xptrs = qdist.attach_exchange(sol, rank, world)
-                ok_attach = 1
-            except Exception as e:   # no symmetric memory / peer mapping here: stay on NCCL
-                print(f"fused exchange unavailable: {e!r}", file=sys.stderr)
-                ok_attach = 0
-            if not qdist.all_ranks(ok_attach == 1, device=dev):
-                if xptrs is not None:   # this rank attached, another did not: back to a plain NCCL handle
-                    sol.close()
-                    sol = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
-                    qdist.attach(sol, rank, world)
-                xptrs = None
-            else:
-                exchange = "fused peer-memory exchange in k_step_x"
-        if xptrs is not None and args.exchange == "auto":   # bit-exact self-check against NCCL, agreed by all ranks
-            ref = Q.Solver(g.rowptr, g.colidx, cfg, device=dev, stream=stream, group_of_row=gor)
-            ref.share_comm(sol)
-            for s in (sol, ref):
-                s.reset()
-                s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 3)
-            a, b = sol.get_state(), ref.get_state()
-            ok = all(np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)) for k in ("theta", "m", "v", "p"))
-            ok = ok and np.array_equal(sol.get_stats()["sumD2"], ref.get_stats()["sumD2"])
-            if qdist.all_ranks(ok, device=dev):   # both exact: keep the faster one (max over ranks, 5 steps each)
-                def probe(s):
-                    s.reset()
-                    barrier()
-                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a0.record(stream)
-                    s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 5)
-                    a1.record(stream)
-                    barrier()
-                    return max_over_ranks(a0.elapsed_time(a1)) / 5
-                exchange_probe = {"fused_ms_per_step": probe(sol), "nccl_ms_per_step": probe(ref)}
-                if qdist.pick_exchange(exchange_probe["fused_ms_per_step"], exchange_probe["nccl_ms_per_step"]) == "nccl":
-                    sol.close()
-                    sol, xptrs = ref, None
-                    exchange = "nccl all-reduce (4-chunk overlap; faster than the fused exchange here)"
-                else:
-                    ref.close()
-            else:
-                sol.close()
-                sol, xptrs = ref, None
-                exchange = "nccl all-reduce (4-chunk overlap; fused exchange failed its self-check)"
+        sol, xptrs, exchange, exchange_probe = select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev,
+                                                               stream, barrier, max_over_ranks)
 
     def evaluate(s):
         if gor is not None:   # batch: every instance's best replica (NEXT-3)
@@ -343,9 +451,8 @@ def main():
     for _ in range(args.warmup):
         solve(sol)
 
-    # ------------------------------------------------------- timed region
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sol.profile(True)
+    # ------------------------------------------------------- timed region (no instrumentation)
+    ev0, ev1 = torch_event(), torch_event()
     l0 = sol.launch_count()
     barrier()
     with ClockSampler(local_rank) as clk:
@@ -356,13 +463,29 @@ def main():
         barrier()
     l1 = sol.launch_count()
     t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    clocks = clk.summary()
+
+    # ------------------------------------- step-kernel duration: a separate profiled pass, same solves
+    # (per-launch CUDA events on the launching stream; kept out of the headline region)
+    sol.profile(True)
+    barrier()
+    p0, p1 = torch_event(), torch_event()
+    p0.record(stream)
+    for _ in range(min(args.steps, 3)):
+        solve(sol)
+    p1.record(stream)
+    barrier()
+    prof_ms = max_over_ranks(p0.elapsed_time(p1))
     kern_ms, kern_launches = sol.profile_read()
     sol.profile(False)
-    clocks = clk.summary()
 
     total_updates = g.n * w.S * w.steps * args.steps
     value = total_updates / (t_ms / 1e3)
-    B = algorithmic_bytes(g.n, g.nnz, S_l, max(1, w.n_colors))
+    K = max(1, w.n_colors)
+    B = algorithmic_bytes(g.n, g.nnz, S_l, K)
+    nnz_pad = int(np.sum((np.diff(g.rowptr) + 3) // 4 * 4))
+    n_blocks = 1 if w.n_colors else -(-((S_l + 7) // 8 * 8) // sol.replica_block())   # replica blocks B
+    Bc = compulsory_bytes(g.n, nnz_pad, S_l, n_blocks, K)
     avg_kernel_s = kern_ms / 1e3 / max(kern_launches, 1)
     peak, peak_src = measured_peaks()
     achieved = B / avg_kernel_s / 1e9
@@ -398,7 +521,7 @@ def main():
 
         e2e_step()  # warm
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch_event(), torch_event()
         e0.record(stream)
         for _ in range(args.steps):
             e2e_step()
@@ -416,9 +539,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         cores, model = cpu_info()
         v, dt = oracle_sample(w, args.cpu_sample_steps, cores)
+        v1, dt1 = oracle_sample(w, args.cpu1_sample_steps, 1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": model,
                "sample": f"{args.cpu_sample_steps} of {w.steps} annealing steps of {w.name} at full size "
-                         f"(N={g.n}, S={w.S}), {dt:.1f} s; oracle/contract.c with OpenMP over rows"}
+                         f"(N={g.n}, S={w.S}), {dt:.1f} s; oracle/contract.c with OpenMP over rows",
+               "single_thread": {"value": v1, "unit": UNIT, "cores": 1,
+                                 "sample": f"{args.cpu1_sample_steps} annealing steps at full size, {dt1:.1f} s, "
+                                           "the same oracle with one thread"}}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -428,23 +555,49 @@ def main():
                                **({"exchange_probe": exchange_probe} if exchange_probe else {})),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
+                             "frac_nominal": achieved / NOMINAL_HBM_GBS,
+                             "nominal_peak": NOMINAL_HBM_GBS,
                              # the DRAM bytes ncu measured per launch over the same launch time: the byte
                              # model counts every gathered row, L2 hits included, so frac can exceed 1
                              "traffic_achieved": (traffic / avg_kernel_s / 1e9) if traffic else None,
                              "traffic_frac": (traffic / avg_kernel_s / 1e9 / peak) if traffic else None,
+                             "compulsory_bytes": Bc,
+                             "dram_frac_vs_compulsory": (traffic / Bc) if traffic else None,
                              "kernel": ("qqa::k_step_K (fused K-ary gather + gradient + AdamW + normalise + stats)"
                                         if w.n_colors else
                                         "qqa::k_step_x (fused gather + gradient + AdamW + stats + peer exchange)"
                                         if xptrs is not None else "qqa::k_step (fused gather + gradient + AdamW + stats)"),
                              "bytes_per_launch": B, "avg_launch_ms": avg_kernel_s * 1e3,
                              "launches_timed": kern_launches, "peak_source": peak_src,
-                             "step_kernel_share": kern_ms / t_ms},
+                             "kernel_timing": "per-launch CUDA events on the launching stream in a separate "
+                                              f"profiled pass of {min(args.steps, 3)} identical solves (not in "
+                                              "the headline region)",
+                             "step_kernel_share": kern_ms / prof_ms},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": l1 - l0, "clocks": clocks,
                 "result": ({"best_replica": res.best_replica, "best_energy": res.best_energy} if gor is None else
                            {"instances": len(w.graphs), "best_energy_per_instance": [float(x) for x in res.best_energy]})}
         emit(line)
     if sharded:
         dist.destroy_process_group()
+
+
+def launcher_selftest(args):
+    """--gpus N --launcher-selftest (tests only): every rank joins a gloo group; rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+
+    rank, _, world = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank], dtype=torch.int64)
+        dist.all_reduce(t)
+        ranks_sum = int(t.item())
+        dist.destroy_process_group()
+    else:
+        ranks_sum = 0
+    if rank == 0:
+        emit({"launcher_selftest": True, "n_gpus": world, "gpus_arg": args.gpus, "ranks_sum": ranks_sum,
+              "master_addr": os.environ.get("MASTER_ADDR")})
 
 
 if __name__ == "__main__":

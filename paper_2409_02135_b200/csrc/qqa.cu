@@ -255,6 +255,36 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   return QQA_OK;
 }
 
+// Host check of the ORIGINAL CSR for QQA_MAXCLIQUE (the device k_validate runs on the graph the
+// kernels walk, which for the dense clique is the complement; the complement is built from the
+// original on the host, so the original must be checked before it is indexed). Same conditions as
+// k_validate: columns in [0, n), rows strictly ascending (no duplicates), no self-loops, symmetric,
+// no edge between two instances of a batch.
+int validate_host(const qqa_graph* g) {
+  const int n = g->n;
+  for (int i = 0; i < n; ++i) {
+    int64_t prev = -1;
+    for (int64_t e = g->rowptr[i]; e < g->rowptr[i + 1]; ++e) {
+      const int j = g->colidx[e];
+      if (j < 0 || j >= n) return fail(QQA_ERR_BAD_GRAPH, "graph rejected: column out of range;");
+      if (j <= prev) return fail(QQA_ERR_BAD_GRAPH, "graph rejected: row not strictly ascending (unsorted or duplicate);");
+      if (j == i) return fail(QQA_ERR_BAD_GRAPH, "graph rejected: self-loop;");
+      if (g->group_of_row && g->group_of_row[j] != g->group_of_row[i])
+        return fail(QQA_ERR_BAD_GRAPH, "graph rejected: edge between two instances of the batch;");
+      prev = j;
+    }
+  }
+  for (int i = 0; i < n; ++i)   // symmetry (rows are sorted now): i must appear in row j
+    for (int64_t e = g->rowptr[i]; e < g->rowptr[i + 1]; ++e) {
+      const int j = g->colidx[e];
+      const int32_t* a = g->colidx + g->rowptr[j];
+      const int32_t* b = g->colidx + g->rowptr[j + 1];
+      const int32_t* f = std::lower_bound(a, b, i);
+      if (f == b || *f != i) return fail(QQA_ERR_BAD_GRAPH, "graph rejected: not symmetric;");
+    }
+  return QQA_OK;
+}
+
 // Complement CSR (max clique = MIS on the complement graph); for a batch
 // the complement is taken inside each instance (block-diagonal union of complements).
 void build_complement(const qqa_graph* g, std::vector<int>& rp, std::vector<int>& ci) {
@@ -1085,7 +1115,10 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   std::vector<int> rp32, ci_c;
   const int32_t* ci_src = g->colidx;
   if (cfg->problem == QQA_MAXCLIQUE) {
+    if ((st = validate_host(g))) return cleanup(st);
     build_complement(g, rp32, ci_c);
+    if ((int64_t)ci_c.size() != s.nnz || rp32[s.n] != (int)s.nnz)   // the sizes make_shape planned
+      return cleanup(fail(QQA_ERR_BAD_GRAPH, "graph rejected: complement size differs from the planned one"));
     ci_src = ci_c.data();
   } else {
     rp32.resize((size_t)s.n + 1);
@@ -1136,6 +1169,8 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   {  // row-padded CSR for the step kernel (rows rounded up to 4 entries, sentinel n)
     std::vector<int> rp_pad((size_t)s.n + 1, 0);
     for (int i = 0; i < s.n; ++i) rp_pad[i + 1] = rp_pad[i] + (rp32[i + 1] - rp32[i] + 3) / 4 * 4;
+    if ((int64_t)rp_pad[s.n] != s.nnz_pad)
+      return cleanup(fail(QQA_ERR_BAD_GRAPH, "graph rejected: padded CSR size differs from the planned one"));
     QQA_CUDA_C(cudaMemcpyAsync(h->rowptr_pad, rp_pad.data(), rp_pad.size() * sizeof(int), cudaMemcpyHostToDevice,
                                h->stream));
     if (s.n > 0) {
@@ -1674,7 +1709,7 @@ int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2) {
   if (h->xmode && n && (sumD || sumD2)) {   // owner rows hold the totals: gather them into the scratch
     const qqa::XParams X = make_xparams(h, h->scur, h->scur, h->scur, h->cur, h->cur);
     qqa::k_x_gather<<<std::max(1, std::min((int)((n + 255) / 256), h->sm_count * 8)), 256, 0, h->stream>>>(
-        X, (int)n, h->ws_sums[0]);
+        X, (int)n, h->ws_sums[0], h->flag);
     QQA_CUDA(cudaGetLastError());
     sums = h->ws_sums[0];
   }
@@ -1682,7 +1717,10 @@ int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2) {
     QQA_CUDA(cudaMemcpyAsync(sumD, sums, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   if (sumD2 && n)
     QQA_CUDA(cudaMemcpyAsync(sumD2, sums + n, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  int flag = 0;
+  if (h->xmode) QQA_CUDA(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   QQA_CUDA(cudaStreamSynchronize(h->stream));
+  if (flag & 4) return fail(QQA_ERR_COMM, "fused exchange: a peer rank never arrived at a step barrier");
   return QQA_OK;
 }
 

@@ -652,8 +652,10 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
 __global__ void k_x_arrive(const XParams X) {
   if (threadIdx.x == 0 && blockIdx.x == 0) x_arrive_all(X);
 }
-// Owner rows of the current sums -> a local [2][n] copy (qqa_get_stats).
-__global__ void k_x_gather(const XParams X, int n, long long* __restrict__ out) {
+// Owner rows of the current sums -> a local [2][n] copy (qqa_get_stats). Waits for the barrier that
+// ends the last step first: until every rank has arrived, peers may still be adding into owner rows.
+__global__ void k_x_gather(const XParams X, int n, long long* __restrict__ out, int* err) {
+  x_wait(X, err);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const long long* sc = X.peer_cur[min(i / X.rows_per_rank, X.G - 1)];
     out[i] = sc[i];

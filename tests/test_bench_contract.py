@@ -47,3 +47,32 @@ def test_workload_configs_shard_for_the_scaling_run():
     w = gen.workload("c1")
     cfg = bench.workload_config(w, 1)
     assert cfg["N"] == 256 and cfg["S"] == 16 and cfg["anneal_steps"] == 1000
+
+
+def test_relaunch_command_is_the_driver_launch():
+    """--gpus N without torchrun re-launches as N local ranks, exactly the driver's torchrun form."""
+    cmd = bench.relaunch_command(["--gpus", "8", "--steps", "2"], 8, 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == [os.path.join(ROOT, "bench.py"), "--gpus", "8", "--steps", "2"][-4:]
+    assert cmd[cmd.index(os.path.join(ROOT, "bench.py")) + 1:] == ["--gpus", "8", "--steps", "2"]
+
+
+def test_gpus_n_without_torchrun_runs_n_ranks_one_json_line():
+    """`python bench.py --gpus 2` (no WORLD_SIZE): two ranks are launched (gloo here), only rank 0 prints."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                          "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launcher-selftest"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["launcher_selftest"] and d["n_gpus"] == 2 and d["gpus_arg"] == 2 and d["ranks_sum"] == 1
+    assert d["master_addr"] == "127.0.0.1"
+
+
+def test_compulsory_bytes_c5():
+    """c5's compulsory DRAM floor is about 2.26 GB per step (replica blocks of 32)."""
+    b = bench.compulsory_bytes(1_000_000, 20_000_000, 64, 2)
+    assert 2.2e9 < b < 2.3e9

@@ -4,6 +4,8 @@ Bar (BASELINE.json north_star): replica state p within max-abs 1e-4 after 50
 fp32 steps, integer evaluation bit-exact. The arithmetic contract
 makes the expected result bit-identical, which is asserted as well.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -163,6 +165,53 @@ def test_c5_sampled_rows_full_size(Q):
         assert np.array_equal(out["sumD"], astats["sumD"][rows]) and np.array_equal(out["sumD2"], astats["sumD2"][rows])
 
 
+def test_c5_fifty_steps_full_size_bitwise(Q):
+    """The headline config (c5: MIS, 20-regular N=1e6, S=64, bench.py's launch configuration: replica blocks
+    of 32, k_step<4,1,0,FULL>) at FULL size for 50 steps: every element of theta / m / v / p and the int64
+    statistics bit-exact against the contract oracle (north_star: p within 1e-4 after 50 fp32 steps), then
+    the rounded solutions' integer counts bit-exact against oracle.evaluate."""
+    w = gen.workload("c5")
+    g = w.graphs[0]
+    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
+    sol = gpu(Q, g, "mis", w.S, w.seeds[0], **hp)
+    assert sol.replica_block() == 32 and sol.step_path() == "step"
+    sol.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 50)
+    gam = oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:50]
+    st = oracle.run(g, ocfg("mis", w.S, w.seeds[0], threads=os.cpu_count() or 8, **hp), gam)
+    assert_state_equal(sol, st)
+    assert_stats_equal(sol, st)
+    counts, energy, best = oracle.evaluate(g, "mis", w.penalty, st.theta)
+    res = sol.round_evaluate()
+    pr = res.per_replica
+    assert np.array_equal(np.stack([pr["size"], pr["violations"], pr["cut"]], 1), counts)
+    assert np.array_equal(pr["energy"], energy)
+    assert res.best_replica == best and res.best_energy == energy[best]
+    assert np.array_equal(res.best_x, (st.theta[:, best] >= 0).astype(np.uint8))
+
+
+def test_20_regular_full_schedule_replica_blocks_of_32(Q, monkeypatch):
+    """c5's graph family and kernel late in the anneal: MIS on a 20-regular graph (N = 2000, S = 64) with
+    QQA_BLOCK_REPLICAS=32 -- the replica-blocked layout and k_step<4,1,0,FULL> that c5 runs -- over the
+    whole 3000-step schedule of c5, bit-exact against the contract oracle, then evaluation bit-exact."""
+    w = gen.workload("c5")
+    g = gen.random_regular(2000, 20, 5)
+    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
+    monkeypatch.setenv("QQA_BLOCK_REPLICAS", "32")
+    sol = gpu(Q, g, "mis", w.S, w.seeds[0], **hp)
+    assert sol.replica_block() == 32 and sol.step_path() == "step"
+    sol.run_linear(w.gamma_min, w.gamma_max, w.steps)
+    st = oracle.run(g, ocfg("mis", w.S, w.seeds[0], threads=os.cpu_count() or 8, **hp),
+                    oracle.schedule(w.gamma_min, w.gamma_max, w.steps))
+    assert_state_equal(sol, st)
+    assert_stats_equal(sol, st)
+    counts, energy, best = oracle.evaluate(g, "mis", w.penalty, st.theta)
+    res = sol.round_evaluate()
+    pr = res.per_replica
+    assert np.array_equal(np.stack([pr["size"], pr["violations"], pr["cut"]], 1), counts)
+    assert res.best_replica == best and res.best_energy == energy[best]
+    assert pr["violations"][best] == 0
+
+
 def test_full_schedule_c1_bit_exact(Q):
     """All 1000 steps of c1, then rounding / evaluation / best replica."""
     w = gen.workload("c1")
@@ -215,8 +264,9 @@ def test_reset_restarts_identically(Q):
     assert s1["step"] == 0 and np.array_equal(s0["theta"], s1["theta"]) and np.array_equal(s0["m"], s1["m"])
 
 
+@pytest.mark.parametrize("problem", ["mis", "maxcut", "maxclique", "maxclique_sparse", "coloring"])
 @pytest.mark.parametrize("breakit", ["asym", "unsorted", "loop", "range", "dup"])
-def test_bad_graph_rejected(Q, breakit):
+def test_bad_graph_rejected(Q, breakit, problem):
     g = gen.random_regular(50, 4, 1)
     rp, ci = g.rowptr.copy(), g.colidx.copy()
     if breakit == "asym":
@@ -230,8 +280,21 @@ def test_bad_graph_rejected(Q, breakit):
         ci[rp[7]] = 10_000
     elif breakit == "dup":
         ci[rp[2] + 1] = ci[rp[2]]
+    with pytest.raises(Q.QQAError) as e:   # every problem validates (the dense clique on the host)
+        Q.Solver(rp, ci, Q.make_config(problem, S_total=8, **({"n_colors": 4} if problem == "coloring" else {})))
+    assert e.value.status == 2
+
+
+def test_bad_clique_batch_edge_rejected(Q):
+    """Max clique on a batch: an edge joining two instances is rejected before the complement is built."""
+    g0, g1 = gen.erdos_renyi(20, 0.5, 1), gen.erdos_renyi(20, 0.5, 2)
+    g, gor = gen.disjoint_union([g0, g1])
+    u, v = g.edges()
+    u = np.append(u, 3)
+    v = np.append(v, 25)
+    bad = gen.from_edges(g.n, u, v)
     with pytest.raises(Q.QQAError) as e:
-        Q.Solver(rp, ci, Q.make_config("mis", S_total=8))
+        Q.Solver(bad.rowptr, bad.colidx, Q.make_config("maxclique", S_total=8), group_of_row=gor)
     assert e.value.status == 2
 
 

@@ -124,6 +124,24 @@ def test_fifty_steps_mis_matches_definition_c1():
     assert np.abs(st.p - D.sigmoid(th)).max() < 1e-4
 
 
+def test_fifty_steps_mis_matches_definition_20_regular():
+    """The headline graph family (c5: MIS on a random 20-regular graph, S = 64, BASELINE.json configs[4]) at
+    N = 2000: the fp32 contract against the fp64 definition (Eq. 6/7/10, App. D, AdamW P:220-222) after
+    50 steps of c5's schedule, p within north_star's 1e-4 (survey Appendix E measured 5.2e-6)."""
+    w = gen.workload("c5")
+    g = gen.random_regular(2000, 20, 5)
+    A = D.dense_adjacency(g.n, g.rowptr, g.colidx)
+    hp = {k: v for k, v in w.hparams().items() if k not in ("problem", "map", "temperature", "n_colors")}
+    cfg = oracle.make_cfg("mis", S=w.S, seed=w.seeds[0], threads=4, **hp)
+    gam = oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:50]
+    st = oracle.run(g, cfg, gam)
+    th, _, _ = D.run("mis", A, D.init_theta(g.n, w.S, w.seeds[0]), gam.astype(np.float64), alpha=w.alpha,
+                     lam=w.penalty, comm=w.comm, lr=w.lr, wd=w.weight_decay)
+    dp = np.abs(st.p - D.sigmoid(th)).max()
+    assert dp < 1e-4, dp
+    assert dp > 0.0   # two different arithmetics (fp32 contract vs fp64): the pin is not vacuous
+
+
 def test_threads_bit_identical():
     g = gen.erdos_renyi(300, 0.05, 8)
     gam = oracle.schedule(-2.0, 0.1, 40)
