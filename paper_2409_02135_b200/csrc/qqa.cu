@@ -339,6 +339,7 @@ struct qqa_handle {
   float* w_pad = nullptr;
   float* wdeg = nullptr;
   long long* wsums = nullptr;  // [S_total][2] evaluation weight sums (fixed point 2^24)
+  bool serpentine = false;     // replica blocks swept in alternating order step to step (QQA_SERPENTINE)
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
   int run_cta = 256;           // threads per CTA of k_run (1024: contiguous rows per SM)
   // fused statistics exchange over peer memory (qqa_attach_exchange; k_step_x instead of k_step + NCCL)
@@ -852,6 +853,7 @@ int do_steps_x(qqa_handle* h, const float* gamma, int64_t n_steps) {
     const int a = h->cur, b = h->cur ^ 1;
     const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
     P.var.p_cur = h->p[a]; P.var.p_next = h->p[b];
+    P.var.rev = (h->serpentine && h->s.B > 1 && (t & 1)) ? 1 : 0;
     if (h->s.n > 0) {
       const qqa::XParams X = make_xparams(h, sa, sb, sz, a, b);
       int st;
@@ -905,6 +907,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
     const int a = h->cur, b = h->cur ^ 1;
     const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
     P.var.p_cur = h->p[a]; P.var.p_next = h->p[b];
+    P.var.rev = (h->serpentine && h->s.B > 1 && (t & 1)) ? 1 : 0;
     P.ms = h->ms;
     P.colsum = h->colsum[a];
     P.var.sums_next = h->sums[sb];
@@ -1110,6 +1113,16 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     h->wdeg = (float*)(ws + L.wdeg);
   }
   h->wsums = (long long*)(ws + L.wsums);
+  if (const char* env = std::getenv("QQA_SERPENTINE")) h->serpentine = std::atoi(env) != 0;
+  if (const char* env = std::getenv("QQA_L2_PERSIST_MB")) {   // experiment: L2 set-aside for evict_last lines
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+    const size_t want = std::min<size_t>((size_t)std::atoi(env) << 20, (size_t)maxp);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) (void)cudaGetLastError();
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    std::fprintf(stderr, "qqa: persisting L2 set-aside %zu bytes (max %d)\n", got, maxp);
+  }
 
   // Graph -> device (int32 offsets). Max clique walks the complement graph.
   std::vector<int> rp32, ci_c;

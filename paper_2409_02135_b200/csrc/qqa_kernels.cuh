@@ -204,7 +204,8 @@ __device__ __forceinline__ V8 zero8() {
 
 // L2 policies (compile-time; measured in profiles/r1_design_iterations.md):
 //   QQA_GATHER_POLICY 0: gathered p rows evict_last, 1: evict_normal
-//   QQA_PNEXT_POLICY  0: p_next stored evict_normal, 1: evict_last (next step's gather source)
+//   QQA_PNEXT_POLICY  0: p_next stored evict_normal, 1: evict_last (next step's gather source),
+//                     2: evict_first (streamed like theta / m / v)
 //   QQA_INDEX_POLICY  0: CSR indices through the default path, 1: streamed (L1::no_allocate, L2 evict_first)
 #ifndef QQA_GATHER_POLICY
 #define QQA_GATHER_POLICY 0
@@ -269,6 +270,8 @@ __device__ __forceinline__ void st8(float* ptr, const V8& v) {
 __device__ __forceinline__ void st8_pnext(float* ptr, const V8& v) {
 #if QQA_PNEXT_POLICY == 1
   asm volatile("st.global.L2::evict_last.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" :: "l"(ptr), QQA_V8_IN(v) : "memory");
+#elif QQA_PNEXT_POLICY == 2
+  st8_stream(ptr, v);
 #else
   st8(ptr, v);
 #endif
@@ -289,6 +292,8 @@ struct StepVar {
   long long* sums_zero;                 // [2][n] buffer of the step after next (zeroed here), B > 1
   float kt, st, rt;                     // -2 alpha gamma_t, lr/(1-b1^t), 1/sqrt(1-b2^t) (host double -> float)
   unsigned long long nkey;              // noise key of (t, row 0): nbase + t n S_total (binary) / + offset (K-ary)
+  int rev;                              // 1: sweep the replica blocks in reverse (serpentine order over steps,
+                                        // so a step starts on the block whose p the previous step wrote last)
 };
 
 // ------------------------------------------------------------ parameters
@@ -561,11 +566,13 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
   const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
   const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
   bool bad = false;
-  for (int b = 0; b < P.B; ++b)
+  for (int bb = 0; bb < P.B; ++bb) {
+    const int b = P.var.rev ? P.B - 1 - bb : bb;
     for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
       const float2 msi = P.ms[i];
       step_item<LANES, VPL, MODE, FULL>(P, P.var, b, i, lane, gmask, msi.x, msi.y, bad);
     }
+  }
   if (bad) atomicOr(P.flag, 1);
 }
 
@@ -633,7 +640,8 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
   const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
   x_wait(X, P.flag);
   bool bad = false;
-  for (int b = 0; b < P.B; ++b)
+  for (int bb = 0; bb < P.B; ++bb) {
+    const int b = P.var.rev ? P.B - 1 - bb : bb;
     for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
       const int own = min(i / X.rows_per_rank, X.G - 1);
       const long long* sc = X.peer_cur[own];
@@ -643,6 +651,7 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
       step_item<LANES, VPL, MODE, FULL>(P, P.var, b, i, lane, gmask, mu, sd, bad, true, X.peer_next[own],
                                   (own == X.rank) ? X.zero : nullptr);
     }
+  }
   if (bad) atomicOr(P.flag, 1);
   x_signal(X);
 }
