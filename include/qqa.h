@@ -8,6 +8,7 @@
  *   p      = sigmoid(theta)                                    P:143 (north_star)
  *   q_i    = sum_{j in N(i)} p_j                               CSR gather
  *   dR/dp  = dl/dp + gamma * ds/dp - alpha_c (p - mu_i)/STD_i   Eq. 6, 7, 10
+ *            (evaluated as (p - mu_i) kc_i, kc_i = -alpha_c / STD_i once per row)
  *            MIS / max-clique-on-complement: dl/dp = -1 + lambda q
  *            Max-Cut:                        dl/dp = -deg + 2 q
  *            ds/dp = -2 alpha (2p - 1)^(alpha - 1)                     (Eq. 7)
@@ -163,28 +164,38 @@ QQA_API int qqa_version(void);                          /* QQA_ABI_VERSION      
 QQA_API const char* qqa_last_error(void);               /* thread-local message of the last failure */
 QQA_API const char* qqa_status_string(int status);
 
-/* Device bytes the workspace must have for (graph, config). Host-only. */
+/* Device bytes the workspace must have for (graph, config): the replica state theta / m / v / p x 2
+ * ([B][n+1][SB] float32), the padded CSR, the statistics and evaluation buffers.
+ * Host-only; INVALID_ARG / UNSUPPORTED as qqa_create. */
 QQA_API int qqa_workspace_bytes(const qqa_graph* g, const qqa_config* cfg, size_t* bytes);
 
-/* Validate and copy the graph, carve the workspace, initialise the replicas
- * (theta_0, m = v = 0, p_0, replica statistics). d_workspace: device pointer,
- * 256-byte aligned, >= qqa_workspace_bytes. stream: cudaStream_t (NULL = legacy
- * default stream). (sync) */
+/* Validate and copy the graph, carve the workspace, initialise the replicas: the S parallel runs
+ * of P:189-201 (Eq. 8-10), theta_0 ~ U(init_lo, init_hi) (BASELINE.json configs; the paper is silent,
+ * reading R18), m = v = 0 (Adam), p_0 = sigma(theta_0) and the replica statistics
+ * mu_i, STD_i of Eq. 10. Graph: host pointers, copied (the dense max clique builds the
+ * complement on the host). d_workspace: device pointer, 256-byte aligned,
+ * >= qqa_workspace_bytes, owned by the caller. stream: cudaStream_t (NULL = legacy default stream).
+ * Errors: INVALID_ARG (config / pointers), BAD_GRAPH (the CSR conditions above, checked on the
+ * device, or on the host for QQA_MAXCLIQUE), UNSUPPORTED (sizes), WORKSPACE, CUDA. (sync) */
 QQA_API int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg,
                void* d_workspace, size_t workspace_bytes, void* stream);
 
-/* Re-initialise the replica state from the seed (as at create); step counter 0.
- * With a communicator attached this is collective. Async. */
+/* Re-initialise the replica state from the seed (as at create: theta_0, m = v = 0, statistics of
+ * p_0); step counter 0. With a communicator attached this is collective. Async. */
 QQA_API int qqa_reset(qqa_handle* h);
 
 /* Multi-GPU (one process per GPU, replicas sharded: rank r holds
- * [replica_offset, replica_offset + S_local), S_local equal on all ranks).
+ * [replica_offset, replica_offset + S_local), S_local equal on all ranks). The S parallel runs of
+ * P:189-201 interact only through mu_i and STD_i of Eq. 10, so the only exchange is the
+ * sum of their fixed-point terms ("batch parallel computation", "additional GPUs").
  * Rank 0 calls qqa_nccl_unique_id and broadcasts the 128 bytes; every rank
  * then calls qqa_attach_comm (collective), which re-initialises the replica
  * state as qqa_reset does (theta_0 depends only on the global replica index,
  * so every sharding starts from the same ensemble). Each step then
  * all-reduces the 2n int64 statistic sums over NCCL. (sync) */
-QQA_API int qqa_nccl_unique_id(uint8_t out[128]);
+QQA_API int qqa_nccl_unique_id(uint8_t out[128]);   /* host 128 bytes out; COMM on NCCL failure        */
+/* id: rank 0's 128 bytes; requires S_total = nranks * S_local and replica_offset = rank * S_local
+ * (INVALID_ARG otherwise); the library owns the communicator. COMM on NCCL failure. (sync) */
 QQA_API int qqa_attach_comm(qqa_handle* h, const uint8_t id[128], int rank, int nranks);
 /* Use donor's communicator (same device, same rank layout) instead of creating
  * one: a handle for a new input can join a running job without another NCCL
@@ -218,8 +229,10 @@ QQA_API int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int ra
 QQA_API int qqa_loopback_sync_init(qqa_handle** hs, int G);
 QQA_API int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps);
 
-/* Run n_steps annealing steps with the given per-step gamma (host float[n_steps]).
- * The Adam step counter persists across calls. Async. */
+/* Run n_steps annealing steps (Eq. 6-10 gradient, AdamW P:220-222, sigma / Clamp map P:143 /
+ * Eq. 11) with the given per-step gamma (host float[n_steps], read during the call; P:245 the
+ * annealing of gamma). The Adam step counter persists across calls (reading R11). Non-finite values
+ * surface as NONFINITE at the next (sync) evaluation. INVALID_ARG: n_steps < 0 or gamma NULL. Async. */
 QQA_API int qqa_run(qqa_handle* h, const float* gamma_host, int64_t n_steps);
 
 /* Run steps t0..t1-1 of the linear schedule gamma_t = gmin + (gmax-gmin) t/(T-1)
@@ -248,17 +261,20 @@ QQA_API int qqa_round_evaluate_groups(qqa_handle* h, int64_t* counts, double* en
 /* Number of instances of the handle's graph (1 without group_of_row). Host-only. */
 QQA_API int qqa_n_groups(qqa_handle* h, int32_t* n_groups);
 
-/* Checkpoint / inspection: host [n][S_local] float arrays, NULL to skip.
- * p = sigmoid(theta) as used by the next step; step = Adam steps taken. (sync)
+/* Checkpoint / inspection (SURVEY.md §5 checkpoint / resume): host [n][S_local] float arrays
+ * (variable-major, replica-contiguous, caller-owned), NULL to skip. theta / m / v: the AdamW state of
+ * P:220-222; p = sigmoid(theta) as used by the next step; step = Adam steps taken. (sync)
  * QQA_COLORING: arrays are [n][S_local][K]; theta and p both receive P. */
 QQA_API int qqa_get_state(qqa_handle* h, float* theta, float* m, float* v, float* p, int64_t* step);
-/* Replica statistics of the current p: c (shift, float[n]) and the int64 sums
- * (sumD, sumD2: int64[n], already reduced over ranks). (sync)
+/* Replica statistics of the current p (Eq. 10): c (shift, float[n]) and the int64 sums
+ * (sumD, sumD2: int64[n], already reduced over ranks; fixed point 2^40 of p - c and (p - c)^2).
+ * With the fused exchange it waits for the barrier that ends the last step (COMM if a peer never
+ * arrived). (sync)
  * QQA_COLORING: per (variable, colour), arrays [n][K]. */
 QQA_API int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2);
-/* Resume from a checkpoint: theta/m/v host [n][S_local]; c = shift of the
- * statistics (float[n], NULL = 1/2); step = Adam steps taken. Collective with a
- * communicator. (sync) QQA_COLORING: theta = P, [n][S_local][K]; c [n][K] (NULL = 1/K). */
+/* Resume from a checkpoint: theta/m/v host [n][S_local] (the AdamW state of P:220-222); c = shift
+ * of the statistics (float[n], NULL = 1/2); step = Adam steps taken (reading R11). Recomputes p and
+ * the statistics of Eq. 10 from theta. Collective with a communicator. INVALID_ARG on NULL / step < 0. (sync) QQA_COLORING: theta = P, [n][S_local][K]; c [n][K] (NULL = 1/K). */
 QQA_API int qqa_set_state(qqa_handle* h, const float* theta, const float* m, const float* v,
                   const float* c, int64_t step);
 
@@ -282,7 +298,8 @@ QQA_API int qqa_step_path(qqa_handle* h, int* path);
 /* Replica block SB of the layout [B][n+1][SB] (0 for colouring). Host-only. */
 QQA_API int qqa_replica_block(qqa_handle* h, int* SB);
 
-/* Free the handle (and its communicator); the workspace is not freed. (sync) */
+/* Free the handle (and its communicator when no other handle shares it); the workspace is the
+ * caller's and is not freed. NULL is OK. (sync) */
 QQA_API int qqa_destroy(qqa_handle* h);
 
 #ifdef __cplusplus

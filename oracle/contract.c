@@ -44,6 +44,9 @@
  *     (oc_exp_neg), p = 1/(1+E) for theta >= 0 else E/(1+E);
  *   - cross-replica stats as exact int64 fixed-point sums (scale 2^40) of
  *     d = p - c_i and fl(d*d), c_i = the previous step's mean (1/2 at init);
+ *   - binary gradient: g_p = fma(p - mu_i, kc_i, fma(k_t, (2p-1)^(alpha-1), obj)) with the
+ *     row's communication coefficient kc_i = fl(-a_c / STD_i) (0 if STD_i < 1e-6), one
+ *     division per row (round 2; the K-ary rows keep -a_c ((p - mu) / STD) per element);
  *   - per-step scalars computed in double on the host, rounded to fp32.
  * The contract is pinned against the fp64 definition (oracle/definition.py)
  * in tests/test_oracle_contract.py.
@@ -320,6 +323,9 @@ static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, co
 
     float mu, sd;
     finalize_stats(c_i, sD_i, sD2_i, S, &mu, &sd);
+    /* Eq. 10 gradient -alpha_c (p - mu) / STD as (p - mu) kc with the row's kc = -alpha_c / STD
+     * (one division per row; 0 if STD < 1e-6, reading R6) */
+    const float kc = (sd >= 1e-6f) ? (-ac) / sd : 0.0f;
 
     /* q_i^s = sum_{j in N(i)} p_j^s, ascending CSR order */
     for (int32_t s = 0; s < S; ++s) q[s] = 0.0f;
@@ -343,8 +349,7 @@ static int update_row(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, co
         const float obj = (cf->problem == OC_MAXCUT) ? fmaf(2.0f, q[s], -degf)
                           : (cf->problem == OC_MAXCLIQUE_SPARSE) ? fmaf(lam, (Tcol[s] - 0.5f) - q[s], -1.0f)
                           : fmaf(lam, q[s], -1.0f);
-        const float com = (sd >= 1e-6f) ? (-ac) * ((pi - mu) / sd) : 0.0f;
-        const float gp = fmaf(kt, ep, obj) + com;         /* (obj + entropy) + comm */
+        const float gp = fmaf(pi - mu, kc, fmaf(kt, ep, obj));   /* (obj + entropy) + comm, fused */
         /* sigmoid: chain rule dR/dtheta = dR/dp p (1-p); clamp: the parameter is p */
         const float g = clamp ? gp : gp * (pi * (1.0f - pi));
         /* AdamW */

@@ -24,10 +24,13 @@
 // (VPL 8-vectors per lane when SB > 256).
 //
 // Arithmetic: the fp32 contract of DESIGN.md §3. Every contract operation is
-// written with an explicit round-to-nearest intrinsic (__fadd_rn, __fmul_rn,
-// ...), which nvcc never contracts into FMA, and the file is compiled with
-// -fmad=false as a second guard. Adding a padding entry adds +0.0f to a sum
-// that is never -0.0f (p >= 0, q starts at +0), which leaves it unchanged.
+// written with an explicit round-to-nearest intrinsic: separate roundings as
+// __fadd_rn / __fmul_rn / __fdiv_rn (which nvcc never contracts into an FMA; the
+// file is also compiled with -fmad=false), and the multiply-adds the contract
+// fuses as explicit __fmaf_rn (one rounding, C's fmaf on the oracle side: the
+// exp / ln / cos Horner steps, the gradient, AdamW and the noise add). Adding a
+// padding entry adds +0.0f to a sum that is never -0.0f (p >= 0, q starts at
+// +0), which leaves it unchanged.
 #pragma once
 #include <cstdint>
 #include <cooperative_groups.h>
@@ -325,11 +328,15 @@ struct StepParams {
 // the map for one element. MODE bit 0: clamp (the parameter th is p itself, no
 // chain factor, p = Clamp(th)); otherwise p = sigmoid(th). Returns p_next; bad
 // is set when the pre-map parameter is non-finite.
+// The communication coefficient of a row, kc_i = -alpha_c / STD_i (0 if STD_i < 1e-6, reading R6): computed
+// once per row (one division), so the per-element term of Eq. 10 is one fused multiply-add.
+__device__ __forceinline__ float comm_coef(float comm, float sd) { return (sd >= 1e-6f) ? fdiv(-comm, sd) : 0.0f; }
+
 template <int MODE>
 __device__ __forceinline__ float update_element(const StepParams& P, const StepVar& V, float q, float aux,
-                                                float pi, float mu, float sd, float& th, float& mm, float& vv,
+                                                float pi, float mu, float kc, float& th, float& mm, float& vv,
                                                 float xi, bool& bad) {
-  const float e = fsub(fmul(2.0f, pi), 1.0f);
+  const float e = __fmaf_rn(2.0f, pi, -1.0f);                         // 2p - 1 (2p is exact: = fl(fl(2p) - 1))
   float ep = e;
   for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);                 // (2p-1)^(alpha-1)
   // __fmaf_rn(a, b, c) = one fused multiply-add (one rounding), C's fmaf
@@ -337,8 +344,8 @@ __device__ __forceinline__ float update_element(const StepParams& P, const StepV
   const float obj = (MODE & kModeSparseClique) ? __fmaf_rn(P.lam, fsub(fsub(aux, 0.5f), q), -1.0f)
                     : (P.problem == kMAXCUT) ? __fmaf_rn(2.0f, q, -aux)                   // -deg + 2q
                                              : __fmaf_rn(P.lam, q, -1.0f);                // -1 + lambda q
-  const float com = (sd >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, mu), sd)) : 0.0f;
-  const float gp = fadd(__fmaf_rn(V.kt, ep, obj), com);              // (obj - 2 alpha gamma (2p-1)^(alpha-1)) + comm
+  // (obj - 2 alpha gamma (2p-1)^(alpha-1)) + (p - mu) kc: entropy and communication terms fused
+  const float gp = __fmaf_rn(fsub(pi, mu), kc, __fmaf_rn(V.kt, ep, obj));
   const float g = (MODE & kModeClamp) ? gp                             // sensitive transition: d/dp
                                       : fmul(gp, fmul(pi, fsub(1.0f, pi)));  // chain rule through sigmoid
   const float t1 = fmul(th, P.at);                                    // decoupled weight decay
@@ -499,6 +506,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
                                                   : (float)(__ldg(P.rowptr + i + 1) - __ldg(P.rowptr + i));
 
       // ---- gradient, AdamW, (noise), map, statistics of p_next
+      const float kc = comm_coef(P.comm, sd);   // once per item: -alpha_c / STD_i
       long long sD = 0, sD2 = 0;
       const unsigned long long rkey = V.nkey + (unsigned long long)i * P.S_total_u;  // noise key of (t, i, replica 0)
 #pragma unroll
@@ -525,10 +533,10 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
           for (int k = 0; k < 8; k += 2) {            // a replica pair shares one noise hash (cos / sin halves)
             float z0 = 0.0f, z1 = 0.0f;
             if (MODE & kModeNoise) gauss_pair_c(mix64(rkey + (unsigned long long)(P.off + s0 + k)), z0, z1);
-            pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, sd, th.f[k],
+            pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, kc, th.f[k],
                                            mm.f[k], vv.f[k], z0, bad);
             pn.f[k + 1] = update_element<MODE>(P, V, acc[w].f[k + 1], aux_of<MODE>(P, degf, s0 + k + 1), pp.f[k + 1],
-                                               mu, sd, th.f[k + 1], mm.f[k + 1], vv.f[k + 1], z1, bad);
+                                               mu, kc, th.f[k + 1], mm.f[k + 1], vv.f[k + 1], z1, bad);
             long long D, D2;
             stat_terms(pn.f[k], mu, D, D2);
             sD += D; sD2 += D2;
@@ -540,7 +548,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
           for (int k = 0; k < 8; ++k) {
             if (s0 + k < P.S_local) {
               const float z = (MODE & kModeNoise) ? noise_of(rkey, P.off + s0 + k) : 0.0f;
-              pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, sd, th.f[k],
+              pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, kc, th.f[k],
                                              mm.f[k], vv.f[k], z, bad);
               long long D, D2;
               stat_terms(pn.f[k], mu, D, D2);
@@ -788,7 +796,7 @@ __global__ void __launch_bounds__(1024, 1) k_run_cluster(const RunParams R) {
     for (int r = tid; r < nr; r += nt) {   // (mu_i, STD_i) of the current p; shift of the next sums
       float mu, sd;
       finalize_stats(sc[r], scur[r], scur[RC + r], R.S_total, mu, sd);
-      sms[r] = make_float2(mu, sd);
+      sms[r] = make_float2(mu, comm_coef(P.comm, sd));   // (mu_i, kc_i)
       sc[r] = mu;
       snext[r] = 0;
       snext[RC + r] = 0;
