@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define QQA_ABI_VERSION 6
+#define QQA_ABI_VERSION 7
 
 #if defined(__GNUC__)
 #define QQA_API __attribute__((visibility("default")))
@@ -228,6 +228,15 @@ QQA_API int qqa_exchange_bytes(qqa_handle* h, size_t* bytes);
 QQA_API int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks);
 QQA_API int qqa_loopback_sync_init(qqa_handle** hs, int G);
 QQA_API int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps);
+/* Concurrent one-GPU emulation of the fused exchange (test of its barrier / atomics protocol; DESIGN.md
+ * §6): hs[r] = shard r of G (1..8) with qqa_attach_exchange done as rank r of G on one device and stream
+ * (buffers on that device), in lockstep after qqa_loopback_sync_init. Runs n_steps steps (gamma_host
+ * float[n_steps]) of all G ranks as ONE cooperative launch whose grid is G slices of co-resident CTAs,
+ * slice r executing rank r's k_step_x body: the ranks really run at the same time and wait on each
+ * other's arrivals (B200_PROFILING.md: ranks that wait on one another must not be separate launches on
+ * one GPU). Same results as the per-step k_step_x launches. INVALID_ARG if the shards are not such a
+ * set, UNSUPPORTED for layouts without an emulation kernel (lanes > 8 or vpl > 1). (sync) */
+QQA_API int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps);
 
 /* Run n_steps annealing steps (Eq. 6-10 gradient, AdamW P:220-222, sigma / Clamp map P:143 /
  * Eq. 11) with the given per-step gamma (host float[n_steps], read during the call; P:245 the

@@ -823,12 +823,9 @@ int do_steps_cluster(qqa_handle* h, const float* gamma, int64_t n_steps) {
   return QQA_OK;
 }
 
-// Fused-exchange steps: one k_step_x launch per step (it waits for the previous step's barrier,
-// finalizes from the owners' sums, adds into the owners' next sums and arrives); no NCCL, no k_finalize.
-int do_steps_x(qqa_handle* h, const float* gamma, int64_t n_steps) {
+// Step-invariant parameters of the fused-exchange step (k_step_x and its one-GPU emulation).
+qqa::StepParams xstep_base(const qqa_handle* h) {
   const qqa_config& c = h->cfg;
-  const qqa::XStepKernel kx = pick_xstep(h->s.lanes, h->s.vpl, step_mode(c, h->s.weighted), full_lanes(h->s));
-  if (!kx) return fail(QQA_ERR_UNSUPPORTED, "no fused-exchange kernel for this mode");
   qqa::StepParams P{};
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
@@ -843,17 +840,36 @@ int do_steps_x(qqa_handle* h, const float* gamma, int64_t n_steps) {
   P.at = (float)(1.0 - (double)c.lr * (double)c.weight_decay);
   P.ns = (float)std::sqrt(2.0 * (double)c.lr * (double)c.temperature);
   P.S_total_u = (unsigned long long)h->s.S_total;
-  const uint64_t nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);
+  return P;
+}
+
+// The per-step part of the fused-exchange step t = h->step + 1 (buffers a -> b, scalars of gamma).
+qqa::StepVar xstep_var(const qqa_handle* h, float gamma) {
+  const qqa_config& c = h->cfg;
+  const int64_t t = h->step + 1;
+  qqa::StepVar V{};
+  V.nkey = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull) + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total;
+  V.kt = (float)(-2.0 * (double)c.alpha * (double)gamma);
+  V.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
+  V.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
+  V.p_cur = h->p[h->cur];
+  V.p_next = h->p[h->cur ^ 1];
+  V.rev = (h->serpentine && h->s.B > 1 && (t & 1)) ? 1 : 0;
+  return V;
+}
+
+// Fused-exchange steps: one k_step_x launch per step (it waits for the previous step's barrier,
+// finalizes from the owners' sums, adds into the owners' next sums and arrives); no NCCL, no k_finalize.
+int do_steps_x(qqa_handle* h, const float* gamma, int64_t n_steps) {
+  const qqa_config& c = h->cfg;
+  const qqa::XStepKernel kx = pick_xstep(h->s.lanes, h->s.vpl, step_mode(c, h->s.weighted), full_lanes(h->s));
+  if (!kx) return fail(QQA_ERR_UNSUPPORTED, "no fused-exchange kernel for this mode");
+  qqa::StepParams P = xstep_base(h);
   for (int64_t k = 0; k < n_steps; ++k) {
     const int64_t t = h->step + 1;
-    P.var.nkey = nbase + (uint64_t)t * (uint64_t)h->s.n * (uint64_t)h->s.S_total;
-    P.var.kt = (float)(-2.0 * (double)c.alpha * (double)gamma[k]);
-    P.var.st = (float)((double)c.lr / (1.0 - std::pow((double)c.beta1, (double)t)));
-    P.var.rt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)c.beta2, (double)t)));
+    P.var = xstep_var(h, gamma[k]);
     const int a = h->cur, b = h->cur ^ 1;
     const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
-    P.var.p_cur = h->p[a]; P.var.p_next = h->p[b];
-    P.var.rev = (h->serpentine && h->s.B > 1 && (t & 1)) ? 1 : 0;
     if (h->s.n > 0) {
       const qqa::XParams X = make_xparams(h, sa, sb, sz, a, b);
       int st;
@@ -1418,6 +1434,74 @@ int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_
     if (!hs[0]->xmode && (st = loopback_reduce(hs, G))) return st;   // fused shards exchanged in-kernel
   }
   QQA_CUDA(cudaStreamSynchronize(hs[0]->stream));
+  return QQA_OK;
+}
+
+int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps) {
+  NvtxRange nvtx("qqa_exchange_emulate");
+  if (!hs || G < 1 || G > qqa::kMaxRanks) return fail(QQA_ERR_INVALID_ARG, "handles is NULL or G not in 1..8");
+  if (n_steps < 0 || (n_steps > 0 && !gamma_host)) return fail(QQA_ERR_INVALID_ARG, "bad n_steps or gamma NULL");
+  for (int r = 0; r < G; ++r) {
+    const qqa_handle* h = hs[r];
+    if (!h) return fail(QQA_ERR_INVALID_ARG, "a handle is NULL");
+    if (!h->xmode || h->xG != G || h->xrank != r)
+      return fail(QQA_ERR_INVALID_ARG, "every shard r must have the fused exchange attached as rank r of G");
+    if (h->device != hs[0]->device || h->stream != hs[0]->stream || h->s.n != hs[0]->s.n ||
+        h->s.lanes != hs[0]->s.lanes || h->s.vpl != hs[0]->s.vpl || h->s.SB != hs[0]->s.SB ||
+        step_mode(h->cfg, h->s.weighted) != step_mode(hs[0]->cfg, hs[0]->s.weighted) || h->step != hs[0]->step ||
+        h->cur != hs[0]->cur || h->scur != hs[0]->scur || h->xsync != hs[0]->xsync)
+      return fail(QQA_ERR_INVALID_ARG, "emulated shards must share device, stream, layout, mode and be in lockstep");
+  }
+  qqa_handle* h0 = hs[0];
+  int st = set_device(h0);
+  if (st) return st;
+  if (n_steps == 0 || h0->s.n == 0) return QQA_OK;
+  const qqa::XEmulKernel ke = qqa::xemul_kernel(h0->s.lanes, h0->s.vpl, step_mode(h0->cfg, h0->s.weighted),
+                                                full_lanes(h0->s));
+  if (!ke) return fail(QQA_ERR_UNSUPPORTED, "no emulation kernel for this layout / mode");
+  // the per-(step, rank) parameters exactly as do_steps_x would launch them, step by step
+  std::vector<qqa::StepParams> base((size_t)G);
+  std::vector<qqa::StepVar> var((size_t)n_steps * G);
+  std::vector<qqa::XParams> xp((size_t)n_steps * G);
+  for (int r = 0; r < G; ++r) base[r] = xstep_base(hs[r]);
+  for (int64_t k = 0; k < n_steps; ++k)
+    for (int r = 0; r < G; ++r) {
+      qqa_handle* h = hs[r];
+      const int a = h->cur, b = h->cur ^ 1;
+      const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
+      var[(size_t)k * G + r] = xstep_var(h, gamma_host[k]);
+      xp[(size_t)k * G + r] = make_xparams(h, sa, sb, sz, a, b);
+      h->xsync++;
+      h->cur = b;
+      h->scur = sb;
+      h->step += 1;
+      h->launches++;
+    }
+  const size_t nb = base.size() * sizeof(qqa::StepParams), nv = var.size() * sizeof(qqa::StepVar),
+               nx = xp.size() * sizeof(qqa::XParams);
+  char* d = nullptr;
+  QQA_CUDA(cudaMalloc(&d, nb + nv + nx + 512));
+  struct Free { char* p; ~Free() { cudaFree(p); } } guard{d};
+  char* db = d;
+  char* dv = d + up(nb, 256);
+  char* dx = dv + up(nv, 256);
+  QQA_CUDA(cudaMemcpyAsync(db, base.data(), nb, cudaMemcpyHostToDevice, h0->stream));
+  QQA_CUDA(cudaMemcpyAsync(dv, var.data(), nv, cudaMemcpyHostToDevice, h0->stream));
+  QQA_CUDA(cudaMemcpyAsync(dx, xp.data(), nx, cudaMemcpyHostToDevice, h0->stream));
+  int per_sm = 0;
+  QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)ke, 256, 0));
+  const int cta_per_rank = std::max(1, per_sm * h0->sm_count / G);
+  if ((int64_t)per_sm * h0->sm_count < G) return fail(QQA_ERR_UNSUPPORTED, "too few co-resident CTAs for G ranks");
+  qqa::XEmulParams E{};
+  E.base = reinterpret_cast<const qqa::StepParams*>(db);
+  E.var = reinterpret_cast<const qqa::StepVar*>(dv);
+  E.xp = reinterpret_cast<const qqa::XParams*>(dx);
+  E.G = G;
+  E.nsteps = (int)n_steps;
+  E.cta_per_rank = cta_per_rank;
+  void* args[] = {(void*)&E};
+  QQA_CUDA(cudaLaunchCooperativeKernel((const void*)ke, dim3(G * cta_per_rank), dim3(256), args, 0, h0->stream));
+  QQA_CUDA(cudaStreamSynchronize(h0->stream));
   return QQA_OK;
 }
 

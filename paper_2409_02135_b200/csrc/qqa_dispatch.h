@@ -45,6 +45,11 @@ XStepKernel xstep_kernel_m1(int lanes, int vpl, bool full);
 XStepKernel xstep_kernel_m2(int lanes, int vpl, bool full);
 XStepKernel xstep_kernel_m3(int lanes, int vpl, bool full);
 
+// k_step_x_emul<lanes, 1, MODE> (one-GPU concurrent emulation of the fused exchange, k_xemul.cu):
+// lanes 1..8, vpl 1, MODE 0..3; nullptr otherwise.
+using XEmulKernel = void (*)(const XEmulParams);
+XEmulKernel xemul_kernel(int lanes, int vpl, int mode, bool full);
+
 // k_run_cluster<MODE> (MODE 0..3, compiled in k_cluster.cu); nullptr otherwise.
 RunKernel cluster_kernel(int mode);
 

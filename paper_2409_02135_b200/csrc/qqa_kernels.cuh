@@ -27,7 +27,7 @@
 // written with an explicit round-to-nearest intrinsic: separate roundings as
 // __fadd_rn / __fmul_rn / __fdiv_rn (which nvcc never contracts into an FMA; the
 // file is also compiled with -fmad=false), and the multiply-adds the contract
-// fuses as explicit __fmaf_rn (one rounding, C's fmaf on the oracle side: the
+// fuses as explicit __fmaf_rn (one rounding, C's fmaf in DESIGN.md §3: the
 // exp / ln / cos Horner steps, the gradient, AdamW and the noise add). Adding a
 // padding entry adds +0.0f to a sum that is never -0.0f (p >= 0, q starts at
 // +0), which leaves it unchanged.
@@ -206,10 +206,12 @@ __device__ __forceinline__ V8 zero8() {
                      "f"(v.f[4]), "f"(v.f[5]), "f"(v.f[6]), "f"(v.f[7])
 
 // L2 policies (compile-time; measured in profiles/r1_design_iterations.md):
-//   QQA_GATHER_POLICY 0: gathered p rows evict_last, 1: evict_normal
+//   QQA_GATHER_POLICY 0: gathered p rows evict_last, 1: evict_normal, 2: evict_last + L1::no_allocate,
+//                     3: ld.global.cg (L2 only) evict_last
 //   QQA_PNEXT_POLICY  0: p_next stored evict_normal, 1: evict_last (next step's gather source),
 //                     2: evict_first (streamed like theta / m / v)
-//   QQA_INDEX_POLICY  0: CSR indices through the default path, 1: streamed (L1::no_allocate, L2 evict_first)
+//   QQA_INDEX_POLICY  0: CSR indices through the default path, 1: streamed (L1::no_allocate, L2 evict_first),
+//                     2: L1-allocating, L2 evict_first
 #ifndef QQA_GATHER_POLICY
 #define QQA_GATHER_POLICY 0
 #endif
@@ -236,6 +238,11 @@ __device__ __forceinline__ V8 ld8_gather(const float* ptr) {
   V8 r;
 #if QQA_GATHER_POLICY == 1
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : QQA_V8_OUT(r) : "l"(ptr));
+#elif QQA_GATHER_POLICY == 2
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : QQA_V8_OUT(r) : "l"(ptr));
+#elif QQA_GATHER_POLICY == 3
+  asm volatile("ld.global.cg.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : QQA_V8_OUT(r) : "l"(ptr));
 #else
   asm volatile("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : QQA_V8_OUT(r) : "l"(ptr));
@@ -249,6 +256,12 @@ __device__ __forceinline__ int4 ld_idx4(const int* ptr) {
   int4 r;   // evict-first policy via an L2 cache hint (the qualifier form needs 256-bit accesses)
   asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
                " ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], pol;\n}"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
+  return r;
+#elif QQA_INDEX_POLICY == 2
+  int4 r;   // L2 evict_first (the CSR streams through L2 once per replica block) but L1-allocating
+  asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+               " ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], pol;\n}"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
   return r;
 #else
@@ -332,8 +345,10 @@ struct StepParams {
 // once per row (one division), so the per-element term of Eq. 10 is one fused multiply-add.
 __device__ __forceinline__ float comm_coef(float comm, float sd) { return (sd >= 1e-6f) ? fdiv(-comm, sd) : 0.0f; }
 
+// aux: the constant term of the objective gradient, -1 (MIS / clique-on-complement) or -deg_i (Max-Cut),
+// with ok = lambda or 2 (obj_coefs); the replica's column sum T (printed clique relaxation).
 template <int MODE>
-__device__ __forceinline__ float update_element(const StepParams& P, const StepVar& V, float q, float aux,
+__device__ __forceinline__ float update_element(const StepParams& P, const StepVar& V, float q, float ok, float aux,
                                                 float pi, float mu, float kc, float& th, float& mm, float& vv,
                                                 float xi, bool& bad) {
   const float e = __fmaf_rn(2.0f, pi, -1.0f);                         // 2p - 1 (2p is exact: = fl(fl(2p) - 1))
@@ -341,9 +356,10 @@ __device__ __forceinline__ float update_element(const StepParams& P, const StepV
   for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);                 // (2p-1)^(alpha-1)
   // __fmaf_rn(a, b, c) = one fused multiply-add (one rounding), C's fmaf
   // aux: the degree (Max-Cut) or the replica's column sum T (printed clique relaxation)
+  // MIS / clique-on-complement: fma(lambda, q, -1); Max-Cut: fma(2, q, -deg) -- the operands (ok, oc) are
+  // selected once per item by the caller (obj_coefs), the same single rounding either way
   const float obj = (MODE & kModeSparseClique) ? __fmaf_rn(P.lam, fsub(fsub(aux, 0.5f), q), -1.0f)
-                    : (P.problem == kMAXCUT) ? __fmaf_rn(2.0f, q, -aux)                   // -deg + 2q
-                                             : __fmaf_rn(P.lam, q, -1.0f);                // -1 + lambda q
+                                               : __fmaf_rn(ok, q, aux);
   // (obj - 2 alpha gamma (2p-1)^(alpha-1)) + (p - mu) kc: entropy and communication terms fused
   const float gp = __fmaf_rn(fsub(pi, mu), kc, __fmaf_rn(V.kt, ep, obj));
   const float g = (MODE & kModeClamp) ? gp                             // sensitive transition: d/dp
@@ -363,12 +379,19 @@ __device__ __forceinline__ float update_element(const StepParams& P, const StepV
   return sigmoid_c(w);
 }
 
-// Per-element extra input of the objective: the variable's degree (Max-Cut), or the replica's column
-// sum T_s = (float)((double)C_s 2^-40) of the printed clique relaxation.
+// Per-element constant term of the objective gradient: oc (-1, or -deg_i for Max-Cut), or the replica's
+// column sum T_s = (float)((double)C_s 2^-40) of the printed clique relaxation.
 template <int MODE>
-__device__ __forceinline__ float aux_of(const StepParams& P, float degf, int s) {
-  if (!(MODE & kModeSparseClique)) return degf;
+__device__ __forceinline__ float aux_of(const StepParams& P, float oc, int s) {
+  if (!(MODE & kModeSparseClique)) return oc;
   return __double2float_rn(__dmul_rn(__ll2double_rn(__ldg(P.colsum + s)), 0x1p-40));
+}
+
+// (ok, oc) of obj = fma(ok, q, oc): (lambda, -1) for MIS / clique-on-complement, (2, -deg_i) for Max-Cut.
+__device__ __forceinline__ void obj_coefs(const StepParams& P, float degf, float& ok, float& oc) {
+  const bool cut = P.problem == kMAXCUT;
+  ok = cut ? 2.0f : P.lam;
+  oc = cut ? -degf : -1.0f;
 }
 
 // Reduce the group's fixed-point partial sums and publish them for variable i.
@@ -507,6 +530,8 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 
       // ---- gradient, AdamW, (noise), map, statistics of p_next
       const float kc = comm_coef(P.comm, sd);   // once per item: -alpha_c / STD_i
+      float ok, oc;
+      obj_coefs(P, degf, ok, oc);
       long long sD = 0, sD2 = 0;
       const unsigned long long rkey = V.nkey + (unsigned long long)i * P.S_total_u;  // noise key of (t, i, replica 0)
 #pragma unroll
@@ -533,10 +558,10 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
           for (int k = 0; k < 8; k += 2) {            // a replica pair shares one noise hash (cos / sin halves)
             float z0 = 0.0f, z1 = 0.0f;
             if (MODE & kModeNoise) gauss_pair_c(mix64(rkey + (unsigned long long)(P.off + s0 + k)), z0, z1);
-            pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, kc, th.f[k],
-                                           mm.f[k], vv.f[k], z0, bad);
-            pn.f[k + 1] = update_element<MODE>(P, V, acc[w].f[k + 1], aux_of<MODE>(P, degf, s0 + k + 1), pp.f[k + 1],
-                                               mu, kc, th.f[k + 1], mm.f[k + 1], vv.f[k + 1], z1, bad);
+            pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], ok, aux_of<MODE>(P, oc, s0 + k), pp.f[k], mu, kc,
+                                           th.f[k], mm.f[k], vv.f[k], z0, bad);
+            pn.f[k + 1] = update_element<MODE>(P, V, acc[w].f[k + 1], ok, aux_of<MODE>(P, oc, s0 + k + 1),
+                                               pp.f[k + 1], mu, kc, th.f[k + 1], mm.f[k + 1], vv.f[k + 1], z1, bad);
             long long D, D2;
             stat_terms(pn.f[k], mu, D, D2);
             sD += D; sD2 += D2;
@@ -548,8 +573,8 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
           for (int k = 0; k < 8; ++k) {
             if (s0 + k < P.S_local) {
               const float z = (MODE & kModeNoise) ? noise_of(rkey, P.off + s0 + k) : 0.0f;
-              pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], aux_of<MODE>(P, degf, s0 + k), pp.f[k], mu, kc, th.f[k],
-                                             mm.f[k], vv.f[k], z, bad);
+              pn.f[k] = update_element<MODE>(P, V, acc[w].f[k], ok, aux_of<MODE>(P, oc, s0 + k), pp.f[k], mu, kc,
+                                             th.f[k], mm.f[k], vv.f[k], z, bad);
               long long D, D2;
               stat_terms(pn.f[k], mu, D, D2);
               sD += D; sD2 += D2;
@@ -627,25 +652,27 @@ __device__ __forceinline__ void x_arrive_all(const XParams& X) {
     asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(X.peer_flag[r]) : "memory");
 }
 
-// The last CTA of the launch (ticket) releases this rank's arrival into every rank's counter.
-__device__ __forceinline__ void x_signal(const XParams& X) {
+// The last of the rank's ncta CTAs (ticket) releases this rank's arrival into every rank's counter.
+__device__ __forceinline__ void x_signal(const XParams& X, unsigned ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();   // this CTA's peer additions, ordered before the ticket
     const unsigned t = atomicAdd(X.ticket, 1u);
-    if (t == gridDim.x - 1) {
+    if (t == ncta - 1) {
       *X.ticket = 0;
       x_arrive_all(X);
     }
   }
 }
 
+// One step of one rank with the fused exchange, run by the rank's CTAs cta = 0..ncta-1 (a k_step_x
+// launch: blockIdx.x of gridDim.x; the one-GPU emulation k_step_x_emul: a slice of one cooperative grid).
 template <int LANES, int VPL, int MODE, bool FULL>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
+__device__ __forceinline__ void step_x_body(const StepParams& P, const XParams& X, int cta, int ncta) {
   const int lane = threadIdx.x & (LANES - 1);
   const unsigned gmask = group_mask<LANES>();
-  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
-  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  const int group = (int)((cta * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((ncta * blockDim.x) / LANES);
   x_wait(X, P.flag);
   bool bad = false;
   for (int bb = 0; bb < P.B; ++bb) {
@@ -661,7 +688,38 @@ __global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_s
     }
   }
   if (bad) atomicOr(P.flag, 1);
-  x_signal(X);
+  x_signal(X, (unsigned)ncta);
+}
+
+template <int LANES, int VPL, int MODE, bool FULL>
+__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
+  step_x_body<LANES, VPL, MODE, FULL>(P, X, (int)blockIdx.x, (int)gridDim.x);
+}
+
+// One-GPU emulation of G ranks running the fused exchange CONCURRENTLY (test of the barrier / atomics
+// protocol, qqa_exchange_emulate): one cooperative launch whose grid is G slices of cta_per_rank CTAs;
+// slice r runs rank r's k_step_x body for steps 0..nsteps-1 with its own parameters, so ranks really
+// wait on one another's arrivals (all CTAs are co-resident). Per (step j, rank r): P = base[r] with
+// var = var[j G + r], X = xp[j G + r]. The gathered p rows and peer sums of step j were written by other
+// CTAs during step j-1 of this same launch; x_wait's acquire load invalidates the SM's L1 (SASS
+// CCTL.IVALL) before any of them is read, as the grid barrier of the persistent k_run does.
+struct XEmulParams {
+  const StepParams* base;   // [G]
+  const StepVar* var;       // [nsteps][G]
+  const XParams* xp;        // [nsteps][G]
+  int G, nsteps, cta_per_rank;
+};
+
+template <int LANES, int VPL, int MODE, bool FULL>
+__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step_x_emul(const XEmulParams E) {
+  const int r = (int)blockIdx.x / E.cta_per_rank, cta = (int)blockIdx.x % E.cta_per_rank;
+  if (r >= E.G) return;
+  for (int j = 0; j < E.nsteps; ++j) {
+    StepParams P = E.base[r];
+    P.var = E.var[(size_t)j * E.G + r];
+    const XParams X = E.xp[(size_t)j * E.G + r];
+    step_x_body<LANES, VPL, MODE, FULL>(P, X, cta, E.cta_per_rank);
+  }
 }
 
 #ifndef QQA_INST_ONLY
@@ -831,7 +889,9 @@ __global__ void __launch_bounds__(1024, 1) k_run_cluster(const RunParams R) {
         float th = sth[at], mm = smm[at], vv = svv[at];
         const float pi = (MODE & kModeClamp) ? th : pc[at];
         const float2 st = sms[r];
-        const float pv = update_element<MODE>(P, V, q, degf, pi, st.x, st.y, th, mm, vv, z, bad);
+        float ok, oc;
+        obj_coefs(P, degf, ok, oc);
+        const float pv = update_element<MODE>(P, V, q, ok, oc, pi, st.x, st.y, th, mm, vv, z, bad);
         sth[at] = th; smm[at] = mm; svv[at] = vv; pn[at] = pv;
         stat_terms(pv, st.x, D, D2);
       }

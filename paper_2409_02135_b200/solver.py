@@ -263,3 +263,11 @@ def loopback_run(shards, gammas) -> None:
     step (the NCCL all-reduce of a real G-GPU run, emulated on one device)."""
     g = np.ascontiguousarray(gammas, np.float32)
     check(lib.qqa_loopback_run(_handles(shards), len(shards), g.ctypes.data, len(g)))
+
+
+def exchange_emulate(shards, gammas) -> None:
+    """Run G fused-exchange shard solvers (attached as ranks 0..G-1 on one device) CONCURRENTLY for
+    len(gammas) steps: one cooperative launch, G slices of co-resident CTAs waiting on each other's
+    barrier arrivals (qqa_exchange_emulate; tests of the exchange protocol)."""
+    g = np.ascontiguousarray(gammas, np.float32)
+    check(lib.qqa_exchange_emulate(_handles(shards), len(shards), g.ctypes.data, len(g)))

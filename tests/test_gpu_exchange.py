@@ -6,7 +6,8 @@ in the same buffers. On one device the G ranks are G shard handles on one stream
 (rank 0..G-1 for step t, then step t+1), so no kernel ever waits for a kernel queued behind it; the
 peer "memory" is the other handles' buffers on the same GPU. The shards must reproduce the handle
 holding every replica bit for bit, and the one-rank NCCL path. A rank that never arrives must be
-reported, not hang.
+reported, not hang. The concurrent tests run all G ranks at the same time in one cooperative launch
+(qqa_exchange_emulate), so the barrier and the remote atomics are exercised under real concurrency.
 """
 import numpy as np
 import pytest
@@ -75,6 +76,74 @@ def test_fused_exchange_shards_reproduce_the_full_ensemble(Q, monkeypatch, case)
         pr = sh.round_evaluate().per_replica
         for f in ("size", "violations", "cut", "energy"):
             assert np.array_equal(pr[f], fr[f][r * S_l:(r + 1) * S_l]), (r, f)
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_fused_exchange_concurrent_ranks_reproduce_the_full_ensemble(Q, monkeypatch, case):
+    """The same shards, but the G ranks run CONCURRENTLY: one cooperative launch (qqa_exchange_emulate) whose
+    grid is G slices of co-resident CTAs, so every rank's step really waits on the other ranks' arrivals
+    (red.release.sys / ld.acquire.sys barrier) and their remote atomics race with its own -- the multi-GPU
+    protocol under real concurrency on one device. Bit-exact against the handle holding all replicas."""
+    problem, G, S_l, hp, sb = CASES[case]
+    if sb:
+        monkeypatch.setenv("QQA_BLOCK_REPLICAS", sb)
+    g = gen.erdos_renyi(120, 0.5, 7) if problem == "maxclique" else gen.erdos_renyi(501, 0.03, 40 + case)
+    S = G * S_l
+    gam = oracle.schedule(-5.0 if problem == "maxcut" else -2.0, 0.1, 400)[:60]
+    full = Q.Solver(g.rowptr, g.colidx, Q.make_config(problem, S_total=S, seed=9, **hp))
+    full.run(gam)
+    shards = [Q.Solver(g.rowptr, g.colidx, Q.make_config(problem, S_total=S, seed=9, replica_offset=r * S_l,
+                                                         S_local=S_l, **hp)) for r in range(G)]
+    bufs, ptrs = exchange_buffers(shards)
+    for r, sh in enumerate(shards):
+        sh.attach_exchange(ptrs, r, G, keep=bufs)
+    Q.loopback_sync_init(shards)
+    Q.exchange_emulate(shards, gam[:35])     # concurrent ranks, 35 steps in one launch
+    for t in range(35, 60):                  # then the production per-step launches continue from there
+        for sh in shards:
+            sh.run(gam[t:t + 1])
+    fs, fst = full.get_state(), full.get_stats()
+    for r, sh in enumerate(shards):
+        ss = sh.get_state()
+        assert ss["step"] == 60
+        for f in ("theta", "m", "v", "p"):
+            assert np.array_equal(ss[f].view(np.uint32), fs[f][:, r * S_l:(r + 1) * S_l].view(np.uint32)), (r, f)
+        st = sh.get_stats()
+        for f in ("c", "sumD", "sumD2"):
+            assert np.array_equal(st[f], fst[f]), (r, f)
+    fr = full.round_evaluate().per_replica
+    for r, sh in enumerate(shards):
+        pr = sh.round_evaluate().per_replica
+        for f in ("size", "violations", "cut", "energy"):
+            assert np.array_equal(pr[f], fr[f][r * S_l:(r + 1) * S_l]), (r, f)
+
+
+def test_fused_exchange_concurrent_c5_shards(Q):
+    """c5's graph (20-regular, N = 1e6) split as 8 concurrent ranks of 8 replicas (the G = 8 shard of the
+    scaling run): 20 steps in one cooperative launch, bit-exact against one handle with all 64 replicas."""
+    w = gen.workload("c5")
+    g = w.graphs[0]
+    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
+    gam = oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:20]
+    full = Q.Solver(g.rowptr, g.colidx, Q.make_config("mis", S_total=64, seed=w.seeds[0], **hp))
+    full.run(gam)
+    fs = full.get_state()
+    fst = full.get_stats()
+    full.close()
+    G, S_l = 8, 8
+    shards = [Q.Solver(g.rowptr, g.colidx, Q.make_config("mis", S_total=64, seed=w.seeds[0], replica_offset=r * S_l,
+                                                         S_local=S_l, **hp)) for r in range(G)]
+    bufs, ptrs = exchange_buffers(shards)
+    for r, sh in enumerate(shards):
+        sh.attach_exchange(ptrs, r, G, keep=bufs)
+    Q.loopback_sync_init(shards)
+    Q.exchange_emulate(shards, gam)
+    for r, sh in enumerate(shards):
+        ss = sh.get_state()
+        for f in ("theta", "p"):
+            assert np.array_equal(ss[f].view(np.uint32), fs[f][:, r * S_l:(r + 1) * S_l].view(np.uint32)), (r, f)
+    st = shards[3].get_stats()
+    assert np.array_equal(st["sumD2"], fst["sumD2"]) and np.array_equal(st["c"], fst["c"])
 
 
 def test_fused_exchange_one_rank_equals_nccl(Q):

@@ -32,15 +32,18 @@ def _get(usage, mangled):
 
 def test_headline_c5_kernel_fits_four_ctas(usage):
     """c5 runs k_step<4,1,0,FULL> (two replica blocks of 32, every lane holds a vector): 64 registers and
-    at most the 16-byte spill around the division slow-path calls that the measured-faster FMA contract
-    leaves (profiles/r1_design_iterations.md); more would cost occupancy-bound bandwidth."""
+    at most the 24-byte spill around the division slow-path calls (16 bytes with the round-1 FMA contract,
+    24 since the per-row communication coefficient adds a division site per item; same-box c5 step time
+    unchanged, 812 vs 812 us, profiles/r2_design_iterations.md); more would cost occupancy-bound bandwidth."""
     reg, stack = _get(usage, "_ZN3qqa6k_stepILi4ELi1ELi0ELb1EEEvNS_10StepParamsE")     # k_step<4,1,0,FULL>
-    assert reg <= 64 and stack <= 16
+    assert reg <= 64 and stack <= 24
 
 
-def test_unblocked_64_replica_kernel_has_no_spills(usage):
+def test_unblocked_64_replica_kernel_spills_at_most_the_division_frame(usage):
+    """k_step<8,1,0> (64 replicas unblocked): no spill in round 1; the per-row communication coefficient's
+    division site (round 2) leaves a 16-byte frame around the slow-path calls."""
     reg, stack = _get(usage, "_ZN3qqa6k_stepILi8ELi1ELi0ELb0EEEvNS_10StepParamsE")     # k_step<8,1,0>
-    assert reg <= 64 and stack == 0
+    assert reg <= 64 and stack <= 16
 
 
 @pytest.mark.parametrize("lanes", [1, 2, 4, 8, 16, 32])
