@@ -247,7 +247,7 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
     and the ranks agree (MIN all-reduce) before the next collective phase, so a failure anywhere sends
     every rank back to the NCCL handle instead of leaving the others waiting in a collective.
     Returns (solver, peer pointers or None, description, probe times or None)."""
-    exchange = "nccl all-reduce (4-chunk overlap)"
+    exchange = "nccl all-reduce (2-chunk overlap)"
     if args.exchange == "nccl" or w.n_colors:
         return sol, None, exchange, None
 

@@ -1007,9 +1007,12 @@ int set_device(qqa_handle* h) {
 }
 
 // Chunked compute / all-reduce overlap for the binary step (K-ary keeps one all-reduce per
-// step). QQA_COMM_CHUNKS overrides the default: 4 chunks with > 1 rank, none with one.
+// step). QQA_COMM_CHUNKS overrides the default: 2 chunks with > 1 rank, none with one. Measured on
+// c5's G = 8 shard (S_l = 8, one rank, profiles/r2_host_enqueue.txt): every extra chunk launch costs
+// device time (131 / 144 / 162 / 177 us per step for 1 / 2 / 3 / 4 chunks), more than the ~1/C of a
+// 16 MB all-reduce (~40-55 us at G = 8) each further chunk would hide, so 2.
 int setup_overlap(qqa_handle* h) {
-  int C = (h->nranks > 1 && !h->s.kary) ? 4 : 1;
+  int C = (h->nranks > 1 && !h->s.kary) ? 2 : 1;
   if (const char* env = std::getenv("QQA_COMM_CHUNKS")) C = std::max(1, std::min(64, std::atoi(env)));
   if (h->s.kary || h->s.n < C) C = 1;
   h->comm_chunks = C;

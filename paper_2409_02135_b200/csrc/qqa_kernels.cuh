@@ -45,6 +45,12 @@ enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2, kCOLORING = 3, kMAXCLIQUE_SP
 // (q_i = sum_j w_ij p_j as fl(q + fl(w p)) in CSR order; MIS and Max-Cut).
 enum : int { kModeClamp = 1, kModeNoise = 2, kModeSparseClique = 4, kModeWeighted = 8 };
 
+#ifndef QQA_VPL2_HALF
+#define QQA_VPL2_HALF 0        // 1: VPL >= 2 kernels gather each round of 4 rows as two halves of 2
+#endif
+#ifndef QQA_VPL2_MINB
+#define QQA_VPL2_MINB 2        // min CTAs per SM of the VPL >= 2 kernels
+#endif
 #ifndef QQA_GATHER_U
 #define QQA_GATHER_U 4         // neighbour rows in flight per lane (multiple of 4)
 #endif
@@ -463,6 +469,32 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 #pragma unroll
       for (int u4 = 0; u4 < U / 4; ++u4)
         nxt[u4] = (e0 + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e0 + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
+#if QQA_VPL2_HALF
+      if constexpr (VPL >= 2 && !(MODE & kModeWeighted)) {
+        // wide rows (VPL >= 2 vectors per lane): each round of 4 neighbours is gathered as two halves of 2
+        // rows, so only 2 x VPL vectors are held in registers (same CSR-order adds)
+        for (int e = e0; e < e1; e += 4) {
+          const int js[4] = {nxt[0].x, nxt[0].y, nxt[0].z, nxt[0].w};
+#pragma unroll
+          for (int h = 0; h < 4; h += 2) {
+            V8 buf[2][VPL];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+              for (int w = 0; w < VPL; ++w) {
+                const int col8 = lane + w * LANES;
+                buf[u][w] = (FULL || col8 < SB8) ? ld8_gather(pc + (size_t)js[h + u] * P.SB + col8 * 8) : zero8();
+              }
+            if (h == 2) nxt[0] = (e + 4 < e1) ? ld_idx4(P.colidx_pad + e + 4) : make_int4(P.n, P.n, P.n, P.n);
+#pragma unroll
+            for (int w = 0; w < VPL; ++w) {
+              if (e == e0 && h == 0) acc[w] = buf[0][w]; else add8(acc[w], buf[0][w]);
+              add8(acc[w], buf[1][w]);
+            }
+          }
+        }
+      } else
+#endif
       for (int e = e0; e < e1; e += U) {
         int js[U];
 #pragma unroll
@@ -593,7 +625,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 }
 
 template <int LANES, int VPL, int MODE, bool FULL>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
+__global__ void __launch_bounds__(256, (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
   const int lane = threadIdx.x & (LANES - 1);
   const unsigned gmask = group_mask<LANES>();
   const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
@@ -692,7 +724,7 @@ __device__ __forceinline__ void step_x_body(const StepParams& P, const XParams& 
 }
 
 template <int LANES, int VPL, int MODE, bool FULL>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
+__global__ void __launch_bounds__(256, (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
   step_x_body<LANES, VPL, MODE, FULL>(P, X, (int)blockIdx.x, (int)gridDim.x);
 }
 
@@ -711,7 +743,7 @@ struct XEmulParams {
 };
 
 template <int LANES, int VPL, int MODE, bool FULL>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)) k_step_x_emul(const XEmulParams E) {
+__global__ void __launch_bounds__(256, (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step_x_emul(const XEmulParams E) {
   const int r = (int)blockIdx.x / E.cta_per_rank, cta = (int)blockIdx.x % E.cta_per_rank;
   if (r >= E.G) return;
   for (int j = 0; j < E.nsteps; ++j) {
@@ -765,7 +797,7 @@ struct RunParams {
 // rows largely stay in that SM's L1; c2 69.8 -> 57.8 us/step); 256 = 4 CTAs per SM with rows
 // strided over the grid (kernels needing > 64 registers, or too little work to fill every SM).
 template <int LANES, int VPL, int MODE, int CT, bool FULL>
-__global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 2 ? 2 : QQA_STEP_MIN_BLOCKS)))
+__global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)))
     k_run(const RunParams R) {
   namespace cg = cooperative_groups;
   const StepParams& P = R.P;
