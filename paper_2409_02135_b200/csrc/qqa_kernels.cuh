@@ -45,11 +45,14 @@ enum : int { kMIS = 0, kMAXCUT = 1, kMAXCLIQUE = 2, kCOLORING = 3, kMAXCLIQUE_SP
 // (q_i = sum_j w_ij p_j as fl(q + fl(w p)) in CSR order; MIS and Max-Cut).
 enum : int { kModeClamp = 1, kModeNoise = 2, kModeSparseClique = 4, kModeWeighted = 8 };
 
+// Kernels with VPL >= 2 vectors per lane (S_p > 256, e.g. c4's S = 512) gather each round of 4 neighbour
+// rows as two halves of 2 rows, which takes them from 121 to 80 registers and 2 to 3 CTAs per SM
+// (c4: 137.4 -> 128.1 us per step, same CSR-order adds; profiles/r2_ab_c4_half_rounds.txt).
 #ifndef QQA_VPL2_HALF
-#define QQA_VPL2_HALF 0        // 1: VPL >= 2 kernels gather each round of 4 rows as two halves of 2
+#define QQA_VPL2_HALF 1        // 0: the round-1 gather (4 rows x VPL vectors in registers)
 #endif
 #ifndef QQA_VPL2_MINB
-#define QQA_VPL2_MINB 2        // min CTAs per SM of the VPL >= 2 kernels
+#define QQA_VPL2_MINB 3        // min CTAs per SM of the VPL = 2 kernels (2 with QQA_VPL2_HALF=0; VPL = 4: 2)
 #endif
 #ifndef QQA_GATHER_U
 #define QQA_GATHER_U 4         // neighbour rows in flight per lane (multiple of 4)
@@ -625,7 +628,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 }
 
 template <int LANES, int VPL, int MODE, bool FULL>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
+__global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step(const StepParams P) {
   const int lane = threadIdx.x & (LANES - 1);
   const unsigned gmask = group_mask<LANES>();
   const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
@@ -724,7 +727,7 @@ __device__ __forceinline__ void step_x_body(const StepParams& P, const XParams& 
 }
 
 template <int LANES, int VPL, int MODE, bool FULL>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
+__global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step_x(const StepParams P, const XParams X) {
   step_x_body<LANES, VPL, MODE, FULL>(P, X, (int)blockIdx.x, (int)gridDim.x);
 }
 
@@ -743,7 +746,7 @@ struct XEmulParams {
 };
 
 template <int LANES, int VPL, int MODE, bool FULL>
-__global__ void __launch_bounds__(256, (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step_x_emul(const XEmulParams E) {
+__global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step_x_emul(const XEmulParams E) {
   const int r = (int)blockIdx.x / E.cta_per_rank, cta = (int)blockIdx.x % E.cta_per_rank;
   if (r >= E.G) return;
   for (int j = 0; j < E.nsteps; ++j) {
@@ -797,7 +800,7 @@ struct RunParams {
 // rows largely stay in that SM's L1; c2 69.8 -> 57.8 us/step); 256 = 4 CTAs per SM with rows
 // strided over the grid (kernels needing > 64 registers, or too little work to fill every SM).
 template <int LANES, int VPL, int MODE, int CT, bool FULL>
-__global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)))
+__global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)))
     k_run(const RunParams R) {
   namespace cg = cooperative_groups;
   const StepParams& P = R.P;

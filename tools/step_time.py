@@ -11,9 +11,9 @@ import paper_2409_02135_b200 as Q  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 w = gen.workload(name)
-g = w.graphs[0]
+(g, gor) = w.batched()          # a batch (c2, t1) runs as one block-diagonal handle, as bench.py does
 hp = {k: v for k, v in w.hparams().items() if k != "problem"}
-sol = Q.Solver(g.rowptr, g.colidx, Q.make_config(w.problem, S_total=w.S, seed=w.seeds[0], **hp))
+sol = Q.Solver(g.rowptr, g.colidx, Q.make_config(w.problem, S_total=w.S, seed=w.seeds[0], **hp), group_of_row=gor)
 sol.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 5)   # warm-up
 sol.profile(True)
 sol.run_linear(w.gamma_min, w.gamma_max, w.steps, 5, 5 + steps)
