@@ -53,6 +53,7 @@ constexpr int kSchedCap = 4096;   // steps per persistent launch (device table o
 constexpr int64_t kClusterMaxElems = 1 << 15;   // n S_p up to this runs in one thread-block cluster (k_run_cluster)
 constexpr int64_t kClusterMaxGather = 1 << 19;  // ... if its DSMEM gather (padded nnz x S_p values per step) is small
 constexpr double kL2BlockBudget = 128.0 * 1024 * 1024;  // p larger than this is replica-blocked (measured)
+constexpr double kKaryChunkBudget = 32.0 * 1024 * 1024; // K-ary: gathered lines of one replica chunk (measured, §4)
 size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Shape {
@@ -218,6 +219,11 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
     s.K = c->n_colors;
     s.KP = (s.K + 3) / 4 * 4;
     s.LK = std::max(4, std::min(32, next_pow2(c->S_local)));
+    // The step walks (replica chunk, variable) items chunk-major, so while the grid sweeps a chunk only
+    // that chunk's lines of P are gathered: n LK KP 4 bytes. Chunks are narrowed until that fits the
+    // ~32 MB an all-SM gather keeps in L2 (k8: 32 -> 8 lanes, 836 -> 706 us per step).
+    while (s.LK > 4 && (double)g->n * s.LK * s.KP * sizeof(float) > kKaryChunkBudget) s.LK >>= 1;
+    if (const char* env = std::getenv("QQA_KARY_LANES")) s.LK = std::max(4, std::min(32, next_pow2(std::atoi(env))));
   }
   // Replica blocking: when one copy of p is larger than the L2
   // budget, split the replicas into blocks of SB (a power of two >= 8) so that
@@ -611,6 +617,8 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
   qqa::StepKParams P{};
   P.rowptr = h->rowptr; P.colidx = h->colidx; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = s.n; P.S = s.S_local; P.K = s.K; P.L = s.LK;
+  P.cmaj = 1;   // chunk-major item order (measured: k8 -4 % at the same chunk width, q13 -16 %)
+  if (const char* env = std::getenv("QQA_KARY_CMAJ")) P.cmaj = std::atoi(env) != 0;
   P.Kf = (float)s.K; P.comm = c.comm; P.alpha = c.alpha;
   P.kgrad = c.kary_grad;
   P.b1 = c.beta1; P.c1 = (float)(1.0 - (double)c.beta1);

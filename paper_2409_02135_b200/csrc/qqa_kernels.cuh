@@ -236,8 +236,8 @@ __device__ __forceinline__ V8 zero8() {
 #ifndef QQA_RECOMPUTE_P
 #define QQA_RECOMPUTE_P 0
 #endif
-// 1: the next round's CSR indices are loaded before this round's gathers (software pipeline;
-// measured slower on c5 -- extra live registers spill -- so off, profiles/r1_design_iterations.md)
+// 1: the next round's CSR indices are loaded before this round's gathers in every kernel (software
+// pipeline; the non-FULL kernels always do, see step_item; the FULL ones do not: r1 and r2 measurements)
 #ifndef QQA_IDX_PIPELINE
 #define QQA_IDX_PIPELINE 0
 #endif
@@ -465,6 +465,10 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
       V8 acc[VPL];
       const int e0 = __ldg(P.rowptr_pad + i), e1 = __ldg(P.rowptr_pad + i + 1);
       constexpr int U = (VPL == 1) ? QQA_GATHER_U : 4;   // neighbour rows in flight per lane
+      // Index loads of round k+1 issued before round k's gathers: measured faster for the non-FULL shapes
+      // (the ER batches c2 / t1, S_p = 104: -3.6 % / -2.1 %) and neutral or slower for the FULL ones (c3 +0.4 %,
+      // c5 ±0.3 %; profiles/r2_ab_index_pipeline.txt), so it is compiled into the non-FULL kernels only.
+      constexpr bool kIdxPipe = QQA_IDX_PIPELINE || !FULL;
       // The indices of round k+1 are loaded before the gathers of round k (software pipeline), so
       // each round waits for one memory latency, not an index load followed by the gathers.
       // Rows are padded to multiples of 4 (not of U): past the row end the sentinel row n is read.
@@ -504,11 +508,11 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         for (int u4 = 0; u4 < U / 4; ++u4) {
           js[4 * u4] = nxt[u4].x; js[4 * u4 + 1] = nxt[u4].y; js[4 * u4 + 2] = nxt[u4].z; js[4 * u4 + 3] = nxt[u4].w;
         }
-#if QQA_IDX_PIPELINE
+        if constexpr (kIdxPipe) {
 #pragma unroll
-        for (int u4 = 0; u4 < U / 4; ++u4)
-          nxt[u4] = (e + U + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e + U + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
-#endif
+          for (int u4 = 0; u4 < U / 4; ++u4)
+            nxt[u4] = (e + U + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e + U + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
+        }
         V8 buf[U][VPL];
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -517,11 +521,11 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
             const int col8 = lane + w * LANES;
             buf[u][w] = (FULL || col8 < SB8) ? ld8_gather(pc + (size_t)js[u] * P.SB + col8 * 8) : zero8();
           }
-#if !QQA_IDX_PIPELINE
+        if constexpr (!kIdxPipe) {
 #pragma unroll
-        for (int u4 = 0; u4 < U / 4; ++u4)
-          nxt[u4] = (e + U + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e + U + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
-#endif
+          for (int u4 = 0; u4 < U / 4; ++u4)
+            nxt[u4] = (e + U + 4 * u4 < e1) ? ld_idx4(P.colidx_pad + e + U + 4 * u4) : make_int4(P.n, P.n, P.n, P.n);
+        }
         if (MODE & kModeWeighted) {   // q = fl(q + fl(w p)) in CSR order from +0 (padding: w = 0, p = 0)
           float wt[U];
 #pragma unroll
@@ -1301,6 +1305,9 @@ struct StepKParams {
   int* __restrict__ flag;
   int n, S, K, L;
   int kgrad;                            // 1: gradient through the map, g - <g, p> (reading R33)
+  int cmaj;                             // 1: items ordered chunk-major (all variables of replica chunk 0, then
+                                        // chunk 1, ...): while the grid sweeps one chunk only that chunk's
+                                        // lines of P are gathered (n L KP 4 bytes), which can stay in L2
   float Kf, comm, b1, c1, b2, c2, eps, unif;   // unif = (float)(1/K)
   int alpha;
   float kt, at, st, rt, ns;
@@ -1356,7 +1363,9 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(co
   const long long items = (long long)P.n * nch;
   bool bad = false;
   for (long long it = (long long)blockIdx.x * groups_cta + gl; it < items; it += (long long)gridDim.x * groups_cta) {
-    const int i = (int)(it / nch), ch = (int)(it - (long long)i * nch);
+    int i, ch;
+    if (P.cmaj) { ch = (int)(it / P.n); i = (int)(it - (long long)ch * P.n); }
+    else { i = (int)(it / nch); ch = (int)(it - (long long)i * nch); }
     const int r = ch * L + lane;
     const bool live = r < P.S;
     float w[KP];                                          // the replica's new P (0 on idle lanes)
@@ -1491,7 +1500,9 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
   bool bad = false;
   for (long long it = (long long)blockIdx.x * warps_cta + (threadIdx.x >> 5); it < items;
        it += (long long)gridDim.x * warps_cta) {
-    const int i = (int)(it / nch), ch = (int)(it - (long long)i * nch);
+    int i, ch;
+    if (P.cmaj) { ch = (int)(it / P.n); i = (int)(it - (long long)ch * P.n); }
+    else { i = (int)(it / nch); ch = (int)(it - (long long)i * nch); }
     const int r = ch * kQuadReps + rq;
     const bool rep = r < P.S;                            // a live replica (all 4 lanes)
     const bool live = rep && q < NQ;                     // ... and a quad holding colours
