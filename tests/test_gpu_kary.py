@@ -164,3 +164,23 @@ def test_gradient_through_the_map_reaches_table_4_on_small_queens(Q):
                                                          temperature=0.001))
         sol.run_linear(-2.0, 0.1, 3000)
         assert int(sol.round_evaluate().best_energy) == 0, (r, K)
+
+
+@pytest.mark.parametrize("K,S", [(8, 64), (13, 100), (5, 9)])
+def test_item_order_and_chunk_width_do_not_change_results(Q, monkeypatch, K, S):
+    """Round 2 walks (replica chunk, variable) items chunk-major with chunks narrowed to fit L2 (DESIGN.md §5);
+    the per-(variable, colour) statistics meet in exact int64 atomics, so every order and chunk width gives the
+    same bits, and the contract oracle's."""
+    g = gen.random_regular(600, 8, 4)
+    gam = oracle.schedule(-2.0, 0.1, 200)[:40]
+    hp = dict(lr=0.01, comm=0.3)
+    st = oracle.run_K(g, ocfg(S, 21, **hp), K, gam)
+    for cmaj in ("0", "1"):
+        for lanes in ("4", "8", "32"):
+            monkeypatch.setenv("QQA_KARY_CMAJ", cmaj)
+            monkeypatch.setenv("QQA_KARY_LANES", lanes)
+            monkeypatch.setenv("QQA_KARY_QUAD", "0")   # k_step_K itself for every K (the quad kernel: KP 12 / 16)
+            sol = gpu(Q, g, K, S, 21, **hp)
+            sol.run(gam)
+            assert_equal_K(sol, st)
+            sol.close()
