@@ -36,6 +36,17 @@ XStepKernel xstep_for(int lanes, int vpl, bool full) {
   return nullptr;
 }
 
+// k_step_st<lanes, M> (staged state; VPL = 1, FULL shapes, modes 0-3); nullptr otherwise.
+template <int M>
+StepKernel stage_for(int lanes) {
+  if (M & (kModeSparseClique | kModeWeighted)) return nullptr;
+#define QQA_TCASE(L) \
+  if (lanes == L) return k_step_st<L, (M & 3)>;
+  QQA_TCASE(1) QQA_TCASE(2) QQA_TCASE(4) QQA_TCASE(8) QQA_TCASE(16) QQA_TCASE(32)
+#undef QQA_TCASE
+  return nullptr;
+}
+
 template <int M>
 RunKernel run_kernel_for(int lanes, int vpl, int cta, bool full) {
   if (M & kModeSparseClique) return nullptr;   // its column sums need a pass between steps: no k_run

@@ -346,6 +346,9 @@ struct qqa_handle {
   float* wdeg = nullptr;
   long long* wsums = nullptr;  // [S_total][2] evaluation weight sums (fixed point 2^24)
   bool serpentine = false;     // replica blocks swept in alternating order step to step (QQA_SERPENTINE)
+  qqa::StepKernel kst = nullptr;   // k_step_st (staged state) for the launch-per-step path, nullptr: k_step
+  int grid_st = 0;
+  size_t st_smem = 0;
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
   int run_cta = 256;           // threads per CTA of k_run (1024: contiguous rows per SM)
   // fused statistics exchange over peer memory (qqa_attach_exchange; k_step_x instead of k_step + NCCL)
@@ -948,7 +951,10 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
       for (int ch = 0; ch < C; ++ch) {
         P.row_begin = (int)((int64_t)h->s.n * ch / C);
         P.row_end = (int)((int64_t)h->s.n * (ch + 1) / C);
-        ks<<<h->grid_step, 256, 0, h->stream>>>(P);
+        if (h->kst)
+          h->kst<<<h->grid_st, 256, h->st_smem, h->stream>>>(P);
+        else
+          ks<<<h->grid_step, 256, 0, h->stream>>>(P);
         QQA_CUDA(cudaGetLastError());
         h->launches++;
         if (C > 1) {  // all-reduce this chunk's rows on the comm stream while the next chunk computes
@@ -1263,6 +1269,28 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     }
     h->grid_fin = std::max(1, std::min((s.n + 255) / 256, h->sm_count * 8));
     if ((st = grid_for((const void*)ki, h->sm_count, s.n, s.lanes, h->grid_init))) return cleanup(st);
+    {  // staged-state step kernel (VPL 1, FULL shapes, modes 0-3), opt-in (QQA_STAGE=1): measured slower on
+       // c5 (873 vs 812 us per step; its 32 KB of shared memory per CTA takes L1 space the in-flight gathers
+       // use, profiles/r2_design_iterations.md)
+      const int mode = step_mode(*cfg, s.weighted);
+      bool want = false;
+      if (const char* env = std::getenv("QQA_STAGE")) want = std::atoi(env) != 0;
+      if (want && s.vpl == 1 && full_lanes(s) && mode <= 3) {
+        qqa::StepKernel kt = mode == 0 ? qqa::stage_kernel_m0(s.lanes) : mode == 1 ? qqa::stage_kernel_m1(s.lanes)
+                           : mode == 2 ? qqa::stage_kernel_m2(s.lanes) : qqa::stage_kernel_m3(s.lanes);
+        if (kt) {
+          const size_t smem = 8 * 256 * sizeof(float4);   // [4 vectors][2 halves][256 threads] x 16 B
+          int per_sm = 0;
+          QQA_CUDA_C(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kt, 256, smem));
+          if (per_sm > 0) {
+            h->kst = kt;
+            h->st_smem = smem;
+            const int need = (int)std::max<int64_t>(1, ((int64_t)s.n * s.lanes + 255) / 256);
+            h->grid_st = std::max(1, std::min(need, per_sm * h->sm_count));
+          }
+        }
+      }
+    }
     if (s.B == 1 && !s.weighted && cfg->problem != QQA_MAXCLIQUE_SPARSE && s.n > 0 &&
         (int64_t)s.n * s.S_p <= kClusterMaxElems && s.nnz_pad * s.S_p <= kClusterMaxGather) {   // tiny: one cluster
       const qqa::RunKernel kc = qqa::cluster_kernel(step_mode(*cfg, s.weighted));

@@ -39,6 +39,12 @@ RunKernel run_kernel_m9(int lanes, int vpl, int cta, bool full);
 RunKernel run_kernel_m10(int lanes, int vpl, int cta, bool full);
 RunKernel run_kernel_m11(int lanes, int vpl, int cta, bool full);
 
+// k_step_st<lanes, MODE> (staged state, VPL = 1, FULL shapes), MODE 0..3; nullptr otherwise.
+StepKernel stage_kernel_m0(int lanes);
+StepKernel stage_kernel_m1(int lanes);
+StepKernel stage_kernel_m2(int lanes);
+StepKernel stage_kernel_m3(int lanes);
+
 // k_step_x<lanes, vpl, MODE> (fused statistics exchange), MODE 0..3; nullptr otherwise.
 XStepKernel xstep_kernel_m0(int lanes, int vpl, bool full);
 XStepKernel xstep_kernel_m1(int lanes, int vpl, bool full);

@@ -307,6 +307,39 @@ __device__ __forceinline__ V8 ld8(const float* ptr) {
   return r;
 }
 
+// Staged state (k_step_st): the next item's theta / m / v / p vectors are copied global -> shared memory
+// with cp.async (no registers held while in flight) during the current item's update, so their DRAM
+// latency is hidden. Shared layout [4 vectors][2 halves][blockDim] of 16 bytes: thread t's 16-byte halves
+// are consecutive across the warp (conflict-free LDS.128).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// the streamed theta / m / v: L2 evict_first, as ld8_stream (they would otherwise push gathered p rows out)
+__device__ __forceinline__ void cp_async16_ef(uint32_t dst, const void* src) {
+  asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+               " cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, pol;\n}" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void stage_v8(const float4* smem, int vec, const float* src) {
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  if (vec < 3) {   // theta, m, v
+    cp_async16_ef(base + (uint32_t)(((2 * vec + 0) * nt + t) * 16), src);
+    cp_async16_ef(base + (uint32_t)(((2 * vec + 1) * nt + t) * 16), src + 4);
+  } else {         // p: part of the gathered block
+    cp_async16(base + (uint32_t)(((2 * vec + 0) * nt + t) * 16), src);
+    cp_async16(base + (uint32_t)(((2 * vec + 1) * nt + t) * 16), src + 4);
+  }
+}
+__device__ __forceinline__ V8 unstage_v8(const float4* smem, int vec) {
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  const float4 a = smem[(2 * vec + 0) * nt + t], b = smem[(2 * vec + 1) * nt + t];
+  V8 r;
+  r.f[0] = a.x; r.f[1] = a.y; r.f[2] = a.z; r.f[3] = a.w; r.f[4] = b.x; r.f[5] = b.y; r.f[6] = b.z; r.f[7] = b.w;
+  return r;
+}
+
 // The per-step part of a step launch: buffers of this step and its scalars.
 // (A member of the kernel parameters for the launch-per-step kernel, so it stays in the
 // constant bank; a register copy per step in the persistent kernel.)
@@ -454,10 +487,11 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
 // One work item (replica block b, variable i) of the step: gather, update, statistics.
 // FULL: every lane holds a vector of the block (SB / 8 == LANES * VPL), so the gather needs no
 // per-lane guard (a compile-time variant; measured 1.7 % on c5).
-template <int LANES, int VPL, int MODE, bool FULL = false>
+template <int LANES, int VPL, int MODE, bool FULL = false, bool STAGE = false>
 __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
                                           unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false,
-                                          long long* sums_dst = nullptr, long long* zero_dst = nullptr) {
+                                          long long* sums_dst = nullptr, long long* zero_dst = nullptr,
+                                          const float4* stage = nullptr, int nb = -1, int ni = -1) {
       const int SB8 = P.SB >> 3;
       const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
       const float* __restrict__ pc = V.p_cur + blk;
@@ -578,11 +612,29 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         const int col8 = lane + w * LANES;
         if (!FULL && col8 >= SB8) continue;
         const size_t at = blk + (size_t)i * P.SB + col8 * 8;
-        V8 th = ld8_stream(P.theta + at);
-        V8 mm = ld8_stream(P.m + at);
-        V8 vv = ld8_stream(P.v + at);
-        V8 pp;
-        if (MODE & kModeClamp) {
+        V8 th, mm, vv, pp;
+        if constexpr (STAGE) {   // this item's state was staged into shared memory during the previous item
+          cp_async_wait_all();
+          th = unstage_v8(stage, 0);
+          mm = unstage_v8(stage, 1);
+          vv = unstage_v8(stage, 2);
+          if (!(MODE & kModeClamp)) pp = unstage_v8(stage, 3);
+          if (nb >= 0) {         // stage the next item's (nb, ni) while this one updates
+            const size_t an = (size_t)nb * ((size_t)P.n + 1) * P.SB + (size_t)ni * P.SB + col8 * 8;
+            stage_v8(stage, 0, P.theta + an);
+            stage_v8(stage, 1, P.m + an);
+            stage_v8(stage, 2, P.v + an);
+            if (!(MODE & kModeClamp)) stage_v8(stage, 3, V.p_cur + an);
+          }
+          cp_async_commit();
+        } else {
+          th = ld8_stream(P.theta + at);
+          mm = ld8_stream(P.m + at);
+          vv = ld8_stream(P.v + at);
+        }
+        if (STAGE && !(MODE & kModeClamp)) {
+          // pp staged above
+        } else if (MODE & kModeClamp) {
           pp = th;                                    // clamp map: the parameter is p
         } else if (QQA_RECOMPUTE_P) {
 #pragma unroll
@@ -644,6 +696,42 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB 
       const float2 msi = P.ms[i];
       step_item<LANES, VPL, MODE, FULL>(P, P.var, b, i, lane, gmask, msi.x, msi.y, bad);
     }
+  }
+  if (bad) atomicOr(P.flag, 1);
+}
+
+// k_step with the staged state (VPL = 1, FULL): the same items in the same order; item k+1's theta / m / v / p
+// are in flight in shared memory (cp.async) while item k updates and item k+1 gathers. Bit-identical to k_step.
+// Opt-in (QQA_STAGE=1): measured slower than k_step on c5 (873 / 935 vs 812 / 813 us per step at SB = 32 / 16),
+// the shared memory it needs is L1 the in-flight gathers no longer get.
+template <int LANES, int MODE>
+__global__ void __launch_bounds__(256, QQA_STEP_MIN_BLOCKS) k_step_st(const StepParams P) {
+  extern __shared__ float4 stage_smem[];
+  const int lane = threadIdx.x & (LANES - 1);
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  bool bad = false;
+  // item sequence: block passes bb = 0..B-1 (block b = rev ? B-1-bb : bb), rows row_begin + group + k ngroups
+  auto blk_of = [&](int bb) { return P.var.rev ? P.B - 1 - bb : bb; };
+  int bb = 0, i = P.row_begin + group;
+  if (i >= P.row_end) bb = P.B;   // no rows for this group
+  if (bb < P.B) {
+    const size_t a0 = (size_t)blk_of(bb) * ((size_t)P.n + 1) * P.SB + (size_t)i * P.SB + lane * 8;
+    stage_v8(stage_smem, 0, P.theta + a0);
+    stage_v8(stage_smem, 1, P.m + a0);
+    stage_v8(stage_smem, 2, P.v + a0);
+    if (!(MODE & kModeClamp)) stage_v8(stage_smem, 3, P.var.p_cur + a0);
+    cp_async_commit();
+  }
+  while (bb < P.B) {
+    int nbb = bb, ni = i + ngroups;
+    if (ni >= P.row_end) { nbb = bb + 1; ni = P.row_begin + group; }
+    const float2 msi = P.ms[i];
+    step_item<LANES, 1, MODE, true, true>(P, P.var, blk_of(bb), i, lane, gmask, msi.x, msi.y, bad, false, nullptr,
+                                          nullptr, stage_smem, nbb < P.B ? blk_of(nbb) : -1, ni);
+    bb = nbb;
+    i = ni;
   }
   if (bad) atomicOr(P.flag, 1);
 }

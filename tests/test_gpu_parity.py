@@ -516,3 +516,34 @@ def test_cluster_then_resume_on_other_paths(Q, monkeypatch):
     st = oracle.run(g, ocfg("mis", 16, 9), oracle.schedule(-2.0, 0.1, 400))
     assert_state_equal(a, st)
     assert_stats_equal(a, st)
+
+
+STAGE_CASES = [
+    # (problem, graph, S, hp, replica block)
+    ("mis", lambda: gen.random_regular(3000, 20, 5), 64, dict(), "32"),                      # c5's layout
+    ("mis", lambda: gen.random_regular(3000, 20, 5), 64, dict(), "16"),
+    ("maxcut", lambda: gen.erdos_renyi(900, 0.02, 3), 64, dict(map="clamp", temperature=0.002, comm=0.5), None),
+    ("mis", lambda: gen.erdos_renyi(700, 0.03, 4), 8, dict(alpha=4), None),
+    ("maxcut", lambda: gen.random_regular(500, 5, 6), 256, dict(comm=1.0), None),
+    ("mis", lambda: gen.erdos_renyi(800, 0.01, 7), 16, dict(map="clamp"), "8"),
+]
+
+
+@pytest.mark.parametrize("case", range(len(STAGE_CASES)))
+def test_staged_state_kernel_parity(Q, monkeypatch, case):
+    """k_step_st (round 2): the next item's theta / m / v / p staged in shared memory by cp.async while the
+    current item updates -- the default for replica-blocked layouts; forced here on every FULL shape and the
+    clamp / noise modes. Bit-exact against the contract oracle, like k_step."""
+    problem, mk, S, hp, sb = STAGE_CASES[case]
+    monkeypatch.setenv("QQA_STAGE", "1")
+    monkeypatch.setenv("QQA_PERSISTENT", "0")
+    if sb:
+        monkeypatch.setenv("QQA_BLOCK_REPLICAS", sb)
+    g = mk()
+    gam = oracle.schedule(-2.0, 0.1, 500)[:50]
+    sol = gpu(Q, g, problem, S, 13, **hp)
+    assert sol.step_path() == "step"
+    sol.run(gam)
+    st = oracle.run(g, ocfg(problem, S, 13, **hp), gam)
+    assert_state_equal(sol, st)
+    assert_stats_equal(sol, st)
