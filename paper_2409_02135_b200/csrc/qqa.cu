@@ -1257,6 +1257,9 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg, s.weighted), ks, ki, &kr, h->run_cta, full_lanes(s)))
       return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
     if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);
+    if (const char* env = std::getenv("QQA_STEP_CARVEOUT")) {   // experiment: L1 / shared split of k_step
+      QQA_CUDA_C(cudaFuncSetAttribute((const void*)ks, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(env)));
+    }
     {  // persistent kernel: every CTA must be co-resident (cooperative launch)
       int coop = 0;
       cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
