@@ -222,7 +222,7 @@ QQA_API int qqa_share_comm(qqa_handle* h, qqa_handle* donor);
  *     at r = rank); every rank calls it (collectively when a communicator is attached, which stays
  *     in use for init and evaluation). Zeroes this rank's buffer and re-initialises the replicas.
  *     Without a communicator (shards emulated on one device) call qqa_loopback_sync_init next.
- *   Supported: binary problems without edge weights or the printed clique (else UNSUPPORTED). A peer
+ *   Supported: the binary problems, weighted or not, except the printed clique (else UNSUPPORTED). A peer
  *   that never arrives is reported as QQA_ERR_COMM at the next synchronising call (no hang). */
 QQA_API int qqa_exchange_bytes(qqa_handle* h, size_t* bytes);
 QQA_API int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks);

@@ -27,9 +27,10 @@ StepKernel step_for(int lanes, int vpl, bool full) {
 
 template <int M>
 XStepKernel xstep_for(int lanes, int vpl, bool full) {
-  if (M & (kModeSparseClique | kModeWeighted)) return nullptr;   // fused exchange: modes 0-3
+  if (M & kModeSparseClique) return nullptr;   // fused exchange: modes 0-3 and the weighted 8-11
 #define QQA_XCASE(L, V) \
-  if (lanes == L && vpl == V) return full ? k_step_x<L, V, (M & 3), true> : k_step_x<L, V, (M & 3), false>;
+  if (lanes == L && vpl == V) \
+    return full ? k_step_x<L, V, (M & 11), true> : k_step_x<L, V, (M & 11), false>;
   QQA_XCASE(1, 1) QQA_XCASE(2, 1) QQA_XCASE(4, 1) QQA_XCASE(8, 1) QQA_XCASE(16, 1)
   QQA_XCASE(32, 1) QQA_XCASE(32, 2) QQA_XCASE(32, 4)
 #undef QQA_XCASE

@@ -20,6 +20,10 @@ XEmulKernel xemul_kernel(int lanes, int vpl, int mode, bool full) {
     case 1: return xemul_for<1>(lanes, vpl, full);
     case 2: return xemul_for<2>(lanes, vpl, full);
     case 3: return xemul_for<3>(lanes, vpl, full);
+    case 8: return xemul_for<8>(lanes, vpl, full);
+    case 9: return xemul_for<9>(lanes, vpl, full);
+    case 10: return xemul_for<10>(lanes, vpl, full);
+    case 11: return xemul_for<11>(lanes, vpl, full);
     default: return nullptr;
   }
 }

@@ -540,6 +540,10 @@ qqa::XStepKernel pick_xstep(int lanes, int vpl, int mode, bool full) {
     case 1: return qqa::xstep_kernel_m1(lanes, vpl, full);
     case 2: return qqa::xstep_kernel_m2(lanes, vpl, full);
     case 3: return qqa::xstep_kernel_m3(lanes, vpl, full);
+    case 8: return qqa::xstep_kernel_m8(lanes, vpl, full);
+    case 9: return qqa::xstep_kernel_m9(lanes, vpl, full);
+    case 10: return qqa::xstep_kernel_m10(lanes, vpl, full);
+    case 11: return qqa::xstep_kernel_m11(lanes, vpl, full);
     default: return nullptr;
   }
 }
@@ -839,6 +843,7 @@ qqa::StepParams xstep_base(const qqa_handle* h) {
   const qqa_config& c = h->cfg;
   qqa::StepParams P{};
   P.rowptr = h->rowptr; P.rowptr_pad = h->rowptr_pad; P.colidx_pad = h->colidx_pad;
+  P.w_pad = h->w_pad; P.wdeg = h->wdeg;
   P.theta = h->theta; P.m = h->m; P.v = h->v; P.flag = h->flag;
   P.n = h->s.n; P.SB = h->s.SB; P.B = h->s.B; P.S_local = h->s.S_local; P.S_total = (double)h->s.S_total;
   P.off = c.replica_offset;
@@ -1932,8 +1937,8 @@ int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int 
   if (!h || !peer_bufs) return fail(QQA_ERR_INVALID_ARG, "handle or peer_bufs is NULL");
   if (nranks < 1 || nranks > qqa::kMaxRanks || rank < 0 || rank >= nranks)
     return fail(QQA_ERR_INVALID_ARG, "need 1 <= nranks <= 8 and 0 <= rank < nranks");
-  if (h->s.kary || step_mode(h->cfg, h->s.weighted) > 3)
-    return fail(QQA_ERR_UNSUPPORTED, "the fused exchange supports the binary problems without edge weights or the printed clique");
+  if (h->s.kary || (step_mode(h->cfg, h->s.weighted) & qqa::kModeSparseClique))
+    return fail(QQA_ERR_UNSUPPORTED, "the fused exchange supports the binary problems except the printed clique");
   if ((int64_t)h->s.S_local * nranks != h->s.S_total || h->cfg.replica_offset != rank * h->s.S_local)
     return fail(QQA_ERR_INVALID_ARG, "sharding must be S_total = nranks * S_local and replica_offset = rank * S_local");
   if (h->comm && (h->rank != rank || h->nranks != nranks))

@@ -225,3 +225,37 @@ def test_bench_multi_gpu_code_path_at_one_rank(Q, mode):
     else:
         probe = d["config"]["exchange_probe"]
         assert probe["fused_ms_per_step"] > 0 and probe["nccl_ms_per_step"] > 0
+
+
+@pytest.mark.parametrize("kind,problem,G,S_l,hp", [("pm1", "maxcut", 4, 16, dict(comm=0.3)),
+                                                   ("int", "mis", 2, 32, dict(comm=0.5, map="clamp", temperature=0.002)),
+                                                   ("uniform", "maxcut", 8, 8, dict(comm=0.1))])
+def test_fused_exchange_weighted_graphs(Q, kind, problem, G, S_l, hp):
+    """Edge-weighted graphs (Optsicom +-1 weights) through the fused exchange, ranks run in lockstep
+    and then concurrently (one cooperative launch): bit-identical to the handle holding every replica."""
+    g = gen.with_weights(gen.erdos_renyi(400, 0.03, 11), kind, 5)
+    S = G * S_l
+    gam = oracle.schedule(-5.0 if problem == "maxcut" else -2.0, 0.1, 300)[:40]
+    full = Q.Solver(g.rowptr, g.colidx, Q.make_config(problem, S_total=S, seed=3, **hp), weights=g.weights)
+    full.run(gam)
+    fs, fst = full.get_state(), full.get_stats()
+    shards = [Q.Solver(g.rowptr, g.colidx, Q.make_config(problem, S_total=S, seed=3, replica_offset=r * S_l,
+                                                         S_local=S_l, **hp), weights=g.weights) for r in range(G)]
+    bufs, ptrs = exchange_buffers(shards)
+    for r, sh in enumerate(shards):
+        sh.attach_exchange(ptrs, r, G, keep=bufs)
+    Q.loopback_sync_init(shards)
+    Q.loopback_run(shards, gam[:20])        # lockstep
+    Q.exchange_emulate(shards, gam[20:])    # concurrent
+    for r, sh in enumerate(shards):
+        ss = sh.get_state()
+        for f in ("theta", "m", "v", "p"):
+            assert np.array_equal(ss[f].view(np.uint32), fs[f][:, r * S_l:(r + 1) * S_l].view(np.uint32)), (r, f)
+        st = sh.get_stats()
+        for f in ("c", "sumD", "sumD2"):
+            assert np.array_equal(st[f], fst[f]), (r, f)
+    fr = full.round_evaluate().per_replica
+    for r, sh in enumerate(shards):
+        pr = sh.round_evaluate().per_replica
+        for f in ("wviolations", "wcut", "energy"):
+            assert np.array_equal(pr[f], fr[f][r * S_l:(r + 1) * S_l]), (r, f)
