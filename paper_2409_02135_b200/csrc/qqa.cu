@@ -1152,15 +1152,6 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
   }
   h->wsums = (long long*)(ws + L.wsums);
   if (const char* env = std::getenv("QQA_SERPENTINE")) h->serpentine = std::atoi(env) != 0;
-  if (const char* env = std::getenv("QQA_L2_PERSIST_MB")) {   // experiment: L2 set-aside for evict_last lines
-    int maxp = 0;
-    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
-    const size_t want = std::min<size_t>((size_t)std::atoi(env) << 20, (size_t)maxp);
-    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) (void)cudaGetLastError();
-    size_t got = 0;
-    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
-    std::fprintf(stderr, "qqa: persisting L2 set-aside %zu bytes (max %d)\n", got, maxp);
-  }
 
   // Graph -> device (int32 offsets). Max clique walks the complement graph.
   std::vector<int> rp32, ci_c;

@@ -547,3 +547,19 @@ def test_staged_state_kernel_parity(Q, monkeypatch, case):
     st = oracle.run(g, ocfg(problem, S, 13, **hp), gam)
     assert_state_equal(sol, st)
     assert_stats_equal(sol, st)
+
+
+def test_serpentine_block_order_is_bit_identical(Q, monkeypatch):
+    """QQA_SERPENTINE=1 sweeps the replica blocks in alternating order from step to step (an L2 experiment,
+    DESIGN.md §4, off by default): the blocks meet only in exact int64 atomics, so the bits do not change."""
+    g = gen.random_regular(2000, 20, 5)
+    monkeypatch.setenv("QQA_BLOCK_REPLICAS", "8")
+    ref = gpu(Q, g, "mis", 40, 3)
+    ref.run(oracle.schedule(-2.0, 0.1, 100)[:30])
+    monkeypatch.setenv("QQA_SERPENTINE", "1")
+    ser = gpu(Q, g, "mis", 40, 3)
+    ser.run(oracle.schedule(-2.0, 0.1, 100)[:30])
+    a, b = ref.get_state(), ser.get_state()
+    for k in ("theta", "m", "v", "p"):
+        assert np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)), k
+    assert np.array_equal(ref.get_stats()["sumD2"], ser.get_stats()["sumD2"])
