@@ -262,10 +262,9 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
         print(f"fused exchange unavailable: {e!r}", file=sys.stderr)
         ok = False
     if not agree(ok):
-        if xptrs is not None:   # this rank attached, another did not: back to a plain NCCL handle
-            sol.close()
-            sol = make_solver()
-            qdist.attach(sol, rank, world)
+        if xptrs is not None:   # this rank attached, another did not: back to the NCCL path (no new handle)
+            sol.detach_exchange()
+        sol.reset()             # collective on every rank: the statistics all-reduced over NCCL again
         return sol, None, exchange + " (fused exchange unavailable on a rank)", None
     if args.exchange == "fused":
         return sol, xptrs, "fused peer-memory exchange in k_step_x (forced)", None
@@ -278,12 +277,11 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
         print(f"reference NCCL handle failed: {e!r}", file=sys.stderr)
         ok = False
     if not agree(ok):
-        # keep the fused handle only if nothing can be checked: rebuild a plain NCCL handle instead
+        # nothing can be checked: the timed handle goes back to the NCCL path (no new allocation)
         if ref is not None:
             ref.close()
-        sol.close()
-        sol = make_solver()
-        qdist.attach(sol, rank, world)
+        sol.detach_exchange()
+        sol.reset()   # collective on every rank
         return sol, None, exchange + " (self-check handle unavailable)", None
     ref.share_comm(sol)   # collective over the ranks' NCCL communicator (all ranks reach it together)
 
@@ -304,16 +302,16 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
     if not agree(ok):
         return fallback("fused exchange failed its self-check")
 
-    def probe(s):
+    def probe(s):   # no barrier inside: a rank that raises here must not leave the others in a barrier
         s.reset()
-        barrier()
         a0, a1 = torch_event(), torch_event()
         a0.record(stream)
         s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 5)
         a1.record(stream)
-        barrier()
+        a1.synchronize()
         return a0.elapsed_time(a1) / 5
 
+    barrier()   # every rank is here (they agreed on the self-check): start the probe together
     try:
         tf, tn = probe(sol), probe(ref)
         ok = True

@@ -226,6 +226,11 @@ QQA_API int qqa_share_comm(qqa_handle* h, qqa_handle* donor);
  *   that never arrives is reported as QQA_ERR_COMM at the next synchronising call (no hang). */
 QQA_API int qqa_exchange_bytes(qqa_handle* h, size_t* bytes);
 QQA_API int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks);
+/* Back from the fused exchange to the NCCL all-reduce path (the handle's own statistic buffers; the peer
+ * buffers are no longer touched). Local, no collective; the replica state must then be re-initialised with
+ * qqa_reset or qqa_set_state (collective with a communicator) before the next run. No-op without an
+ * attached exchange. (sync) */
+QQA_API int qqa_detach_exchange(qqa_handle* h);
 QQA_API int qqa_loopback_sync_init(qqa_handle** hs, int G);
 QQA_API int qqa_loopback_run(qqa_handle** hs, int G, const float* gamma_host, int64_t n_steps);
 /* Concurrent one-GPU emulation of the fused exchange (test of its barrier / atomics protocol; DESIGN.md

@@ -1964,6 +1964,26 @@ int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int 
   return QQA_OK;
 }
 
+int qqa_detach_exchange(qqa_handle* h) {
+  if (!h) return fail(QQA_ERR_INVALID_ARG, "handle is NULL");
+  if (!h->xmode) return QQA_OK;
+  int st = set_device(h);
+  if (st) return st;
+  QQA_CUDA(cudaStreamSynchronize(h->stream));
+  for (int k = 0; k < 3; ++k) h->sums[k] = h->ws_sums[k];   // the workspace's own statistic buffers again
+  for (int r = 0; r < qqa::kMaxRanks; ++r) {
+    for (int k = 0; k < 3; ++k) h->xsums[r][k] = nullptr;
+    h->xflag[r] = nullptr;
+  }
+  h->xticket = nullptr;
+  h->xmode = false;
+  h->xrank = 0;
+  h->xG = 1;
+  h->xsync = 0;
+  if ((st = setup_overlap(h))) return st;
+  return QQA_OK;   // the replica state must be re-initialised (qqa_reset / qqa_set_state, collective) before a run
+}
+
 int qqa_step_path(qqa_handle* h, int* path) {
   if (!h || !path) return fail(QQA_ERR_INVALID_ARG, "handle or path is NULL");
   *path = h->s.kary ? QQA_PATH_KARY : h->xmode ? QQA_PATH_EXCHANGE : use_cluster(h, 2) ? QQA_PATH_CLUSTER

@@ -202,6 +202,11 @@ class Solver:
         check(lib.qqa_attach_exchange(self._h, arr, rank, nranks))
         self._exchange_keep = keep
 
+    def detach_exchange(self):
+        """Back to the NCCL path (qqa_detach_exchange); call reset() (collective) before the next run."""
+        check(lib.qqa_detach_exchange(self._h))
+        self._exchange_keep = None
+
     def share_comm(self, donor: "Solver"):
         """Join donor's communicator (no new NCCL bootstrap); collective over its ranks."""
         check(lib.qqa_share_comm(self._h, donor._h))

@@ -259,3 +259,26 @@ def test_fused_exchange_weighted_graphs(Q, kind, problem, G, S_l, hp):
         pr = sh.round_evaluate().per_replica
         for f in ("wviolations", "wcut", "energy"):
             assert np.array_equal(pr[f], fr[f][r * S_l:(r + 1) * S_l]), (r, f)
+
+
+def test_detach_exchange_returns_to_the_nccl_path(Q):
+    """qqa_detach_exchange (bench.py's fallback when a rank cannot run the fused exchange): after a fused run,
+    detach + reset gives a handle on the NCCL path that reproduces a plain NCCL handle bit for bit."""
+    import torch
+    g = gen.random_regular(2000, 10, 2)
+    mk = lambda: Q.Solver(g.rowptr, g.colidx, Q.make_config("mis", S_total=32, seed=4, comm=0.2))
+    a, b = mk(), mk()
+    for s in (a, b):
+        s.attach_comm(Q.Solver.nccl_unique_id(), 0, 1)
+    buf = torch.empty(b.exchange_bytes(), dtype=torch.uint8, device=b.device)
+    b.attach_exchange([buf.data_ptr()], 0, 1, keep=buf)
+    b.run_linear(-2.0, 0.1, 100, 0, 10)
+    b.detach_exchange()
+    assert b.step_path() != "exchange"
+    b.reset()
+    for s in (a, b):
+        s.run_linear(-2.0, 0.1, 100, 0, 40)
+    for k in ("theta", "m", "v", "p"):
+        assert np.array_equal(a.get_state()[k], b.get_state()[k]), k
+    for k in ("c", "sumD", "sumD2"):
+        assert np.array_equal(a.get_stats()[k], b.get_stats()[k]), k
