@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define QQA_ABI_VERSION 7
+#define QQA_ABI_VERSION 8
 
 #if defined(__GNUC__)
 #define QQA_API __attribute__((visibility("default")))
