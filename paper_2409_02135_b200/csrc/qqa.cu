@@ -517,6 +517,7 @@ qqa::XParams make_xparams(const qqa_handle* h, int sa, int sb, int sz, int a, in
   X.ticket = h->xticket;
   X.c_cur = h->c[a];
   X.c_next = h->c[b];
+  X.ms = h->ms;
   X.expect = (unsigned long long)h->xG * h->xsync;
   X.rank = h->xrank;
   X.G = h->xG;
