@@ -53,6 +53,23 @@ def test_c2_all_instances_one_handle(Q):
     assert res.best_replica == bu
 
 
+def test_t1_128_instances_one_handle(Q):
+    """t1 (the paper's Table 1 batch: 128 x ER(N in [700, 800], 0.15), S = 100) as ONE batched handle at full size
+    in bench.py's launch configuration (persistent kernel, non-FULL shape with pipelined index loads), 20 steps:
+    state bit-exact on the union, every instance's counts / energies / best replica / x bit-exact."""
+    w = gen.workload("t1")
+    U, gor = w.batched()
+    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
+    sol = Q.Solver(U.rowptr, U.colidx, Q.make_config("mis", S_total=w.S, seed=w.seeds[0], **hp), group_of_row=gor)
+    assert sol.n_groups == 128 and sol.step_path() == "persistent"
+    sol.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 20)
+    st = oracle.run(U, oracle.make_cfg("mis", S=w.S, seed=w.seeds[0], threads=16, **hp),
+                    oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:20])
+    assert_state_equal(sol, st)
+    assert_stats_equal(sol, st)
+    check_groups(sol.round_evaluate_groups(), U, gor, 128, "mis", st.theta)
+
+
 @pytest.mark.parametrize("problem,mp,T", [("maxcut", "clamp", 0.001), ("maxclique", "sigmoid", 0.0),
                                           ("mis", "clamp", 0.0)])
 def test_batch_full_schedule(Q, problem, mp, T):

@@ -184,3 +184,25 @@ def test_item_order_and_chunk_width_do_not_change_results(Q, monkeypatch, K, S):
             sol.run(gam)
             assert_equal_K(sol, st)
             sol.close()
+
+
+@pytest.mark.parametrize("name,steps", [("k8", 30), ("q13", 30)])
+def test_bench_colouring_workloads_full_size(Q, name, steps):
+    """The K-ary bench workloads at full size in bench.py's launch configuration (k8: N = 1e5, K = 8, S = 64,
+    chunk-major items narrowed to 8-replica chunks; q13: queen13-13, K = 13, S = 1000, colour-quad kernel):
+    P, m, v and the per-(variable, colour) statistics bit-exact after `steps` steps, then colours and
+    conflicts of every replica bit-exact."""
+    w = gen.workload(name)
+    g = w.graphs[0]
+    hp = {k: v for k, v in w.hparams().items() if k not in ("problem", "n_colors")}
+    cfg = Q.make_config("coloring", S_total=w.S, seed=w.seeds[0], n_colors=w.n_colors, **hp)
+    sol = Q.Solver(g.rowptr, g.colidx, cfg)
+    sol.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, steps)
+    ohp = {k: v for k, v in hp.items() if k not in ("map",)}
+    st = oracle.run_K(g, oracle.make_cfg("mis", S=w.S, seed=w.seeds[0], threads=16, **ohp), w.n_colors,
+                      oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:steps])
+    assert_equal_K(sol, st)
+    counts, energy, best, X = oracle.evaluate_K(g, st.P)
+    res = sol.round_evaluate()
+    assert np.array_equal(res.per_replica["violations"], counts[:, 1])
+    assert res.best_replica == best
