@@ -1498,7 +1498,18 @@ int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_
   const qqa::XEmulKernel ke = qqa::xemul_kernel(h0->s.lanes, h0->s.vpl, step_mode(h0->cfg, h0->s.weighted),
                                                 full_lanes(h0->s));
   if (!ke) return fail(QQA_ERR_UNSUPPORTED, "no emulation kernel for this layout / mode");
-  // the per-(step, rank) parameters exactly as do_steps_x would launch them, step by step
+  // the per-(step, rank) parameters exactly as do_steps_x would launch them, step by step (the handles'
+  // step counters advance while they are built; restored if the launch fails)
+  struct Saved { int cur, scur; int64_t step, launches; unsigned long long xsync; };
+  std::vector<Saved> saved((size_t)G);
+  for (int r = 0; r < G; ++r) saved[r] = {hs[r]->cur, hs[r]->scur, hs[r]->step, hs[r]->launches, hs[r]->xsync};
+  auto restore = [&](int status) {
+    for (int r = 0; r < G; ++r) {
+      hs[r]->cur = saved[r].cur; hs[r]->scur = saved[r].scur; hs[r]->step = saved[r].step;
+      hs[r]->launches = saved[r].launches; hs[r]->xsync = saved[r].xsync;
+    }
+    return status;
+  };
   std::vector<qqa::StepParams> base((size_t)G);
   std::vector<qqa::StepVar> var((size_t)n_steps * G);
   std::vector<qqa::XParams> xp((size_t)n_steps * G);
@@ -1518,19 +1529,24 @@ int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_
     }
   const size_t nb = base.size() * sizeof(qqa::StepParams), nv = var.size() * sizeof(qqa::StepVar),
                nx = xp.size() * sizeof(qqa::XParams);
+#define QQA_CUDA_R(call)                                                                          \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return restore(fail(QQA_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
   char* d = nullptr;
-  QQA_CUDA(cudaMalloc(&d, nb + nv + nx + 512));
+  QQA_CUDA_R(cudaMalloc(&d, nb + nv + nx + 512));
   struct Free { char* p; ~Free() { cudaFree(p); } } guard{d};
   char* db = d;
   char* dv = d + up(nb, 256);
   char* dx = dv + up(nv, 256);
-  QQA_CUDA(cudaMemcpyAsync(db, base.data(), nb, cudaMemcpyHostToDevice, h0->stream));
-  QQA_CUDA(cudaMemcpyAsync(dv, var.data(), nv, cudaMemcpyHostToDevice, h0->stream));
-  QQA_CUDA(cudaMemcpyAsync(dx, xp.data(), nx, cudaMemcpyHostToDevice, h0->stream));
+  QQA_CUDA_R(cudaMemcpyAsync(db, base.data(), nb, cudaMemcpyHostToDevice, h0->stream));
+  QQA_CUDA_R(cudaMemcpyAsync(dv, var.data(), nv, cudaMemcpyHostToDevice, h0->stream));
+  QQA_CUDA_R(cudaMemcpyAsync(dx, xp.data(), nx, cudaMemcpyHostToDevice, h0->stream));
   int per_sm = 0;
-  QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)ke, 256, 0));
+  QQA_CUDA_R(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)ke, 256, 0));
   const int cta_per_rank = std::max(1, per_sm * h0->sm_count / G);
-  if ((int64_t)per_sm * h0->sm_count < G) return fail(QQA_ERR_UNSUPPORTED, "too few co-resident CTAs for G ranks");
+  if ((int64_t)per_sm * h0->sm_count < G) return restore(fail(QQA_ERR_UNSUPPORTED, "too few co-resident CTAs for G ranks"));
   qqa::XEmulParams E{};
   E.base = reinterpret_cast<const qqa::StepParams*>(db);
   E.var = reinterpret_cast<const qqa::StepVar*>(dv);
@@ -1539,7 +1555,8 @@ int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_
   E.nsteps = (int)n_steps;
   E.cta_per_rank = cta_per_rank;
   void* args[] = {(void*)&E};
-  QQA_CUDA(cudaLaunchCooperativeKernel((const void*)ke, dim3(G * cta_per_rank), dim3(256), args, 0, h0->stream));
+  QQA_CUDA_R(cudaLaunchCooperativeKernel((const void*)ke, dim3(G * cta_per_rank), dim3(256), args, 0, h0->stream));
+#undef QQA_CUDA_R
   QQA_CUDA(cudaStreamSynchronize(h0->stream));
   return QQA_OK;
 }
