@@ -242,10 +242,13 @@ def emit(line: dict) -> None:
 
 
 def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, stream, barrier, max_over_ranks):
-    """N > 1: the per-step statistics exchange. Every phase that can fail on one rank (symmetric-memory
-    attach, the reference handle, the bit-exact self-check against NCCL, the timing probe) is wrapped,
-    and the ranks agree (MIN all-reduce) before the next collective phase, so a failure anywhere sends
-    every rank back to the NCCL handle instead of leaving the others waiting in a collective.
+    """N > 1: the per-step statistics exchange. Candidates: the NCCL all-reduce, the fused exchange with remote
+    atomics into the owner rows ("atomic") and the owner-slotted fused exchange ("slotted": plain stores into
+    per-writer slots at the owner, owner-side sum, no remote atomics). Each fused mode must pass a bit-exact
+    self-check against NCCL; the fastest exact one (max over ranks) is kept. Every phase that can fail on one
+    rank (attach, the reference handle, a self-check, a probe) is wrapped, and the ranks agree (MIN all-reduce)
+    before the next collective phase, so a failure anywhere sends every rank back to the NCCL path instead of
+    leaving the others waiting in a collective.
     Returns (solver, peer pointers or None, description, probe times or None)."""
     exchange = "nccl all-reduce (2-chunk overlap)"
     if args.exchange == "nccl" or w.n_colors:
@@ -254,9 +257,10 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
     def agree(ok: bool) -> bool:
         return qdist.all_ranks(ok, device=dev)
 
+    first = "slotted" if args.exchange == "slotted" else "atomic"
     xptrs = None
     try:
-        xptrs = qdist.attach_exchange(sol, rank, world)
+        xptrs = qdist.attach_exchange(sol, rank, world, mode=first)
         ok = True
     except Exception as e:   # no symmetric memory / peer mapping here: stay on NCCL
         print(f"fused exchange unavailable: {e!r}", file=sys.stderr)
@@ -266,8 +270,8 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
             sol.detach_exchange()
         sol.reset()             # collective on every rank: the statistics all-reduced over NCCL again
         return sol, None, exchange + " (fused exchange unavailable on a rank)", None
-    if args.exchange == "fused":
-        return sol, xptrs, "fused peer-memory exchange in k_step_x (forced)", None
+    if args.exchange in ("fused", "slotted"):
+        return sol, xptrs, f"fused peer-memory exchange ({first}, forced)", None
 
     ref = None
     try:
@@ -285,22 +289,18 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
         return sol, None, exchange + " (self-check handle unavailable)", None
     ref.share_comm(sol)   # collective over the ranks' NCCL communicator (all ranks reach it together)
 
-    def fallback(why):
-        sol.close()
-        return ref, None, exchange + f" ({why})", None
-
-    try:   # bit-exact self-check of the fused exchange against NCCL, 3 steps
-        for s in (sol, ref):
-            s.reset()
-            s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 3)
-        a, b = sol.get_state(), ref.get_state()
-        ok = all(np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)) for k in ("theta", "m", "v", "p"))
-        ok = ok and np.array_equal(sol.get_stats()["sumD2"], ref.get_stats()["sumD2"])
-    except Exception as e:
-        print(f"fused-exchange self-check raised: {e!r}", file=sys.stderr)
-        ok = False
-    if not agree(ok):
-        return fallback("fused exchange failed its self-check")
+    def self_check() -> bool:   # bit-exact against NCCL, 3 steps
+        try:
+            for s in (sol, ref):
+                s.reset()
+                s.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 3)
+            a, b = sol.get_state(), ref.get_state()
+            ok = all(np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)) for k in ("theta", "m", "v", "p"))
+            ok = ok and np.array_equal(sol.get_stats()["sumD2"], ref.get_stats()["sumD2"])
+        except Exception as e:
+            print(f"fused-exchange self-check raised: {e!r}", file=sys.stderr)
+            ok = False
+        return agree(ok)
 
     def probe(s):   # no barrier inside: a rank that raises here must not leave the others in a barrier
         s.reset()
@@ -311,21 +311,50 @@ def select_exchange(args, w, Q, qdist, sol, make_solver, rank, world, dev, strea
         a1.synchronize()
         return a0.elapsed_time(a1) / 5
 
-    barrier()   # every rank is here (they agreed on the self-check): start the probe together
-    try:
-        tf, tn = probe(sol), probe(ref)
+    def timed(s):
+        barrier()   # every rank is here (they agreed on the self-check): start the probe together
+        try:
+            t, ok = probe(s), True
+        except Exception as e:
+            print(f"exchange probe raised: {e!r}", file=sys.stderr)
+            t, ok = 0.0, False
+        return max_over_ranks(t) if agree(ok) else None
+
+    probe_ms = {"nccl_ms_per_step": timed(ref)}
+    if probe_ms["nccl_ms_per_step"] is None:
+        sol.close()
+        return ref, None, exchange + " (probe failed)", None
+    for mode in ("atomic", "slotted"):
+        if mode != first:   # re-attach the same buffers in the other mode (collective)
+            try:
+                sol.attach_exchange(xptrs, rank, world, keep=sol._exchange_keep, mode=mode)
+                ok = True
+            except Exception as e:
+                print(f"{mode} exchange unavailable: {e!r}", file=sys.stderr)
+                ok = False
+            if not agree(ok):
+                continue
+        if self_check():
+            probe_ms[f"{mode}_ms_per_step"] = timed(sol)
+    fused = {m: probe_ms.get(f"{m}_ms_per_step") for m in ("atomic", "slotted")}
+    fused = {m: t for m, t in fused.items() if t is not None}
+    best = min(fused, key=fused.get) if fused else None
+    if best is None or qdist.pick_exchange(fused[best], probe_ms["nccl_ms_per_step"]) == "nccl":
+        sol.close()
+        why = "faster than the fused exchanges here" if fused else "fused exchanges failed their self-check"
+        return ref, None, exchange + f" ({why})", probe_ms
+    ref.close()
+    try:   # the handle is attached in the last mode tried; switch if the other one won (collective)
+        sol.attach_exchange(xptrs, rank, world, keep=sol._exchange_keep, mode=best)
         ok = True
     except Exception as e:
-        print(f"exchange probe raised: {e!r}", file=sys.stderr)
-        tf, tn, ok = 0.0, 0.0, False
+        print(f"re-attaching the {best} exchange failed: {e!r}", file=sys.stderr)
+        ok = False
     if not agree(ok):
-        return fallback("exchange probe failed")
-    probe_ms = {"fused_ms_per_step": max_over_ranks(tf), "nccl_ms_per_step": max_over_ranks(tn)}
-    if qdist.pick_exchange(probe_ms["fused_ms_per_step"], probe_ms["nccl_ms_per_step"]) == "nccl":
-        sol.close()
-        return ref, None, exchange + " (faster than the fused exchange here)", probe_ms
-    ref.close()
-    return sol, xptrs, "fused peer-memory exchange in k_step_x", probe_ms
+        sol.detach_exchange()
+        sol.reset()
+        return sol, None, exchange + " (fused re-attach failed)", probe_ms
+    return sol, xptrs, f"fused peer-memory exchange ({best})", probe_ms
 
 
 def torch_event():
@@ -349,9 +378,10 @@ def main():
     ap.add_argument("--temperature", type=float, default=None, help="Langevin T (NEXT-2; the paper: 0.001)")
     ap.add_argument("--alpha", type=int, default=None, help="override the alpha-entropy exponent (the paper: 4, P:244)")
     ap.add_argument("--lr", type=float, default=None, help="override the AdamW learning rate (the paper: 1, 0.1 or 0.01, P:670)")
-    ap.add_argument("--exchange", choices=["auto", "fused", "nccl"], default="auto",
+    ap.add_argument("--exchange", choices=["auto", "fused", "slotted", "nccl"], default="auto",
                     help="N > 1: per-step statistics exchange -- fused peer-memory exchange inside the step "
-                         "kernel (auto: after a bit-exact self-check against NCCL) or the NCCL all-reduce")
+                         "kernel with remote atomics (fused) or owner slots (slotted), the NCCL all-reduce, or "
+                         "auto: the fastest of them that passes a bit-exact self-check against NCCL")
     ap.add_argument("--force-dist", action="store_true",
                     help="diagnostics: run the N > 1 code path (process group, NCCL communicator, exchange) at N = 1")
     ap.add_argument("--replicas", type=int, default=None, help="override S (diagnostics: per-rank work of a sharded run)")
@@ -510,7 +540,7 @@ def main():
             if sharded:
                 s.share_comm(sol)
                 if xptrs is not None:   # re-attach the (now idle) exchange buffers of the timed handle
-                    s.attach_exchange(xptrs, rank, world)
+                    s.attach_exchange(xptrs, rank, world, mode=sol._exchange_mode)
             s.run_linear(w.gamma_min, w.gamma_max, w.steps)
             r = (s.round_evaluate_groups(want_x=True, want_counts=True) if gp is not None
                  else s.round_evaluate(want_x=True, want_replicas=True))
@@ -563,8 +593,9 @@ def main():
                              "dram_frac_vs_compulsory": (traffic / Bc) if traffic else None,
                              "kernel": ("qqa::k_step_K (fused K-ary gather + gradient + AdamW + normalise + stats)"
                                         if w.n_colors else
-                                        "qqa::k_step_x (fused gather + gradient + AdamW + stats + peer exchange)"
-                                        if xptrs is not None else "qqa::k_step (fused gather + gradient + AdamW + stats)"),
+                                        "qqa::k_step_x / k_step_xs (fused gather + gradient + AdamW + stats + peer "
+                                        "exchange)" if xptrs is not None
+                                        else "qqa::k_step (fused gather + gradient + AdamW + stats)"),
                              "bytes_per_launch": B, "avg_launch_ms": avg_kernel_s * 1e3,
                              "launches_timed": kern_launches, "peak_source": peak_src,
                              "kernel_timing": "per-launch CUDA events on the launching stream in a separate "

@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define QQA_ABI_VERSION 8
+#define QQA_ABI_VERSION 9
 
 #if defined(__GNUC__)
 #define QQA_API __attribute__((visibility("default")))
@@ -226,6 +226,14 @@ QQA_API int qqa_share_comm(qqa_handle* h, qqa_handle* donor);
  *   that never arrives is reported as QQA_ERR_COMM at the next synchronising call (no hang). */
 QQA_API int qqa_exchange_bytes(qqa_handle* h, size_t* bytes);
 QQA_API int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks);
+/* The same with a choice of exchange: QQA_EXCHANGE_ATOMIC (each rank adds its partials into the owner's rows
+ * with remote int64 atomics, one barrier per step) or QQA_EXCHANGE_SLOTTED (each rank STORES its partials into
+ * its own slot at the owner -- coalesced plain stores, no remote atomics; after a barrier the owner sums the G
+ * slots of its rows, after a second barrier every rank reads the totals; one cooperative step launch with both
+ * barriers; needs one replica block). Both bit-identical to the NCCL path. INVALID_ARG / UNSUPPORTED as above.
+ * (sync) */
+enum { QQA_EXCHANGE_ATOMIC = 0, QQA_EXCHANGE_SLOTTED = 1 };
+QQA_API int qqa_attach_exchange_mode(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks, int mode);
 /* Back from the fused exchange to the NCCL all-reduce path (the handle's own statistic buffers; the peer
  * buffers are no longer touched). Local, no collective; the replica state must then be re-initialised with
  * qqa_reset or qqa_set_state (collective with a communicator) before the next run. No-op without an

@@ -70,6 +70,7 @@ def _declare(lib):
         "qqa_loopback_run": (ctypes.c_int, [P, ctypes.c_int, P, i64]),
         "qqa_exchange_emulate": (ctypes.c_int, [P, ctypes.c_int, P, i64]),
         "qqa_detach_exchange": (ctypes.c_int, [H]),
+        "qqa_attach_exchange_mode": (ctypes.c_int, [H, P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "qqa_run": (ctypes.c_int, [H, P, i64]),
         "qqa_run_linear": (ctypes.c_int, [H, ctypes.c_float, ctypes.c_float, i64, i64, i64]),
         "qqa_round_evaluate": (ctypes.c_int, [H, P, ctypes.POINTER(ctypes.c_int32),

@@ -48,6 +48,19 @@ StepKernel stage_for(int lanes) {
   return nullptr;
 }
 
+// k_step_xs (owner-slotted exchange): the same shapes and modes as k_step_x.
+template <int M>
+XStepKernel xsstep_for(int lanes, int vpl, bool full) {
+  if (M & kModeSparseClique) return nullptr;
+#define QQA_XSCASE(L, V) \
+  if (lanes == L && vpl == V) \
+    return full ? k_step_xs<L, V, (M & 11), true> : k_step_xs<L, V, (M & 11), false>;
+  QQA_XSCASE(1, 1) QQA_XSCASE(2, 1) QQA_XSCASE(4, 1) QQA_XSCASE(8, 1) QQA_XSCASE(16, 1)
+  QQA_XSCASE(32, 1) QQA_XSCASE(32, 2) QQA_XSCASE(32, 4)
+#undef QQA_XSCASE
+  return nullptr;
+}
+
 template <int M>
 RunKernel run_kernel_for(int lanes, int vpl, int cta, bool full) {
   if (M & kModeSparseClique) return nullptr;   // its column sums need a pass between steps: no k_run

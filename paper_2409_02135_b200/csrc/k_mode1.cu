@@ -5,5 +5,6 @@ namespace qqa {
 StepKernel step_kernel_m1(int lanes, int vpl, bool full) { return step_for<1>(lanes, vpl, full); }
 RunKernel run_kernel_m1(int lanes, int vpl, int cta, bool full) { return run_kernel_for<1>(lanes, vpl, cta, full); }
 XStepKernel xstep_kernel_m1(int lanes, int vpl, bool full) { return xstep_for<1>(lanes, vpl, full); }
+XStepKernel xsstep_kernel_m1(int lanes, int vpl, bool full) { return xsstep_for<1>(lanes, vpl, full); }
 StepKernel stage_kernel_m1(int lanes) { return stage_for<1>(lanes); }
 }  // namespace qqa

@@ -5,4 +5,5 @@ namespace qqa {
 StepKernel step_kernel_m11(int lanes, int vpl, bool full) { return step_for<11>(lanes, vpl, full); }
 RunKernel run_kernel_m11(int lanes, int vpl, int cta, bool full) { return run_kernel_for<11>(lanes, vpl, cta, full); }
 XStepKernel xstep_kernel_m11(int lanes, int vpl, bool full) { return xstep_for<11>(lanes, vpl, full); }
+XStepKernel xsstep_kernel_m11(int lanes, int vpl, bool full) { return xsstep_for<11>(lanes, vpl, full); }
 }  // namespace qqa

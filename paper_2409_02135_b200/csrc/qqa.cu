@@ -358,6 +358,10 @@ struct qqa_handle {
   unsigned long long* xflag[qqa::kMaxRanks] = {};
   unsigned int* xticket = nullptr;
   unsigned long long xsync = 0;                  // barriers so far (each adds G arrivals to every counter)
+  bool xslotted = false;                         // owner-slotted exchange (k_step_xs) instead of atomics
+  bool xdefer_init = false;                      // slotted, no communicator: qqa_loopback_sync_init scatters
+  long long* xbase[qqa::kMaxRanks] = {};         // every rank's exchange buffer (slots, then totals)
+  int grid_xs = 0;                               // co-resident grid of k_step_xs (cooperative launch)
   long long* ws_sums[3] = {nullptr, nullptr, nullptr};   // the workspace's own sums (get_stats scratch)
   int cluster_cs = 0;          // k_run_cluster: CTAs per cluster (0: not available for this handle)
   qqa::StepKKernel kq = nullptr;    // K-ary colour-quad step (KP 12 / 16), nullptr: k_step_K
@@ -522,7 +526,31 @@ qqa::XParams make_xparams(const qqa_handle* h, int sa, int sb, int sz, int a, in
   X.rank = h->xrank;
   X.G = h->xG;
   X.rows_per_rank = std::max(1, (h->s.n + h->xG - 1) / h->xG);
+  if (h->xslotted) {   // slots [2 parities][G][2][rpr] then totals [2][rpr] in every rank's buffer
+    const size_t rpr = (size_t)X.rows_per_rank, G = (size_t)h->xG;
+    const size_t pw = (size_t)((h->step + 1) & 1), pr = (size_t)(h->step & 1);   // step t = h->step + 1
+    for (int r = 0; r < h->xG; ++r) {
+      X.slot_w[r] = h->xbase[r] + ((pw * G + (size_t)h->xrank) * 2) * rpr;
+      X.totals[r] = h->xbase[r] + 2 * G * 2 * rpr;
+    }
+    X.slot_r = h->xbase[h->xrank] + (pr * G) * 2 * rpr;
+  }
   return X;
+}
+
+// Owner-slotted exchange: this rank's partial sums of the initial statistics (sums[0], not all-reduced)
+// into its slot (parity 0) at every owner; the arrival that follows ends "step 0".
+int xs_scatter_init(qqa_handle* h) {
+  qqa::XParams X = make_xparams(h, h->scur, h->scur, h->scur, h->cur, h->cur);
+  const size_t rpr = (size_t)X.rows_per_rank, G = (size_t)h->xG;
+  for (int r = 0; r < h->xG; ++r) X.slot_w[r] = h->xbase[r] + ((0 * G + (size_t)h->xrank) * 2) * rpr;
+  if (h->s.n > 0) {
+    const int blocks = std::max(1, std::min((h->s.n + 255) / 256, h->sm_count * 8));
+    qqa::k_xs_scatter<<<blocks, 256, 0, h->stream>>>(X, h->s.n, h->sums[0]);
+    QQA_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  return QQA_OK;
 }
 
 // This rank's arrival at an exchange barrier (after the initial statistics are complete).
@@ -545,6 +573,20 @@ qqa::XStepKernel pick_xstep(int lanes, int vpl, int mode, bool full) {
     case 9: return qqa::xstep_kernel_m9(lanes, vpl, full);
     case 10: return qqa::xstep_kernel_m10(lanes, vpl, full);
     case 11: return qqa::xstep_kernel_m11(lanes, vpl, full);
+    default: return nullptr;
+  }
+}
+
+qqa::XStepKernel pick_xsstep(int lanes, int vpl, int mode, bool full) {
+  switch (mode) {
+    case 0: return qqa::xsstep_kernel_m0(lanes, vpl, full);
+    case 1: return qqa::xsstep_kernel_m1(lanes, vpl, full);
+    case 2: return qqa::xsstep_kernel_m2(lanes, vpl, full);
+    case 3: return qqa::xsstep_kernel_m3(lanes, vpl, full);
+    case 8: return qqa::xsstep_kernel_m8(lanes, vpl, full);
+    case 9: return qqa::xsstep_kernel_m9(lanes, vpl, full);
+    case 10: return qqa::xsstep_kernel_m10(lanes, vpl, full);
+    case 11: return qqa::xsstep_kernel_m11(lanes, vpl, full);
     default: return nullptr;
   }
 }
@@ -573,12 +615,16 @@ int launch_init(qqa_handle* h, bool use_given, const float* c_given) {
     QQA_CUDA(cudaGetLastError());
     h->launches++;
   }
-  if (h->comm) {
+  if (h->comm && !h->xslotted) {
     QQA_NCCL(ncclAllReduce(h->sums[0], h->sums[0], 2 * (size_t)h->s.n, ncclInt64, ncclSum, h->comm, h->stream));
   }
   h->cur = 0;
   h->scur = 0;
-  if (h->xmode && h->comm) {   // every rank's sums[0] holds the totals: first exchange barrier
+  if (h->xslotted && !h->xdefer_init) {   // slotted: partials to the owners' slots, then the first barrier
+    int st;
+    if ((st = xs_scatter_init(h))) return st;
+    if ((st = x_arrive(h))) return st;
+  } else if (h->xmode && h->comm && !h->xslotted) {   // every rank's sums[0] holds the totals: first barrier
     int st;
     if ((st = x_arrive(h))) return st;
   }
@@ -904,11 +950,39 @@ int do_steps_x(qqa_handle* h, const float* gamma, int64_t n_steps) {
   return QQA_OK;
 }
 
+// Owner-slotted exchange steps: one cooperative k_step_xs launch per step (two barrier arrivals each:
+// after the owner reduction and after the step).
+int do_steps_xs(qqa_handle* h, const float* gamma, int64_t n_steps) {
+  const qqa::XStepKernel kx = pick_xsstep(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), full_lanes(h->s));
+  if (!kx || h->grid_xs <= 0) return fail(QQA_ERR_UNSUPPORTED, "no owner-slotted exchange kernel for this layout");
+  qqa::StepParams P = xstep_base(h);
+  for (int64_t k = 0; k < n_steps; ++k) {
+    const int64_t t = h->step + 1;
+    P.var = xstep_var(h, gamma[k]);
+    const int a = h->cur, b = h->cur ^ 1;
+    const int sb = (h->scur + 1) % 3;
+    if (h->s.n > 0) {
+      qqa::XParams X = make_xparams(h, h->scur, sb, (h->scur + 2) % 3, a, b);
+      void* args[] = {(void*)&P, (void*)&X};
+      int st;
+      if ((st = record_start(h))) return st;
+      QQA_CUDA(cudaLaunchCooperativeKernel((const void*)kx, dim3(h->grid_xs), dim3(256), args, 0, h->stream));
+      h->launches++;
+      h->xsync += 2;
+      if ((st = record_end(h))) return st;
+    }
+    h->cur = b;
+    h->scur = sb;
+    h->step = t;
+  }
+  return QQA_OK;
+}
+
 int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   if (n_steps < 0) return fail(QQA_ERR_INVALID_ARG, "n_steps < 0");
   if (n_steps > 0 && !gamma) return fail(QQA_ERR_INVALID_ARG, "gamma is NULL");
   if (h->s.kary) return do_steps_kary(h, gamma, n_steps);
-  if (h->xmode) return do_steps_x(h, gamma, n_steps);
+  if (h->xmode) return h->xslotted ? do_steps_xs(h, gamma, n_steps) : do_steps_x(h, gamma, n_steps);
   if (use_cluster(h, n_steps)) return do_steps_cluster(h, gamma, n_steps);
   if (use_persistent(h, n_steps)) return do_steps_persistent(h, gamma, n_steps);
   StepKernel ks;
@@ -1454,6 +1528,16 @@ int qqa_loopback_sync_init(qqa_handle** hs, int G) {
   int st = check_loopback(hs, G);
   if (st) return st;
   if ((st = set_device(hs[0]))) return st;
+  if (hs[0]->xslotted) {   // owner-slotted shards: every buffer is zeroed now; scatter the partials, arrive
+    for (int r = 0; r < G; ++r) {
+      if (!hs[r]->xdefer_init) continue;
+      if ((st = xs_scatter_init(hs[r]))) return st;
+      if ((st = x_arrive(hs[r]))) return st;
+      hs[r]->xdefer_init = false;
+    }
+    QQA_CUDA(cudaStreamSynchronize(hs[0]->stream));
+    return QQA_OK;
+  }
   if ((st = loopback_reduce(hs, G))) return st;
   for (int r = 0; r < G; ++r)   // fused-exchange shards: the totals are in place, first barrier
     if (hs[r]->xmode && (st = x_arrive(hs[r]))) return st;
@@ -1488,7 +1572,8 @@ int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_
     if (h->device != hs[0]->device || h->stream != hs[0]->stream || h->s.n != hs[0]->s.n ||
         h->s.lanes != hs[0]->s.lanes || h->s.vpl != hs[0]->s.vpl || h->s.SB != hs[0]->s.SB ||
         step_mode(h->cfg, h->s.weighted) != step_mode(hs[0]->cfg, hs[0]->s.weighted) || h->step != hs[0]->step ||
-        h->cur != hs[0]->cur || h->scur != hs[0]->scur || h->xsync != hs[0]->xsync)
+        h->cur != hs[0]->cur || h->scur != hs[0]->scur || h->xsync != hs[0]->xsync ||
+        h->xslotted != hs[0]->xslotted)
       return fail(QQA_ERR_INVALID_ARG, "emulated shards must share device, stream, layout, mode and be in lockstep");
   }
   qqa_handle* h0 = hs[0];
@@ -1521,7 +1606,7 @@ int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_
       const int sa = h->scur, sb = (h->scur + 1) % 3, sz = (h->scur + 2) % 3;
       var[(size_t)k * G + r] = xstep_var(h, gamma_host[k]);
       xp[(size_t)k * G + r] = make_xparams(h, sa, sb, sz, a, b);
-      h->xsync++;
+      h->xsync += h->xslotted ? 2 : 1;
       h->cur = b;
       h->scur = sb;
       h->step += 1;
@@ -1554,6 +1639,7 @@ int qqa_exchange_emulate(qqa_handle** hs, int G, const float* gamma_host, int64_
   E.G = G;
   E.nsteps = (int)n_steps;
   E.cta_per_rank = cta_per_rank;
+  E.slotted = h0->xslotted ? 1 : 0;
   void* args[] = {(void*)&E};
   QQA_CUDA_R(cudaLaunchCooperativeKernel((const void*)ke, dim3(G * cta_per_rank), dim3(256), args, 0, h0->stream));
 #undef QQA_CUDA_R
@@ -1861,10 +1947,13 @@ int qqa_get_stats(qqa_handle* h, float* c, int64_t* sumD, int64_t* sumD2) {
   const long long* sums = h->sums[h->scur];
   if (h->xmode && n && (sumD || sumD2)) {   // owner rows hold the totals: gather them into the scratch
     const qqa::XParams X = make_xparams(h, h->scur, h->scur, h->scur, h->cur, h->cur);
-    qqa::k_x_gather<<<std::max(1, std::min((int)((n + 255) / 256), h->sm_count * 8)), 256, 0, h->stream>>>(
-        X, (int)n, h->ws_sums[0], h->flag);
+    const int blocks = std::max(1, std::min((int)((n + 255) / 256), h->sm_count * 8));
+    if (h->xslotted)   // the current statistics are the G writers' slots of parity (step & 1) at each owner
+      qqa::k_xs_gather<<<blocks, 256, 0, h->stream>>>(X, (int)n, (int)(h->step & 1), h->ws_sums[2], h->flag);
+    else
+      qqa::k_x_gather<<<blocks, 256, 0, h->stream>>>(X, (int)n, h->ws_sums[0], h->flag);
     QQA_CUDA(cudaGetLastError());
-    sums = h->ws_sums[0];
+    sums = h->xslotted ? h->ws_sums[2] : h->ws_sums[0];
   }
   if (sumD && n)
     QQA_CUDA(cudaMemcpyAsync(sumD, sums, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
@@ -1936,14 +2025,29 @@ int qqa_launch_count(qqa_handle* h, int64_t* launches) {
   return QQA_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Exchange buffer of one rank: atomics mode: sums [3][2][n]; slotted mode: slots [2][G][2][ceil(n/G)] then
+// totals [2][ceil(n/G)] (at most 48 n + 4 KB bytes for G <= 8); the arrival counter and ticket after both.
+size_t xflag_offset(const qqa_handle* h) { return 6 * (size_t)h->s.n * sizeof(long long) + 4096; }
+}  // namespace
+
+extern "C" {
+
 int qqa_exchange_bytes(qqa_handle* h, size_t* bytes) {
   if (!h || !bytes) return fail(QQA_ERR_INVALID_ARG, "handle or bytes is NULL");
-  *bytes = 6 * (size_t)h->s.n * sizeof(long long) + 256;   // sums [3][2][n], arrival counter, ticket
+  *bytes = xflag_offset(h) + 256;   // statistics region, then the arrival counter and ticket
   return QQA_OK;
 }
 
 int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks) {
+  return qqa_attach_exchange_mode(h, peer_bufs, rank, nranks, QQA_EXCHANGE_ATOMIC);
+}
+
+int qqa_attach_exchange_mode(qqa_handle* h, const uint64_t* peer_bufs, int rank, int nranks, int mode) {
   if (!h || !peer_bufs) return fail(QQA_ERR_INVALID_ARG, "handle or peer_bufs is NULL");
+  if (mode != QQA_EXCHANGE_ATOMIC && mode != QQA_EXCHANGE_SLOTTED) return fail(QQA_ERR_INVALID_ARG, "unknown exchange mode");
   if (nranks < 1 || nranks > qqa::kMaxRanks || rank < 0 || rank >= nranks)
     return fail(QQA_ERR_INVALID_ARG, "need 1 <= nranks <= 8 and 0 <= rank < nranks");
   if (h->s.kary || (step_mode(h->cfg, h->s.weighted) & qqa::kModeSparseClique))
@@ -1952,23 +2056,49 @@ int qqa_attach_exchange(qqa_handle* h, const uint64_t* peer_bufs, int rank, int 
     return fail(QQA_ERR_INVALID_ARG, "sharding must be S_total = nranks * S_local and replica_offset = rank * S_local");
   if (h->comm && (h->rank != rank || h->nranks != nranks))
     return fail(QQA_ERR_INVALID_ARG, "rank / nranks differ from the attached communicator");
-  if (!pick_xstep(h->s.lanes, h->s.vpl, step_mode(h->cfg, h->s.weighted), full_lanes(h->s)))
+  const bool slotted = mode == QQA_EXCHANGE_SLOTTED;
+  const int smode = step_mode(h->cfg, h->s.weighted);
+  if (!pick_xstep(h->s.lanes, h->s.vpl, smode, full_lanes(h->s)))
     return fail(QQA_ERR_UNSUPPORTED, "no fused-exchange kernel for this replica layout");
+  const qqa::XStepKernel kxs = slotted ? pick_xsstep(h->s.lanes, h->s.vpl, smode, full_lanes(h->s)) : nullptr;
+  if (slotted && (h->s.B != 1 || !kxs))
+    return fail(QQA_ERR_UNSUPPORTED, "the owner-slotted exchange needs one replica block (S_local <= 32 per 128 MB)");
   int st = set_device(h);
   if (st) return st;
+  int grid_xs = 0;
+  if (slotted) {   // cooperative launch: every CTA of the step kernel resident (the mid-kernel barrier)
+    int per_sm = 0, coop = 0;
+    QQA_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device));
+    QQA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kxs, 256, 0));
+    if (!coop || per_sm < 1) return fail(QQA_ERR_UNSUPPORTED, "no cooperative launch for the owner-slotted exchange");
+    const int need = (int)std::max<int64_t>(1, ((int64_t)h->s.n * h->s.lanes + 255) / 256);
+    grid_xs = std::max(1, std::min(need, per_sm * h->sm_count));
+  }
   const size_t n2 = 2 * (size_t)h->s.n;
   for (int r = 0; r < nranks; ++r) {
     if (!peer_bufs[r] || peer_bufs[r] % 256) return fail(QQA_ERR_INVALID_ARG, "peer buffer NULL or not 256-byte aligned");
     long long* base = reinterpret_cast<long long*>(peer_bufs[r]);
+    h->xbase[r] = base;
     for (int k = 0; k < 3; ++k) h->xsums[r][k] = base + k * n2;
-    h->xflag[r] = reinterpret_cast<unsigned long long*>(base + 3 * n2);
+    h->xflag[r] = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + xflag_offset(h));
   }
   if (!h->xmode)
     for (int k = 0; k < 3; ++k) h->ws_sums[k] = h->sums[k];
   h->xticket = reinterpret_cast<unsigned int*>(h->xflag[rank] + 1);
-  QQA_CUDA(cudaMemsetAsync(h->xsums[rank][0], 0, 3 * n2 * sizeof(long long) + 256, h->stream));
+  QQA_CUDA(cudaMemsetAsync(h->xbase[rank], 0, xflag_offset(h) + 256, h->stream));
   QQA_CUDA(cudaStreamSynchronize(h->stream));
-  for (int k = 0; k < 3; ++k) h->sums[k] = h->xsums[rank][k];
+  if (slotted) {   // the handle's own buffers keep the local partials (init); the exchange lives in the slots
+    for (int k = 0; k < 3; ++k) h->sums[k] = h->ws_sums[k];
+    if (h->comm) {  // every rank's buffer is zeroed before any rank scatters into it: a collective in between
+      QQA_NCCL(ncclAllReduce(h->best, h->best, 1, ncclInt32, ncclSum, h->comm, h->stream));
+    }
+    h->xdefer_init = (h->comm == nullptr);   // emulated shards: qqa_loopback_sync_init scatters and arrives
+  } else {
+    for (int k = 0; k < 3; ++k) h->sums[k] = h->xsums[rank][k];
+    h->xdefer_init = false;
+  }
+  h->xslotted = slotted;
+  h->grid_xs = grid_xs;
   h->xmode = true;
   h->xrank = rank;
   h->xG = nranks;
@@ -1994,6 +2124,9 @@ int qqa_detach_exchange(qqa_handle* h) {
     h->xflag[r] = nullptr;
   }
   h->xticket = nullptr;
+  for (int r = 0; r < qqa::kMaxRanks; ++r) h->xbase[r] = nullptr;
+  h->xslotted = false;
+  h->xdefer_init = false;
   h->xmode = false;
   h->xrank = 0;
   h->xG = 1;

@@ -54,6 +54,15 @@ XStepKernel xstep_kernel_m8(int lanes, int vpl, bool full);
 XStepKernel xstep_kernel_m9(int lanes, int vpl, bool full);
 XStepKernel xstep_kernel_m10(int lanes, int vpl, bool full);
 XStepKernel xstep_kernel_m11(int lanes, int vpl, bool full);
+// k_step_xs<lanes, vpl, MODE> (owner-slotted exchange), the same modes; nullptr otherwise.
+XStepKernel xsstep_kernel_m0(int lanes, int vpl, bool full);
+XStepKernel xsstep_kernel_m1(int lanes, int vpl, bool full);
+XStepKernel xsstep_kernel_m2(int lanes, int vpl, bool full);
+XStepKernel xsstep_kernel_m3(int lanes, int vpl, bool full);
+XStepKernel xsstep_kernel_m8(int lanes, int vpl, bool full);
+XStepKernel xsstep_kernel_m9(int lanes, int vpl, bool full);
+XStepKernel xsstep_kernel_m10(int lanes, int vpl, bool full);
+XStepKernel xsstep_kernel_m11(int lanes, int vpl, bool full);
 
 // k_step_x_emul<lanes, 1, MODE> (one-GPU concurrent emulation of the fused exchange, k_xemul.cu):
 // lanes 1..8, vpl 1, MODE 0..3 and 8..11; nullptr otherwise.

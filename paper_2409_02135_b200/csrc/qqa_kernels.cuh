@@ -491,7 +491,8 @@ template <int LANES, int VPL, int MODE, bool FULL = false, bool STAGE = false>
 __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
                                           unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false,
                                           long long* sums_dst = nullptr, long long* zero_dst = nullptr,
-                                          const float4* stage = nullptr, int nb = -1, int ni = -1) {
+                                          const float4* stage = nullptr, int nb = -1, int ni = -1,
+                                          int slot_stride = 0) {
       const int SB8 = P.SB >> 3;
       const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
       const float* __restrict__ pc = V.p_cur + blk;
@@ -677,7 +678,9 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
         st8_stream(P.v + at, vv);
         st8_pnext(V.p_next + at, pn);
       }
-      if (force_atomic)   // fused exchange: the owner's buffers (atomics across ranks and blocks)
+      if (slot_stride > 0)   // owner-slotted exchange: plain stores into this rank's slot at the owner (B = 1)
+        publish_sums<LANES>(sD, sD2, gmask, lane, i, b, slot_stride, 1, sums_dst, nullptr);
+      else if (force_atomic)   // fused exchange: the owner's buffers (atomics across ranks and blocks)
         publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, 2, sums_dst, zero_dst);
       else
         publish_sums<LANES>(sD, sD2, gmask, lane, i, b, P.n, P.B, V.sums_next, V.sums_zero);
@@ -758,21 +761,27 @@ struct XParams {
   float2* ms;                           // [n] (mu, STD) of this step, written by the kernel's own pre-pass
   unsigned long long expect;            // arrivals to wait for = G x barriers before this step
   int rank, G, rows_per_rank;
+  // owner-slotted exchange (k_step_xs): owner r keeps slots [2 parities][G writers][2][rpr] and totals [2][rpr]
+  long long* slot_w[kMaxRanks];         // owner r's slot of THIS rank for this step's partials: [2][rpr]
+  const long long* slot_r;              // this rank's slots of the previous step's partials: [G][2][rpr]
+  long long* totals[kMaxRanks];         // owner r's totals [2][rpr] of the current statistics
 };
 
-__device__ __forceinline__ void x_wait(const XParams& X, int* err) {
+__device__ __forceinline__ void x_wait_until(const XParams& X, unsigned long long expect, int* err) {
   if (threadIdx.x == 0) {
     long long spins = 0;
     for (;;) {
       unsigned long long v;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(X.flag) : "memory");
-      if (v >= X.expect) break;
+      if (v >= expect) break;
       __nanosleep(128);
       if (++spins > (1ll << 25)) { atomicOr(err, 4); break; }   // a peer never arrived: report, do not hang
     }
   }
   __syncthreads();
 }
+
+__device__ __forceinline__ void x_wait(const XParams& X, int* err) { x_wait_until(X, X.expect, err); }
 
 __device__ __forceinline__ void x_arrive_all(const XParams& X) {
   __threadfence_system();
@@ -836,6 +845,64 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB 
   step_x_body<LANES, VPL, MODE, FULL>(P, X, (int)blockIdx.x, (int)gridDim.x);
 }
 
+// Owner-slotted exchange (no remote atomics; one replica block): every rank STORES its replicas' partial
+// (sum D, sum D^2) of row i into its own slot at the row's owner (coalesced 8-byte stores, a warp writes
+// contiguous rows); after a barrier the owner sums the G slots of its rows into totals; after a second
+// barrier every rank reads row i's totals from the owner and finalizes. Slots are double-buffered by step
+// parity and fully rewritten every step (nothing to zero). Bit-identical to the other exchanges (exact
+// integer sums). The mid-kernel barrier needs every CTA of every rank resident: cooperative launch.
+template <int LANES, int VPL, int MODE, bool FULL>
+__device__ __forceinline__ void step_xs_body(const StepParams& P, const XParams& X, int cta, int ncta) {
+  const int lane = threadIdx.x & (LANES - 1);
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((cta * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((ncta * blockDim.x) / LANES);
+  const int rpr = X.rows_per_rank;
+  x_wait(X, P.flag);   // every rank's partials of the previous step are in the slots
+  {                    // owner rows: totals = sum over the G writers' slots
+    const int r0 = X.rank * rpr, own_n = max(0, min(rpr, P.n - r0));
+    const int tid = cta * (int)blockDim.x + (int)threadIdx.x, nt = ncta * (int)blockDim.x;
+    long long* tot = X.totals[X.rank];
+    for (int k = tid; k < own_n; k += nt) {
+      long long s0 = 0, s1 = 0;
+      for (int q = 0; q < X.G; ++q) {
+        s0 += __ldcg(X.slot_r + ((size_t)q * 2 + 0) * rpr + k);
+        s1 += __ldcg(X.slot_r + ((size_t)q * 2 + 1) * rpr + k);
+      }
+      tot[k] = s0;
+      tot[rpr + k] = s1;
+    }
+  }
+  x_signal(X, (unsigned)ncta);
+  x_wait_until(X, X.expect + (unsigned long long)X.G, P.flag);   // every owner's totals are written
+  for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {   // (mu, STD) of the group's rows
+    if (lane == 0) {
+      const int own = min(i / rpr, X.G - 1);
+      const long long* tt = X.totals[own];
+      const int k = i - own * rpr;
+      float mu, sd;
+      finalize_stats(X.c_cur[i], __ldcg(tt + k), __ldcg(tt + rpr + k), P.S_total, mu, sd);
+      X.ms[i] = make_float2(mu, sd);
+      X.c_next[i] = mu;
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
+    const int own = min(i / rpr, X.G - 1);
+    const float2 msi = __ldcg(X.ms + i);
+    step_item<LANES, VPL, MODE, FULL>(P, P.var, 0, i, lane, gmask, msi.x, msi.y, bad, false,
+                                      X.slot_w[own] - (size_t)own * rpr, nullptr, nullptr, -1, -1, rpr);
+  }
+  if (bad) atomicOr(P.flag, 1);
+  x_signal(X, (unsigned)ncta);
+}
+
+template <int LANES, int VPL, int MODE, bool FULL>
+__global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)) k_step_xs(const StepParams P, const XParams X) {
+  step_xs_body<LANES, VPL, MODE, FULL>(P, X, (int)blockIdx.x, (int)gridDim.x);
+}
+
 // One-GPU emulation of G ranks running the fused exchange CONCURRENTLY (test of the barrier / atomics
 // protocol, qqa_exchange_emulate): one cooperative launch whose grid is G slices of cta_per_rank CTAs;
 // slice r runs rank r's k_step_x body for steps 0..nsteps-1 with its own parameters, so ranks really
@@ -848,6 +915,7 @@ struct XEmulParams {
   const StepVar* var;       // [nsteps][G]
   const XParams* xp;        // [nsteps][G]
   int G, nsteps, cta_per_rank;
+  int slotted;              // 1: the owner-slotted exchange (step_xs_body)
 };
 
 template <int LANES, int VPL, int MODE, bool FULL>
@@ -858,7 +926,10 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB 
     StepParams P = E.base[r];
     P.var = E.var[(size_t)j * E.G + r];
     const XParams X = E.xp[(size_t)j * E.G + r];
-    step_x_body<LANES, VPL, MODE, FULL>(P, X, cta, E.cta_per_rank);
+    if (E.slotted)
+      step_xs_body<LANES, VPL, MODE, FULL>(P, X, cta, E.cta_per_rank);
+    else
+      step_x_body<LANES, VPL, MODE, FULL>(P, X, cta, E.cta_per_rank);
   }
 }
 
@@ -867,6 +938,33 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB 
 __global__ void k_x_arrive(const XParams X) {
   if (threadIdx.x == 0 && blockIdx.x == 0) x_arrive_all(X);
 }
+// Owner-slotted exchange, initial statistics: this rank's partial sums [2][n] -> its slot at every owner.
+__global__ void k_xs_scatter(const XParams X, int n, const long long* __restrict__ part) {
+  const int rpr = X.rows_per_rank;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int own = min(i / rpr, X.G - 1);
+    X.slot_w[own][i - own * rpr] = part[i];
+    X.slot_w[own][rpr + i - own * rpr] = part[n + i];
+  }
+}
+// Owner-slotted exchange: the current statistics (sum of the G writers' slots at each row's owner, parity of
+// slot_r) -> a local [2][n] copy (qqa_get_stats); waits for the barrier that ends the last step first.
+__global__ void k_xs_gather(const XParams X, int n, int par, long long* __restrict__ out, int* err) {
+  x_wait(X, err);
+  const int rpr = X.rows_per_rank;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int own = min(i / rpr, X.G - 1);
+    const long long* s = X.totals[own] - 2 * (size_t)X.G * 2 * rpr;   // owner's slot base (totals follow the slots)
+    long long s0 = 0, s1 = 0;
+    for (int q = 0; q < X.G; ++q) {
+      s0 += __ldcg(s + (((size_t)par * X.G + q) * 2 + 0) * rpr + (i - own * rpr));
+      s1 += __ldcg(s + (((size_t)par * X.G + q) * 2 + 1) * rpr + (i - own * rpr));
+    }
+    out[i] = s0;
+    out[n + i] = s1;
+  }
+}
+
 // Owner rows of the current sums -> a local [2][n] copy (qqa_get_stats). Waits for the barrier that
 // ends the last step first: until every rank has arrived, peers may still be adding into owner rows.
 __global__ void k_x_gather(const XParams X, int n, long long* __restrict__ out, int* err) {

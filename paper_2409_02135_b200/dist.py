@@ -36,7 +36,7 @@ def attach(solver, rank: int, world: int, group=None) -> None:
     solver.attach_comm(uid, rank, world)
 
 
-def attach_exchange(solver, rank: int, world: int, group=None):
+def attach_exchange(solver, rank: int, world: int, group=None, mode: str = "atomic"):
     """Collective: the fused statistics exchange over peer memory. Every rank's
     exchange buffer comes from torch symmetric memory, whose rendezvous maps all of them into every
     process; the library gets the peer pointers. Call after ``attach`` (the communicator stays in use
@@ -61,7 +61,7 @@ def attach_exchange(solver, rank: int, world: int, group=None):
     ptrs = list(hdl.buffer_ptrs)
     if len(ptrs) != world or ptrs[rank] != buf.data_ptr():
         raise RuntimeError("symmetric-memory rendezvous returned an unexpected peer map")
-    solver.attach_exchange(ptrs, rank, world, keep=(buf, hdl))
+    solver.attach_exchange(ptrs, rank, world, keep=(buf, hdl), mode=mode)
     return ptrs
 
 

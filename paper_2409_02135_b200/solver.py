@@ -195,17 +195,23 @@ class Solver:
         check(lib.qqa_exchange_bytes(self._h, ctypes.byref(out)))
         return int(out.value)
 
-    def attach_exchange(self, peer_ptrs, rank: int, nranks: int, keep=None):
-        """Fused statistics exchange over peer memory (qqa_attach_exchange): peer_ptrs[r] = rank r's
-        exchange buffer (device pointer mapped in this process). ``keep`` holds the buffers alive."""
+    EXCHANGE_MODES = {"atomic": 0, "slotted": 1}
+
+    def attach_exchange(self, peer_ptrs, rank: int, nranks: int, keep=None, mode: str = "atomic"):
+        """Fused statistics exchange over peer memory (qqa_attach_exchange_mode): peer_ptrs[r] = rank r's
+        exchange buffer (device pointer mapped in this process). mode "atomic" (remote int64 atomics into the
+        owner's rows) or "slotted" (plain stores into per-writer slots at the owner, owner-side sum).
+        ``keep`` holds the buffers alive."""
         arr = (ctypes.c_uint64 * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
-        check(lib.qqa_attach_exchange(self._h, arr, rank, nranks))
+        check(lib.qqa_attach_exchange_mode(self._h, arr, rank, nranks, self.EXCHANGE_MODES[mode]))
         self._exchange_keep = keep
+        self._exchange_mode = mode
 
     def detach_exchange(self):
         """Back to the NCCL path (qqa_detach_exchange); call reset() (collective) before the next run."""
         check(lib.qqa_detach_exchange(self._h))
         self._exchange_keep = None
+        self._exchange_mode = None
 
     def share_comm(self, donor: "Solver"):
         """Join donor's communicator (no new NCCL bootstrap); collective over its ranks."""

@@ -36,7 +36,7 @@ def test_library_is_sm100a(Q):
 
 
 def test_version_and_status_strings(Q):
-    assert Q.lib.qqa_version() == 8
+    assert Q.lib.qqa_version() == 9
     assert Q.lib.qqa_status_string(2) == b"bad graph"
 
 

@@ -52,6 +52,10 @@ class FakeSolver:
     def share_comm(self, donor):
         self._maybe("share_comm")
 
+    def attach_exchange(self, ptrs, rank, world, keep=None, mode="atomic"):
+        self._maybe("attach_exchange")
+        self.kind, self._exchange_keep, self._exchange_mode = "fused", keep, mode
+
     def detach_exchange(self):
         self.kind = "nccl"
 
@@ -97,9 +101,10 @@ def _worker(rank, world, port, scenario, out_dir):
         pick_exchange = staticmethod(qdist.pick_exchange)
 
         @staticmethod
-        def attach_exchange(sol, r, wsz):
+        def attach_exchange(sol, r, wsz, mode="atomic"):
             if inject == "attach_exchange":
                 raise RuntimeError("injected: no symmetric memory")
+            sol._exchange_keep, sol._exchange_mode = None, mode
             return [1, 2]
 
         @staticmethod
@@ -107,7 +112,8 @@ def _worker(rank, world, port, scenario, out_dir):
             pass
 
     fused_ms = scenario.get("fused_ms", 1.0)
-    seq = iter([0.0, fused_ms, 0.0, 2.0])   # (start, end) events of the fused probe, then of the NCCL probe
+    # (start, end) events of the NCCL probe, then of the atomic and the slotted fused probes
+    seq = iter([0.0, 2.0, 0.0, fused_ms, 0.0, scenario.get("slotted_ms", fused_ms)])
     bench.torch_event = lambda: FakeEvent(next(seq))
     args = type("A", (), {"exchange": "auto"})()
     w = type("W", (), {"n_colors": 0, "gamma_min": -2.0, "gamma_max": 0.1, "steps": 10})()
@@ -116,7 +122,8 @@ def _worker(rank, world, port, scenario, out_dir):
                                 lambda: dist.barrier(), lambda x: qdist.max_over_ranks(x))
     kept, xptrs, desc, probe = res
     with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
-        json.dump({"kind": kept.kind, "fused": xptrs is not None, "desc": desc}, f)
+        json.dump({"kind": kept.kind, "fused": xptrs is not None, "desc": desc,
+                   "mode": getattr(kept, "_exchange_mode", None)}, f)
     dist.destroy_process_group()
 
 
@@ -129,6 +136,8 @@ def _worker(rank, world, port, scenario, out_dir):
     {"inject": "get_state", "expect": "nccl"},       # the reference handle's state read raises
     {"inject": None, "fused_ms": 1.0, "expect": "fused"},
     {"inject": None, "fused_ms": 3.0, "expect": "nccl"},
+    {"inject": None, "fused_ms": 3.0, "slotted_ms": 1.5, "expect": "fused", "mode": "slotted"},
+    {"inject": None, "fused_ms": 1.2, "slotted_ms": 1.5, "expect": "fused", "mode": "atomic"},
 ])
 def test_every_rank_agrees_on_the_exchange(tmp_path, scenario):
     mp.start_processes(_worker, args=(2, _free_port(), scenario, str(tmp_path)), nprocs=2, join=True,
@@ -136,3 +145,5 @@ def test_every_rank_agrees_on_the_exchange(tmp_path, scenario):
     got = [json.load(open(tmp_path / f"r{r}.json")) for r in range(2)]
     assert got[0]["fused"] == got[1]["fused"], got
     assert got[0]["fused"] == (scenario["expect"] == "fused"), got
+    if "mode" in scenario:
+        assert got[0]["mode"] == got[1]["mode"] == scenario["mode"], got

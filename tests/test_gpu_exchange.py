@@ -282,3 +282,105 @@ def test_detach_exchange_returns_to_the_nccl_path(Q):
         assert np.array_equal(a.get_state()[k], b.get_state()[k]), k
     for k in ("c", "sumD", "sumD2"):
         assert np.array_equal(a.get_stats()[k], b.get_stats()[k]), k
+
+
+SLOT_CASES = [c for c in CASES if c[4] is None]   # the owner-slotted exchange needs one replica block
+
+
+@pytest.mark.parametrize("case", range(len(SLOT_CASES)))
+def test_slotted_exchange_concurrent_ranks_reproduce_the_full_ensemble(Q, case):
+    """Owner-slotted exchange (qqa_attach_exchange_mode SLOTTED): partials stored into per-writer slots at the
+    owner, owner-side sum after a barrier, totals read after a second barrier -- no remote atomics. G ranks
+    run concurrently in one cooperative launch (the mid-kernel barrier needs every rank resident); bit-exact
+    against the handle holding every replica, including the statistics and the evaluation."""
+    problem, G, S_l, hp, _ = SLOT_CASES[case]
+    g = gen.erdos_renyi(120, 0.5, 7) if problem == "maxclique" else gen.erdos_renyi(501, 0.03, 40 + case)
+    S = G * S_l
+    gam = oracle.schedule(-5.0 if problem == "maxcut" else -2.0, 0.1, 400)[:60]
+    full = Q.Solver(g.rowptr, g.colidx, Q.make_config(problem, S_total=S, seed=9, **hp))
+    full.run(gam)
+    shards = [Q.Solver(g.rowptr, g.colidx, Q.make_config(problem, S_total=S, seed=9, replica_offset=r * S_l,
+                                                         S_local=S_l, **hp)) for r in range(G)]
+    bufs, ptrs = exchange_buffers(shards)
+    for r, sh in enumerate(shards):
+        sh.attach_exchange(ptrs, r, G, keep=bufs, mode="slotted")
+    Q.loopback_sync_init(shards)            # every buffer zeroed: scatter the initial partials, first barrier
+    st0 = shards[1].get_stats()             # the initial totals, gathered from the owners' slots
+    f0 = Q.Solver(g.rowptr, g.colidx, Q.make_config(problem, S_total=S, seed=9, **hp)).get_stats()
+    assert np.array_equal(st0["sumD"], f0["sumD"]) and np.array_equal(st0["sumD2"], f0["sumD2"])
+    Q.exchange_emulate(shards, gam[:25])
+    Q.exchange_emulate(shards, gam[25:])
+    fs, fst = full.get_state(), full.get_stats()
+    for r, sh in enumerate(shards):
+        ss = sh.get_state()
+        assert ss["step"] == 60
+        for f in ("theta", "m", "v", "p"):
+            assert np.array_equal(ss[f].view(np.uint32), fs[f][:, r * S_l:(r + 1) * S_l].view(np.uint32)), (r, f)
+        st = sh.get_stats()
+        for f in ("c", "sumD", "sumD2"):
+            assert np.array_equal(st[f], fst[f]), (r, f)
+    fr = full.round_evaluate().per_replica
+    for r, sh in enumerate(shards):
+        pr = sh.round_evaluate().per_replica
+        for f in ("size", "violations", "cut", "energy"):
+            assert np.array_equal(pr[f], fr[f][r * S_l:(r + 1) * S_l]), (r, f)
+
+
+def test_slotted_exchange_c5_shards_and_one_rank_nccl(Q):
+    """c5's graph as 8 concurrent slotted ranks (20 steps), and one rank with a real NCCL communicator on the
+    production launch (cooperative k_step_xs per step) across reset and resume: both bit-exact."""
+    import torch
+    w = gen.workload("c5")
+    g = w.graphs[0]
+    hp = {k: v for k, v in w.hparams().items() if k != "problem"}
+    gam = oracle.schedule(w.gamma_min, w.gamma_max, w.steps)[:20]
+    full = Q.Solver(g.rowptr, g.colidx, Q.make_config("mis", S_total=64, seed=w.seeds[0], **hp))
+    full.run(gam)
+    fs = full.get_state()
+    full.close()
+    G, S_l = 8, 8
+    shards = [Q.Solver(g.rowptr, g.colidx, Q.make_config("mis", S_total=64, seed=w.seeds[0], replica_offset=r * S_l,
+                                                         S_local=S_l, **hp)) for r in range(G)]
+    bufs, ptrs = exchange_buffers(shards)
+    for r, sh in enumerate(shards):
+        sh.attach_exchange(ptrs, r, G, keep=bufs, mode="slotted")
+    Q.loopback_sync_init(shards)            # every buffer zeroed: scatter the initial partials, first barrier
+    Q.exchange_emulate(shards, gam)
+    for r, sh in enumerate(shards):
+        ss = sh.get_state()
+        assert np.array_equal(ss["theta"].view(np.uint32), fs["theta"][:, r * S_l:(r + 1) * S_l].view(np.uint32)), r
+    for sh in shards:
+        sh.close()
+    del shards, bufs
+    g2 = gen.random_regular(3000, 20, 5)
+    mk = lambda: Q.Solver(g2.rowptr, g2.colidx, Q.make_config("mis", S_total=32, seed=3, comm=0.2))
+    a, b = mk(), mk()
+    for s in (a, b):
+        s.attach_comm(Q.Solver.nccl_unique_id(), 0, 1)
+    buf = torch.empty(b.exchange_bytes(), dtype=torch.uint8, device=b.device)
+    b.attach_exchange([buf.data_ptr()], 0, 1, keep=buf, mode="slotted")
+    assert b.step_path() == "exchange"
+    for s in (a, b):
+        s.reset()
+        s.run_linear(-2.0, 0.1, 300, 0, 60)
+    for k in ("theta", "m", "v", "p"):
+        assert np.array_equal(a.get_state()[k], b.get_state()[k]), k
+    for k in ("c", "sumD", "sumD2"):
+        assert np.array_equal(a.get_stats()[k], b.get_stats()[k]), k
+    ra, rb = a.round_evaluate(), b.round_evaluate()
+    assert ra.best_replica == rb.best_replica and np.array_equal(ra.best_x, rb.best_x)
+    ck, cs = b.get_state(), b.get_stats()
+    b.set_state(ck["theta"], ck["m"], ck["v"], ck["step"], c=cs["c"])
+    for s in (a, b):
+        s.run_linear(-2.0, 0.1, 300, 60, 90)
+    for k in ("theta", "p"):
+        assert np.array_equal(a.get_state()[k], b.get_state()[k]), k
+
+
+def test_slotted_exchange_rejects_replica_blocks(Q, monkeypatch):
+    monkeypatch.setenv("QQA_BLOCK_REPLICAS", "8")
+    g = gen.erdos_renyi(200, 0.05, 1)
+    s = Q.Solver(g.rowptr, g.colidx, Q.make_config("mis", S_total=32, seed=1, replica_offset=0, S_local=16))
+    with pytest.raises(Q.QQAError) as e:
+        s.attach_exchange([1 << 20, 2 << 20], 0, 2, mode="slotted")
+    assert e.value.status == 6

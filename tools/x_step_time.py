@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Per-step kernel time of the sharded paths at one rank (A/B helper): c5's graph with S_l replicas,
-NCCL communicator (k_finalize + k_step) vs the fused exchange (k_step_x).
+NCCL communicator (k_finalize + k_step) vs the fused exchanges (k_step_x: atomics; k_step_xs: owner slots).
   python tools/x_step_time.py [S_l] [steps]"""
 import os
 import sys
@@ -16,12 +16,12 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 w = gen.workload("c5")
 g = w.graphs[0]
 hp = {k: v for k, v in w.hparams().items() if k != "problem"}
-for mode in ("nccl", "fused"):
+for mode in ("nccl", "fused", "slotted"):
     sol = Q.Solver(g.rowptr, g.colidx, Q.make_config("mis", S_total=S_l, seed=5, S_local=S_l, **hp))
     sol.attach_comm(Q.Solver.nccl_unique_id(), 0, 1)
-    if mode == "fused":
+    if mode in ("fused", "slotted"):
         buf = torch.empty(sol.exchange_bytes(), dtype=torch.uint8, device=sol.device)
-        sol.attach_exchange([buf.data_ptr()], 0, 1, keep=buf)
+        sol.attach_exchange([buf.data_ptr()], 0, 1, keep=buf, mode="atomic" if mode == "fused" else "slotted")
     sol.run_linear(w.gamma_min, w.gamma_max, w.steps, 0, 5)
     sol.profile(True)
     sol.run_linear(w.gamma_min, w.gamma_max, w.steps, 5, 5 + steps)
