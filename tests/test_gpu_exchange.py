@@ -203,7 +203,7 @@ def test_fused_exchange_rejects_unsupported(Q):
         s.attach_exchange([1 << 20], 1, 2)    # replica_offset 0 is rank 0's shard
 
 
-@pytest.mark.parametrize("mode", ["auto", "fused"])
+@pytest.mark.parametrize("mode", ["auto", "fused", "slotted"])
 def test_bench_multi_gpu_code_path_at_one_rank(Q, mode):
     """bench.py's N > 1 code path (process group, NCCL communicator, symmetric-memory exchange buffers,
     self-check and speed probe) at one rank: exactly one JSON line on stdout, the exchange recorded."""
@@ -220,11 +220,12 @@ def test_bench_multi_gpu_code_path_at_one_rank(Q, mode):
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["e2e"]["value"] > 0
-    if mode == "fused":
+    if mode in ("fused", "slotted"):
         assert d["config"]["exchange"].startswith("fused") and d["roofline"]["kernel"].startswith("qqa::k_step_x")
-    else:
+        assert ("slotted" in d["config"]["exchange"]) == (mode == "slotted")
+    else:   # c3 has one replica block: both fused modes pass the self-check and are timed beside NCCL
         probe = d["config"]["exchange_probe"]
-        assert probe["fused_ms_per_step"] > 0 and probe["nccl_ms_per_step"] > 0
+        assert probe["nccl_ms_per_step"] > 0 and probe["atomic_ms_per_step"] > 0 and probe["slotted_ms_per_step"] > 0
 
 
 @pytest.mark.parametrize("kind,problem,G,S_l,hp", [("pm1", "maxcut", 4, 16, dict(comm=0.3)),
