@@ -519,7 +519,7 @@ def main():
     achieved = B / avg_kernel_s / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.replicas is None and not args.anneal_steps:   # measured for the default shape
         with open(tpath) as f:
             variant = ("_" + w.map if w.map != "sigmoid" else "") + ("_T" if w.temperature else "")
             traffic = json.load(f).get(f"{w.name}{variant}_x{world}")
