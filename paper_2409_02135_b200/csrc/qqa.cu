@@ -1323,7 +1323,10 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     RunKernel kr = nullptr;
     // contiguous-row persistent CTAs when the kernel fits 64 registers (VPL 1) and the work
     // fills every SM with a 1024-thread CTA (measured: profiles/r1_design_iterations.md)
-    h->run_cta = (s.vpl == 1 && (int64_t)s.n * s.lanes >= (int64_t)h->sm_count * 1024) ? 1024 : 256;
+    // contiguous rows per SM (CT 1024) pay off for a batch of small instances (an SM's rows are about one
+    // instance, whose p rows stay in L1: c2 53.0 vs 56.7 us); a single random graph has no such locality and
+    // runs 3 x 256 threads per SM with more registers (c3 19.8 vs 22.8 us; profiles/r2_ab_run256_minb.txt)
+    h->run_cta = (s.vpl == 1 && s.G > 1 && (int64_t)s.n * s.lanes >= (int64_t)h->sm_count * 1024) ? 1024 : 256;
     if (const char* env = std::getenv("QQA_RUN_CTA")) h->run_cta = (std::atoi(env) == 1024 && s.vpl == 1) ? 1024 : 256;
     if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg, s.weighted), ks, ki, &kr, h->run_cta, full_lanes(s)))
       return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));

@@ -1002,8 +1002,14 @@ struct RunParams {
 // gathers from a compact part of p (for a batch of small instances: about one instance, whose p
 // rows largely stay in that SM's L1; c2 69.8 -> 57.8 us/step); 256 = 4 CTAs per SM with rows
 // strided over the grid (kernels needing > 64 registers, or too little work to fill every SM).
+// CT = 256 with one vector per lane runs 3 CTAs per SM (up to 85 registers: no constant reloads or spills in
+// the update), measured faster than 4 x 64 registers on single-instance L2-resident problems (c3 22.8 -> 19.8
+// us per step, profiles/r2_ab_run256_minb.txt).
+#ifndef QQA_RUN256_MINB
+#define QQA_RUN256_MINB 3
+#endif
 template <int LANES, int VPL, int MODE, int CT, bool FULL>
-__global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_STEP_MIN_BLOCKS)))
+__global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_RUN256_MINB)))
     k_run(const RunParams R) {
   namespace cg = cooperative_groups;
   const StepParams& P = R.P;
