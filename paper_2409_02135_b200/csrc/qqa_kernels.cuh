@@ -1556,8 +1556,11 @@ __device__ __forceinline__ void normalize_colours(float (&w)[KP], int K, float u
 #ifndef QQA_KARY_U_WIDE
 #define QQA_KARY_U_WIDE 2    // neighbour rows in flight per lane for KP > 8
 #endif
+#ifndef QQA_KARY_MINB_NARROW
+#define QQA_KARY_MINB_NARROW 4   // min CTAs per SM for k_step_K, KP <= 8
+#endif
 template <int KP, int MODE>
-__global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : 4)) k_step_K(const StepKParams P) {
+__global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_NARROW)) k_step_K(const StepKParams P) {
   constexpr int U = (KP <= 8) ? 4 : QQA_KARY_U_WIDE;     // neighbour rows in flight per lane
   const int L = P.L;
   const int lane = threadIdx.x & (L - 1);
