@@ -64,6 +64,8 @@ XStepKernel xsstep_for(int lanes, int vpl, bool full) {
 template <int M>
 RunKernel run_kernel_for(int lanes, int vpl, int cta, bool full) {
   if (M & kModeSparseClique) return nullptr;   // its column sums need a pass between steps: no k_run
-  return (cta == 1024 && vpl == 1) ? run_for<M, 1024>(lanes, vpl, full) : run_for<M, 256>(lanes, vpl, full);
+  if (vpl == 1 && cta == 1024) return run_for<M, 1024>(lanes, vpl, full);
+  if (vpl == 1 && cta == 768) return run_for<M, 768>(lanes, vpl, full);
+  return run_for<M, 256>(lanes, vpl, full);
 }
 }  // namespace qqa

@@ -1323,11 +1323,16 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     RunKernel kr = nullptr;
     // contiguous-row persistent CTAs when the kernel fits 64 registers (VPL 1) and the work
     // fills every SM with a 1024-thread CTA (measured: profiles/r1_design_iterations.md)
-    // contiguous rows per SM (CT 1024) pay off for a batch of small instances (an SM's rows are about one
-    // instance, whose p rows stay in L1: c2 53.0 vs 56.7 us); a single random graph has no such locality and
-    // runs 3 x 256 threads per SM with more registers (c3 19.8 vs 22.8 us; profiles/r2_ab_run256_minb.txt)
-    h->run_cta = (s.vpl == 1 && s.G > 1 && (int64_t)s.n * s.lanes >= (int64_t)h->sm_count * 1024) ? 1024 : 256;
-    if (const char* env = std::getenv("QQA_RUN_CTA")) h->run_cta = (std::atoi(env) == 1024 && s.vpl == 1) ? 1024 : 256;
+    // contiguous rows per SM pay off for a batch of small instances (an SM's rows are about one instance,
+    // whose p rows stay in L1: c2 53.0 vs 56.7 us with 256-thread CTAs), best as one 768-thread CTA per SM with
+    // up to 85 registers (c2 48.8 vs 53.2 at 1024 threads and 64 registers; t1 353.0 vs 351.5); a single random
+    // graph has no such locality and runs 3 x 256 threads per SM (c3 19.9 vs 20.9 at 768, 22.8 at 1024;
+    // profiles/r2_ab_run256_minb.txt, r2_ab_run768.txt)
+    h->run_cta = (s.vpl == 1 && s.G > 1 && (int64_t)s.n * s.lanes >= (int64_t)h->sm_count * 768) ? 768 : 256;
+    if (const char* env = std::getenv("QQA_RUN_CTA")) {
+      const int c = std::atoi(env);
+      h->run_cta = (s.vpl == 1 && (c == 1024 || c == 768)) ? c : 256;
+    }
     if (!pick_kernels(s.lanes, s.vpl, step_mode(*cfg, s.weighted), ks, ki, &kr, h->run_cta, full_lanes(s)))
       return cleanup(fail(QQA_ERR_UNSUPPORTED, "no kernel for this S_local"));
     if ((st = grid_for((const void*)ks, h->sm_count, s.n, s.lanes, h->grid_step))) return cleanup(st);

@@ -1009,14 +1009,14 @@ struct RunParams {
 #define QQA_RUN256_MINB 3
 #endif
 template <int LANES, int VPL, int MODE, int CT, bool FULL>
-__global__ void __launch_bounds__(CT, (CT == 1024 ? 1 : (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_RUN256_MINB)))
+__global__ void __launch_bounds__(CT, (CT >= 512 ? 1 : (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB : QQA_RUN256_MINB)))
     k_run(const RunParams R) {
   namespace cg = cooperative_groups;
   const StepParams& P = R.P;
   const int lane = threadIdx.x & (LANES - 1);
   const unsigned gmask = group_mask<LANES>();
   int group, ngroups, row1;
-  if (CT == 1024) {
+  if (CT >= 512) {   // one CTA per SM owning contiguous rows
     const int rows_cta = (P.n + (int)gridDim.x - 1) / (int)gridDim.x;   // contiguous rows of this CTA
     const int row0 = (int)blockIdx.x * rows_cta;
     row1 = min(P.n, row0 + rows_cta);
