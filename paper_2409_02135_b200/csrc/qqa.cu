@@ -850,7 +850,7 @@ int do_steps_cluster(qqa_handle* h, const float* gamma, int64_t n_steps) {
     R.scur0 = h->scur;
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(h->cluster_cs);
-    lc.blockDim = dim3(1024);
+    lc.blockDim = dim3(QQA_CLUSTER_CT);
     lc.dynamicSmemBytes = h->cluster_smem;
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
@@ -1389,7 +1389,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
         }
         cudaLaunchConfig_t lc{};
         lc.gridDim = dim3(cs);
-        lc.blockDim = dim3(1024);
+        lc.blockDim = dim3(QQA_CLUSTER_CT);
         lc.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;

@@ -1055,8 +1055,13 @@ __global__ void __launch_bounds__(CT, (CT >= 512 ? 1 : (VPL >= 4 ? 2 : VPL >= 2 
 // row's sums (shared int64 atomics: exact, order-free), then one cluster barrier publishes p_next.
 // No global memory traffic between the first load and the final write-back, no grid barrier.
 // Same buffers in and out as k_run (p / c ping-pong, sums mod 3), bit-identical.
+// Threads per CTA of the one-cluster anneal: 512 (up to 128 registers) measured faster than 1024 (64) and 256
+// on c1 (2.2 vs 2.4 / 2.5 us per step, profiles/r2_ab_cluster_ct.txt); the element loops stride by blockDim.
+#ifndef QQA_CLUSTER_CT
+#define QQA_CLUSTER_CT 512
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(1024, 1) k_run_cluster(const RunParams R) {
+__global__ void __launch_bounds__(QQA_CLUSTER_CT, 1) k_run_cluster(const RunParams R) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const StepParams& P = R.P;
