@@ -67,12 +67,14 @@ struct Shape {
   bool kary = false;           // graph colouring (NEXT-4): layout [n][S_local][KP]
   bool weighted = false;       // edge weights (MIS / Max-Cut)
   int K = 0, KP = 0, LK = 0;   // colours, padded to a multiple of 4, lanes per variable
+  int KS = 1;                  // source segments of the segmented gather; 1: one-pass k_step
+  int64_t nnz_seg = 0;         // entries of the segment CSRs (each (row, segment) padded to 4)
 };
 
 struct Layout {
   size_t rowptr, colidx, rowptr_pad, colidx_pad, gor, theta, m, v, p0, p1, c0, c1, ms, s0, s1, s2, flag, X,
       counts, tot, energy, best, beste, genergy, gbest, gbeste, xbuf, sched, cs0, cs1, w, w_pad, wdeg, wsums,
-      total;
+      rowptr_seg, colidx_seg, total;
 };
 
 Layout make_layout(const Shape& s) {
@@ -116,6 +118,8 @@ Layout make_layout(const Shape& s) {
   L.w_pad = take(s.weighted ? (size_t)s.nnz_pad * sizeof(float) : 0);   // aligned with colidx_pad
   L.wdeg = take(s.weighted ? (size_t)s.n * sizeof(float) : 0);
   L.wsums = take(2 * (size_t)s.S_total * sizeof(long long));            // [S_total][2] weight sums
+  L.rowptr_seg = take(s.KS > 1 ? (size_t)s.KS * ((size_t)s.n + 1) * sizeof(int) : 0);   // [KS][n+1]
+  L.colidx_seg = take(s.KS > 1 ? (size_t)s.nnz_seg * sizeof(int) : 0);
   L.total = o;
   return L;
 }
@@ -194,6 +198,52 @@ int64_t problem_nnz(const qqa_graph* g, int problem) {
   return pairs - g->nnz;
 }
 
+// Segmented gather: segment k of the sources is [seg_lo(n, KS, k), seg_lo(n, KS, k + 1)).
+int seg_lo(int n, int KS, int k) { return (int)((int64_t)n * k / KS); }
+
+// Segment CSR: for every segment k, row i's neighbours in segment k (CSR order), padded to a multiple of 4
+// with the sentinel n. rp: [KS][n+1] absolute offsets into ci. Returns the entry count; fills rp / ci if given.
+// One pass over each row (its columns ascend, so the segment index only moves forward): O(nnz + KS n).
+int64_t build_seg_csr(const int64_t* rowptr, const int32_t* colidx, int n, int KS, int* rp, int* ci) {
+  std::vector<int> lo((size_t)KS + 1);
+  for (int k = 0; k <= KS; ++k) lo[k] = seg_lo(n, KS, k);
+  lo[KS] = INT32_MAX;   // the last segment takes everything from lo[KS-1] on (incl. out-of-range columns)
+  std::vector<int> cnt(rp ? (size_t)KS * n : 0);
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {   // segment boundaries of a row by binary search (its columns ascend)
+    const int32_t* a = colidx + rowptr[i];
+    const int32_t* end = colidx + rowptr[i + 1];
+    for (int k = 0; k < KS; ++k) {
+      const int32_t* b = (k + 1 < KS) ? std::lower_bound(a, end, lo[k + 1]) : end;
+      const int c = (int)(b - a);
+      total += (c + 3) / 4 * 4;
+      if (rp) cnt[(size_t)k * n + i] = c;
+      a = b;
+    }
+  }
+  if (!rp) return total;
+  int64_t o = 0;
+  for (int k = 0; k < KS; ++k) {
+    for (int i = 0; i < n; ++i) {
+      rp[(size_t)k * (n + 1) + i] = (int)o;
+      o += (cnt[(size_t)k * n + i] + 3) / 4 * 4;
+    }
+    rp[(size_t)k * (n + 1) + n] = (int)o;
+  }
+  if (ci) {
+    for (int i = 0; i < n; ++i) {
+      int64_t e = rowptr[i];
+      for (int k = 0; k < KS; ++k) {
+        int o2 = rp[(size_t)k * (n + 1) + i];
+        const int c = cnt[(size_t)k * n + i];
+        for (int q = 0; q < c; ++q) ci[o2++] = colidx[e++];
+        for (int q = c; q < (c + 3) / 4 * 4; ++q) ci[o2++] = n;
+      }
+    }
+  }
+  return o;
+}
+
 int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
   int st = check_graph(g);
   if (st) return st;
@@ -257,6 +307,16 @@ int make_shape(const qqa_graph* g, const qqa_config* c, Shape& s) {
     s.nnz_pad += (deg + 3) / 4 * 4;
   }
   if (s.nnz_pad >= (int64_t)INT32_MAX) return fail(QQA_ERR_UNSUPPORTED, "padded nnz >= 2^31");
+  // Segmented gather: VPL 1, FULL shapes, unweighted, MIS / Max-Cut on the given graph.
+  s.KS = 1;
+  if (const char* env = std::getenv("QQA_SEGMENTS")) s.KS = std::max(1, std::min(64, std::atoi(env)));
+  if (s.KS > 1 && (s.kary || s.weighted || s.vpl != 1 || !full_lanes(s) || s.n < 4 * s.KS ||
+                   (c->problem != QQA_MIS && c->problem != QQA_MAXCUT)))
+    s.KS = 1;
+  if (s.KS > 1) {
+    s.nnz_seg = build_seg_csr(g->rowptr, g->colidx, s.n, s.KS, nullptr, nullptr);
+    if (s.nnz_seg >= (int64_t)INT32_MAX) s.KS = 1;
+  }
   if ((int64_t)s.B * ((int64_t)s.n + 1) * s.SB >= (int64_t)1 << 40) return fail(QQA_ERR_UNSUPPORTED, "state too large");
   return QQA_OK;
 }
@@ -347,6 +407,11 @@ struct qqa_handle {
   long long* wsums = nullptr;  // [S_total][2] evaluation weight sums (fixed point 2^24)
   bool serpentine = false;     // replica blocks swept in alternating order step to step (QQA_SERPENTINE)
   qqa::StepKernel kst = nullptr;   // k_step_st (staged state) for the launch-per-step path, nullptr: k_step
+  // segmented gather (s.KS > 1): segment CSRs and the three kernels (first / middle partial passes, last + update)
+  int* rowptr_seg = nullptr;
+  int* colidx_seg = nullptr;
+  qqa::StepKernel kseg[3] = {nullptr, nullptr, nullptr};
+  int grid_seg[3] = {0, 0, 0};
   int grid_st = 0;
   size_t st_smem = 0;
   int grid_run = 0;            // co-resident grid of k_run (0: launch-per-step only)
@@ -1028,10 +1093,34 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
       h->launches++;
       int st;
       if ((st = record_start(h))) return st;
+      if (h->s.KS > 1) {   // segmented gather: per replica block, KS - 1 partial passes, then the last + update
+        const int KS = h->s.KS;
+        for (int bq = 0; bq < h->s.B; ++bq) {
+          qqa::StepParams Q = P;
+          Q.blo = bq; Q.bhi = bq + 1;
+          Q.colidx_pad = h->colidx_seg;
+          for (int k = 0; k < KS; ++k) {
+            Q.rowptr_pad = h->rowptr_seg + (size_t)k * ((size_t)h->s.n + 1);
+            const int q = (k == 0) ? 0 : (k < KS - 1) ? 1 : 2;
+            if (k == KS - 1 && C > 1) break;   // chunked last pass below (communicator overlap)
+            Q.row_begin = 0; Q.row_end = h->s.n;
+            h->kseg[q]<<<h->grid_seg[q], 256, 0, h->stream>>>(Q);
+            QQA_CUDA(cudaGetLastError());
+            h->launches++;
+          }
+        }
+      }
       for (int ch = 0; ch < C; ++ch) {
         P.row_begin = (int)((int64_t)h->s.n * ch / C);
         P.row_end = (int)((int64_t)h->s.n * (ch + 1) / C);
-        if (h->kst)
+        if (h->s.KS > 1) {
+          if (C == 1) break;   // every pass already launched above
+          qqa::StepParams Q = P;
+          Q.blo = 0; Q.bhi = h->s.B;
+          Q.colidx_pad = h->colidx_seg;
+          Q.rowptr_pad = h->rowptr_seg + (size_t)(h->s.KS - 1) * ((size_t)h->s.n + 1);
+          h->kseg[2]<<<h->grid_seg[2], 256, 0, h->stream>>>(Q);
+        } else if (h->kst)
           h->kst<<<h->grid_st, 256, h->st_smem, h->stream>>>(P);
         else
           ks<<<h->grid_step, 256, 0, h->stream>>>(P);
@@ -1298,6 +1387,20 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
       h->launches++;
     }
     QQA_CUDA_C(cudaStreamSynchronize(h->stream));  // rp_pad is pageable host memory
+  }
+  if (s.KS > 1) {  // segmented gather: segment CSRs (built on the host from the validated graph) and kernels
+    std::vector<int> rps((size_t)s.KS * ((size_t)s.n + 1)), cis((size_t)s.nnz_seg);
+    if (build_seg_csr(g->rowptr, g->colidx, s.n, s.KS, rps.data(), cis.data()) != s.nnz_seg)
+      return cleanup(fail(QQA_ERR_BAD_GRAPH, "graph rejected: segment CSR size differs from the planned one"));
+    h->rowptr_seg = (int*)(ws + L.rowptr_seg);
+    h->colidx_seg = (int*)(ws + L.colidx_seg);
+    QQA_CUDA_C(cudaMemcpyAsync(h->rowptr_seg, rps.data(), rps.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    QQA_CUDA_C(cudaMemcpyAsync(h->colidx_seg, cis.data(), cis.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    if (!qqa::seg_kernels(s.lanes, step_mode(*cfg, s.weighted), h->kseg[0], h->kseg[1], h->kseg[2]))
+      return cleanup(fail(QQA_ERR_UNSUPPORTED, "no segmented-gather kernel for this shape"));
+    for (int q = 0; q < 3; ++q)
+      if ((st = grid_for((const void*)h->kseg[q], h->sm_count, s.n, s.lanes, h->grid_seg[q]))) return cleanup(st);
+    QQA_CUDA_C(cudaStreamSynchronize(h->stream));   // rps / cis are pageable host memory
   }
   if (s.kary) {
     StepKKernel ks;

@@ -72,6 +72,10 @@ XEmulKernel xemul_kernel(int lanes, int vpl, int mode, bool full);
 // k_run_cluster<MODE> (MODE 0..3, compiled in k_cluster.cu); nullptr otherwise.
 RunKernel cluster_kernel(int mode);
 
+// Segmented gather (k_seg.cu): k_seg_gather<lanes, FIRST> and k_step_seg<lanes, MODE> for VPL 1, FULL
+// shapes, MODE 0..3; false otherwise.
+bool seg_kernels(int lanes, int mode, StepKernel& first, StepKernel& mid, StepKernel& last);
+
 // K-ary kernels for KP in {4, 8, 12, 16}; false otherwise.
 bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);
 // k_step_Kq<KP, MODE> (colour quads, KP = 12 / 16); nullptr otherwise.

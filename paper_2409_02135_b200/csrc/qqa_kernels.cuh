@@ -377,6 +377,7 @@ struct StepParams {
   float at;                             // 1 - lr wd (host double -> float)
   float ns;                             // Langevin scale sqrt(2 lr T) (host double -> float)
   unsigned long long S_total_u;         // key stride per row
+  int blo, bhi;                         // replica blocks [blo, bhi) of a segmented-gather launch (k_seg_*)
 };
 
 // Gradient (Eq. 6/7/10 + App. D), AdamW, optional Langevin noise and
@@ -487,17 +488,24 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
 // One work item (replica block b, variable i) of the step: gather, update, statistics.
 // FULL: every lane holds a vector of the block (SB / 8 == LANES * VPL), so the gather needs no
 // per-lane guard (a compile-time variant; measured 1.7 % on c5).
-template <int LANES, int VPL, int MODE, bool FULL = false, bool STAGE = false>
-__device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
-                                          unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false,
-                                          long long* sums_dst = nullptr, long long* zero_dst = nullptr,
-                                          const float4* stage = nullptr, int nb = -1, int ni = -1,
-                                          int slot_stride = 0) {
+// Gather q_i = sum_j A_ij p_j over block b (CSR order) into acc. QIN: the sum continues a partial sum
+// stored in the item's p_next row by the previous source segment (segmented gather): the
+// neighbours of a row are strictly ascending, so segments of ascending source ranges add them in CSR order
+// and the result is bit-identical to the one-pass gather. SKIP: sentinel entries (column n, the zero row)
+// issue no load (exactly +0 added).
+template <int LANES, int VPL, int MODE, bool FULL, bool QIN = false, bool SKIP = false>
+__device__ __forceinline__ void gather_q(const StepParams& P, const StepVar& V, int b, int i, int lane,
+                                         V8 (&acc)[VPL]) {
       const int SB8 = P.SB >> 3;
       const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
       const float* __restrict__ pc = V.p_cur + blk;
-      // ---- gather q_i over block b
-      V8 acc[VPL];
+      if constexpr (QIN) {
+#pragma unroll
+        for (int w = 0; w < VPL; ++w) {
+          const int col8 = lane + w * LANES;
+          acc[w] = (FULL || col8 < SB8) ? ld8_stream(V.p_next + blk + (size_t)i * P.SB + col8 * 8) : zero8();
+        }
+      }
       const int e0 = __ldg(P.rowptr_pad + i), e1 = __ldg(P.rowptr_pad + i + 1);
       constexpr int U = (VPL == 1) ? QQA_GATHER_U : 4;   // neighbour rows in flight per lane
       // Index loads of round k+1 issued before round k's gathers: measured faster for the non-FULL shapes
@@ -525,12 +533,13 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 #pragma unroll
               for (int w = 0; w < VPL; ++w) {
                 const int col8 = lane + w * LANES;
-                buf[u][w] = (FULL || col8 < SB8) ? ld8_gather(pc + (size_t)js[h + u] * P.SB + col8 * 8) : zero8();
+                buf[u][w] = ((FULL || col8 < SB8) && (!SKIP || js[h + u] != P.n))
+                                ? ld8_gather(pc + (size_t)js[h + u] * P.SB + col8 * 8) : zero8();
               }
             if (h == 2) nxt[0] = (e + 4 < e1) ? ld_idx4(P.colidx_pad + e + 4) : make_int4(P.n, P.n, P.n, P.n);
 #pragma unroll
             for (int w = 0; w < VPL; ++w) {
-              if (e == e0 && h == 0) acc[w] = buf[0][w]; else add8(acc[w], buf[0][w]);
+              if (!QIN && e == e0 && h == 0) acc[w] = buf[0][w]; else add8(acc[w], buf[0][w]);
               add8(acc[w], buf[1][w]);
             }
           }
@@ -554,7 +563,8 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 #pragma unroll
           for (int w = 0; w < VPL; ++w) {
             const int col8 = lane + w * LANES;
-            buf[u][w] = (FULL || col8 < SB8) ? ld8_gather(pc + (size_t)js[u] * P.SB + col8 * 8) : zero8();
+            buf[u][w] = ((FULL || col8 < SB8) && (!SKIP || js[u] != P.n))
+                            ? ld8_gather(pc + (size_t)js[u] * P.SB + col8 * 8) : zero8();
           }
         if constexpr (!kIdxPipe) {
 #pragma unroll
@@ -569,7 +579,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
             wt[u] = w4.x; wt[u + 1] = w4.y; wt[u + 2] = w4.z; wt[u + 3] = w4.w;
           }
-          if (e == e0) {
+          if (!QIN && e == e0) {
 #pragma unroll
             for (int w = 0; w < VPL; ++w) acc[w] = zero8();
           }
@@ -580,7 +590,7 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 #pragma unroll
               for (int k = 0; k < 8; ++k) acc[w].f[k] = fadd(acc[w].f[k], fmul(wt[u], buf[u][w].f[k]));
         } else {
-          if (e == e0) {
+          if (!QIN && e == e0) {
 #pragma unroll
             for (int w = 0; w < VPL; ++w) acc[w] = buf[0][w];
           } else {
@@ -593,10 +603,22 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
             for (int w = 0; w < VPL; ++w) add8(acc[w], buf[u][w]);
         }
       }
-      if (e0 == e1) {
+      if (!QIN && e0 == e1) {
 #pragma unroll
         for (int w = 0; w < VPL; ++w) acc[w] = zero8();
       }
+}
+
+template <int LANES, int VPL, int MODE, bool FULL = false, bool STAGE = false, bool QIN = false, bool SKIP = false>
+__device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
+                                          unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false,
+                                          long long* sums_dst = nullptr, long long* zero_dst = nullptr,
+                                          const float4* stage = nullptr, int nb = -1, int ni = -1,
+                                          int slot_stride = 0) {
+      const int SB8 = P.SB >> 3;
+      const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
+      V8 acc[VPL];
+      gather_q<LANES, VPL, MODE, FULL, QIN, SKIP>(P, V, b, i, lane, acc);
 
       const float degf = (P.problem != kMAXCUT) ? 0.0f
                          : (MODE & kModeWeighted) ? __ldg(P.wdeg + i)
@@ -698,6 +720,44 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB 
     for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
       const float2 msi = P.ms[i];
       step_item<LANES, VPL, MODE, FULL>(P, P.var, b, i, lane, gmask, msi.x, msi.y, bad);
+    }
+  }
+  if (bad) atomicOr(P.flag, 1);
+}
+
+// Segmented gather (round 2): the sources j of block b are split into KS ascending ranges
+// (segments) small enough to stay in L2 while the grid sweeps all rows; launch (b, k) adds segment k's
+// neighbours of every row i to the partial q_i kept in the item's p_next row (written only by this step's
+// last pass of (b, i), by the same lane). k_seg_gather: segments 0..KS-2 (FIRST: segment 0 starts the
+// sum); k_step_seg: the last segment followed by the whole update of k_step. The rows' neighbours are
+// strictly ascending, so the adds happen in CSR order: bit-identical to k_step (test_gpu_segmented.py).
+// VPL = 1, FULL shapes, unweighted modes 0-3; blocks [blo, bhi) of one launch.
+template <int LANES, bool FIRST>
+__global__ void __launch_bounds__(256, QQA_STEP_MIN_BLOCKS) k_seg_gather(const StepParams P) {
+  const int lane = threadIdx.x & (LANES - 1);
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  for (int b = P.blo; b < P.bhi; ++b) {
+    const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;
+    for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
+      V8 acc[1];
+      gather_q<LANES, 1, 0, true, !FIRST, true>(P, P.var, b, i, lane, acc);
+      st8_stream(P.var.p_next + blk + (size_t)i * P.SB + lane * 8, acc[0]);
+    }
+  }
+}
+
+template <int LANES, int MODE>
+__global__ void __launch_bounds__(256, QQA_STEP_MIN_BLOCKS) k_step_seg(const StepParams P) {
+  const int lane = threadIdx.x & (LANES - 1);
+  const unsigned gmask = group_mask<LANES>();
+  const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
+  const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  bool bad = false;
+  for (int b = P.blo; b < P.bhi; ++b) {
+    for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
+      const float2 msi = P.ms[i];
+      step_item<LANES, 1, MODE, true, false, true, true>(P, P.var, b, i, lane, gmask, msi.x, msi.y, bad);
     }
   }
   if (bad) atomicOr(P.flag, 1);
