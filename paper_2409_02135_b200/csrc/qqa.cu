@@ -207,6 +207,10 @@ int seg_lo(int n, int KS, int k) { return (int)((int64_t)n * k / KS); }
 int64_t build_seg_csr(const int64_t* rowptr, const int32_t* colidx, int n, int KS, int* rp, int* ci) {
   std::vector<int> lo((size_t)KS + 1);
   for (int k = 0; k <= KS; ++k) lo[k] = seg_lo(n, KS, k);
+  if (const char* env = std::getenv("QQA_SEG_SPLIT")) {   // experiment: every source in segment 0, the last
+    if (std::atoi(env) != 0)                              // pass an update without a gather
+      for (int k = 1; k < KS; ++k) lo[k] = n;
+  }
   lo[KS] = INT32_MAX;   // the last segment takes everything from lo[KS-1] on (incl. out-of-range columns)
   std::vector<int> cnt(rp ? (size_t)KS * n : 0);
   int64_t total = 0;
@@ -1067,6 +1071,7 @@ int do_steps(qqa_handle* h, const float* gamma, int64_t n_steps) {
   P.eps = c.eps;
   P.ns = (float)std::sqrt(2.0 * (double)c.lr * (double)c.temperature);   // Eq. 9: sqrt(2 eta T)
   P.S_total_u = (unsigned long long)h->s.S_total;
+  P.blo = 0; P.bhi = h->s.B;
   const uint64_t nbase = mix64_host(c.seed ^ 0x6A09E667F3BCC909ull);    // noise stream
   for (int64_t k = 0; k < n_steps; ++k) {
     const int64_t t = h->step + 1;  // Adam step index (reading R11)

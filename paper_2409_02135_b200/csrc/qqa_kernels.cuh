@@ -488,18 +488,23 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
 // One work item (replica block b, variable i) of the step: gather, update, statistics.
 // FULL: every lane holds a vector of the block (SB / 8 == LANES * VPL), so the gather needs no
 // per-lane guard (a compile-time variant; measured 1.7 % on c5).
-// Gather q_i = sum_j A_ij p_j over block b (CSR order) into acc. QIN: the sum continues a partial sum
-// stored in the item's p_next row by the previous source segment (segmented gather): the
-// neighbours of a row are strictly ascending, so segments of ascending source ranges add them in CSR order
-// and the result is bit-identical to the one-pass gather. SKIP: sentinel entries (column n, the zero row)
-// issue no load (exactly +0 added).
-template <int LANES, int VPL, int MODE, bool FULL, bool QIN = false, bool SKIP = false>
-__device__ __forceinline__ void gather_q(const StepParams& P, const StepVar& V, int b, int i, int lane,
-                                         V8 (&acc)[VPL]) {
+// QIN (segmented gather): the sum continues a partial sum stored in the item's p_next row by the
+// previous source segments; a row's neighbours ascend, so segments of ascending source ranges add them in
+// CSR order and the bits equal the one-pass gather. SKIP: sentinel entries (column n, the zero row) issue no
+// load (exactly +0 added). Both are compile-time: the default kernels' code is unchanged by them (SASS
+// compared).
+template <int LANES, int VPL, int MODE, bool FULL = false, bool STAGE = false, bool QIN = false, bool SKIP = false>
+__device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
+                                          unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false,
+                                          long long* sums_dst = nullptr, long long* zero_dst = nullptr,
+                                          const float4* stage = nullptr, int nb = -1, int ni = -1,
+                                          int slot_stride = 0) {
       const int SB8 = P.SB >> 3;
       const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
       const float* __restrict__ pc = V.p_cur + blk;
-      if constexpr (QIN) {
+      // ---- gather q_i over block b
+      V8 acc[VPL];
+      if constexpr (QIN) {   // segmented gather: continue the partial sum stored in the item's p_next row
 #pragma unroll
         for (int w = 0; w < VPL; ++w) {
           const int col8 = lane + w * LANES;
@@ -607,18 +612,6 @@ __device__ __forceinline__ void gather_q(const StepParams& P, const StepVar& V, 
 #pragma unroll
         for (int w = 0; w < VPL; ++w) acc[w] = zero8();
       }
-}
-
-template <int LANES, int VPL, int MODE, bool FULL = false, bool STAGE = false, bool QIN = false, bool SKIP = false>
-__device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V, int b, int i, int lane,
-                                          unsigned gmask, float mu, float sd, bool& bad, bool force_atomic = false,
-                                          long long* sums_dst = nullptr, long long* zero_dst = nullptr,
-                                          const float4* stage = nullptr, int nb = -1, int ni = -1,
-                                          int slot_stride = 0) {
-      const int SB8 = P.SB >> 3;
-      const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;     // float offset of block b
-      V8 acc[VPL];
-      gather_q<LANES, VPL, MODE, FULL, QIN, SKIP>(P, V, b, i, lane, acc);
 
       const float degf = (P.problem != kMAXCUT) ? 0.0f
                          : (MODE & kModeWeighted) ? __ldg(P.wdeg + i)
@@ -732,17 +725,53 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : VPL >= 2 ? QQA_VPL2_MINB 
 // sum); k_step_seg: the last segment followed by the whole update of k_step. The rows' neighbours are
 // strictly ascending, so the adds happen in CSR order: bit-identical to k_step (test_gpu_segmented.py).
 // VPL = 1, FULL shapes, unweighted modes 0-3; blocks [blo, bhi) of one launch.
+// One item of a partial pass with the NEXT item's row bounds and first index quad loaded while this item
+// gathers (a gather-only pass is bound by the rowptr -> index -> row chain, not by bandwidth; ncu r2).
+// The sum starts from +0 (or the stored partial): 0 + x == x for the p >= +0 values added.
+template <int LANES, bool QIN>
+__device__ __forceinline__ V8 seg_gather_item(const StepParams& P, const StepVar& V, size_t blk, int i, int lane,
+                                              int e0, int e1, int4 nxt, int in, int& e0n, int& e1n, int4& nxtn) {
+  const float* __restrict__ pc = V.p_cur + blk;
+  const int4 sent = make_int4(P.n, P.n, P.n, P.n);
+  V8 acc = QIN ? ld8_stream(V.p_next + blk + (size_t)i * P.SB + lane * 8) : zero8();
+  const bool more = in < P.row_end;
+  if (more) { e0n = __ldg(P.rowptr_pad + in); e1n = __ldg(P.rowptr_pad + in + 1); }
+  for (int e = e0; e < e1; e += 4) {
+    const int js[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
+    V8 buf[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) buf[u] = (js[u] != P.n) ? ld8_gather(pc + (size_t)js[u] * P.SB + lane * 8) : zero8();
+    nxt = (e + 4 < e1) ? ld_idx4(P.colidx_pad + e + 4) : sent;
+    if (e == e0) nxtn = (more && e0n < e1n) ? ld_idx4(P.colidx_pad + e0n) : sent;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) add8(acc, buf[u]);
+  }
+  if (e0 == e1) nxtn = (more && e0n < e1n) ? ld_idx4(P.colidx_pad + e0n) : sent;
+  return acc;
+}
+
 template <int LANES, bool FIRST>
 __global__ void __launch_bounds__(256, QQA_STEP_MIN_BLOCKS) k_seg_gather(const StepParams P) {
   const int lane = threadIdx.x & (LANES - 1);
   const int group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LANES);
   const int ngroups = (int)((gridDim.x * blockDim.x) / LANES);
+  const int4 sent = make_int4(P.n, P.n, P.n, P.n);
   for (int b = P.blo; b < P.bhi; ++b) {
     const size_t blk = (size_t)b * ((size_t)P.n + 1) * P.SB;
-    for (int i = P.row_begin + group; i < P.row_end; i += ngroups) {
-      V8 acc[1];
-      gather_q<LANES, 1, 0, true, !FIRST, true>(P, P.var, b, i, lane, acc);
-      st8_stream(P.var.p_next + blk + (size_t)i * P.SB + lane * 8, acc[0]);
+    int i = P.row_begin + group, e0 = 0, e1 = 0;
+    int4 nxt = sent;
+    if (i < P.row_end) {
+      e0 = __ldg(P.rowptr_pad + i);
+      e1 = __ldg(P.rowptr_pad + i + 1);
+      if (e0 < e1) nxt = ld_idx4(P.colidx_pad + e0);
+    }
+    while (i < P.row_end) {
+      const int in = i + ngroups;
+      int e0n = 0, e1n = 0;
+      int4 nxtn = sent;
+      const V8 acc = seg_gather_item<LANES, !FIRST>(P, P.var, blk, i, lane, e0, e1, nxt, in, e0n, e1n, nxtn);
+      st8_stream(P.var.p_next + blk + (size_t)i * P.SB + lane * 8, acc);
+      i = in; e0 = e0n; e1 = e1n; nxt = nxtn;
     }
   }
 }

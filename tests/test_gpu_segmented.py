@@ -104,3 +104,4 @@ def test_segments_ignored_where_unsupported(Q, monkeypatch):
     l0 = sol.launch_count()
     sol.run(oracle.schedule(-2.0, 0.1, 10)[:2])
     assert sol.launch_count() - l0 == 2 * 2
+
