@@ -89,6 +89,40 @@ def maybe_relaunch(args, argv: list[str]) -> bool:
     sys.exit(r.returncode)
 
 
+def kary_chunk_floats(n: int, S_local: int, K: int) -> int:
+    """Floats of one gathered K-ary row: L replicas x KP colours, with the replica-chunk width L that
+    qqa_create picks (csrc/qqa.cu make_shape: pow2 >= S_local in [4, 32], halved while n L KP 4 > 32 MB)."""
+    KP = (K + 3) // 4 * 4
+    L = 4
+    while L < min(32, S_local):
+        L *= 2
+    while L > 4 and n * L * KP * 4 > 32 * 1024 * 1024:
+        L //= 2
+    return L * KP
+
+
+def l2_gather_line(gathered_bytes: int, kernel_s: float, row_bytes: int):
+    peak, width = l2_gather_peak(row_bytes)
+    if peak is None or kernel_s <= 0:
+        return None
+    achieved = gathered_bytes / kernel_s / 1e9
+    return {"bound": "l2", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "gathered_bytes_per_step": gathered_bytes, "row_bytes": row_bytes, "probe_row_bytes": width,
+            "peak_source": "profiles/l2_gather_peaks.json (tools/probes/l2bw.cu, measured)"}
+
+
+def l2_gather_peak(row_bytes: int):
+    """The L2 -> SM gather ceiling for rows of row_bytes (profiles/l2_gather_peaks.json, measured by
+    tools/probes/l2bw.cu): the table entry of the largest probed width <= row_bytes."""
+    path = os.path.join(ROOT, "profiles", "l2_gather_peaks.json")
+    if not os.path.exists(path) or row_bytes < 32:
+        return None, None
+    with open(path) as f:
+        tab = {int(k): float(v) for k, v in json.load(f)["row_bytes_gbs"].items()}
+    w = max(k for k in tab if k <= row_bytes)
+    return tab[w], w
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -515,6 +549,7 @@ def main():
     n_blocks = 1 if w.n_colors else -(-((S_l + 7) // 8 * 8) // sol.replica_block())   # replica blocks B
     Bc = compulsory_bytes(g.n, nnz_pad, S_l, n_blocks, K)
     avg_kernel_s = kern_ms / 1e3 / max(kern_launches, 1)
+    row_bytes = 4 * (kary_chunk_floats(g.n, S_l, w.n_colors) if w.n_colors else sol.replica_block())
     peak, peak_src = measured_peaks()
     achieved = B / avg_kernel_s / 1e9
     traffic = None
@@ -602,6 +637,10 @@ def main():
                                               f"profiled pass of {min(args.steps, 3)} identical solves (not in "
                                               "the headline region)",
                              "step_kernel_share": kern_ms / prof_ms},
+                # the gather against its L2 -> SM ceiling (the bound of the L2-resident workloads): gathered
+                # neighbour bytes 4 nnz S_l K per step over the step-kernel time, vs the probe's rate for rows of
+                # this width (a row = one replica block of one variable, SB floats; K-ary: L x KP floats)
+                "l2_gather": l2_gather_line(4 * g.nnz * S_l * K, avg_kernel_s, row_bytes),
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": l1 - l0, "clocks": clocks,
                 "result": ({"best_replica": res.best_replica, "best_energy": res.best_energy} if gor is None else
                            {"instances": len(w.graphs), "best_energy_per_instance": [float(x) for x in res.best_energy]})}

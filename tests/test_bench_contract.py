@@ -76,3 +76,20 @@ def test_compulsory_bytes_c5():
     """c5's compulsory DRAM floor is about 2.26 GB per step (replica blocks of 32)."""
     b = bench.compulsory_bytes(1_000_000, 20_000_000, 64, 2)
     assert 2.2e9 < b < 2.3e9
+
+
+def test_l2_gather_roofline_fields():
+    """The L2 gather line picks the probe entry of the largest width <= the row and reports the fraction."""
+    assert bench.l2_gather_peak(128)[1] == 128
+    assert bench.l2_gather_peak(416)[1] == 256      # c2 / t1: 13 vectors of 32 B
+    assert bench.l2_gather_peak(2048)[1] == 1024    # c4: rows wider than the probe
+    assert bench.l2_gather_peak(16) == (None, None)
+    d = bench.l2_gather_line(2_000_000_000, 1e-4, 2048)
+    assert d["bound"] == "l2" and abs(d["achieved"] - 20000.0) < 1e-6 and abs(d["frac"] - 20000.0 / d["peak"]) < 1e-12
+
+
+def test_kary_chunk_width_rule():
+    """K-ary gathered row = L replicas x KP colours with make_shape's chunk width (k8: L = 8, q13: L = 32)."""
+    assert bench.kary_chunk_floats(100_000, 64, 8) == 8 * 8
+    assert bench.kary_chunk_floats(169, 1000, 13) == 32 * 16
+    assert bench.kary_chunk_floats(1000, 3, 4) == 4 * 4
