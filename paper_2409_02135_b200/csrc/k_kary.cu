@@ -3,11 +3,13 @@
 #include "qqa_dispatch.h"
 
 namespace qqa {
-bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp) {
+bool kary_kernels(int KP, int K, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp) {
   const bool noise = (mode & kModeNoise) != 0;
+  const bool fk = K == KP;   // no padding colours: k_step_K<KP, MODE, true>
 #define QQA_KCASE(KPV)                                            \
   if (KP == KPV) {                                                \
-    ks = noise ? k_step_K<KPV, kModeNoise> : k_step_K<KPV, 0>;    \
+    ks = noise ? (fk ? k_step_K<KPV, kModeNoise, true> : k_step_K<KPV, kModeNoise>)         \
+               : (fk ? k_step_K<KPV, 0, true> : k_step_K<KPV, 0>);                         \
     ki = k_init_K<KPV>;                                           \
     kp = k_pack_K<KPV>;                                           \
     return true;                                                  \

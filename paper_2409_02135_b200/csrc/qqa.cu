@@ -513,8 +513,8 @@ using StepKKernel = qqa::StepKKernel;
 using InitKKernel = qqa::InitKKernel;
 using PackKKernel = qqa::PackKKernel;
 
-bool pick_kary(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp) {
-  return qqa::kary_kernels(KP, mode, ks, ki, kp);   // k_kary.cu
+bool pick_kary(int KP, int K, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp) {
+  return qqa::kary_kernels(KP, K, mode, ks, ki, kp);   // k_kary.cu
 }
 
 // k_t of the K-ary entropy: -gamma c_K alpha K, c_K = 1/((K-1)((K-1)^(alpha-1) + 1)) (host double -> fp32)
@@ -553,7 +553,7 @@ int launch_init_kary(qqa_handle* h, bool use_given, const float* c_given) {
   StepKKernel ks;
   InitKKernel ki;
   PackKKernel kp;
-  pick_kary(s.KP, step_mode(h->cfg, h->s.weighted), ks, ki, kp);
+  pick_kary(s.KP, s.K, step_mode(h->cfg, h->s.weighted), ks, ki, kp);
   qqa::InitKParams P{};
   P.p0 = h->p[0]; P.p1 = h->p[1]; P.m = h->m; P.v = h->v;
   P.c = h->c[0]; P.sums = h->sums[0];
@@ -735,7 +735,7 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
   StepKKernel ks;
   InitKKernel ki;
   PackKKernel kp;
-  pick_kary(s.KP, step_mode(c, s.weighted), ks, ki, kp);
+  pick_kary(s.KP, s.K, step_mode(c, s.weighted), ks, ki, kp);
   const size_t nk = (size_t)s.n * s.K;
   qqa::StepKParams P{};
   P.rowptr = h->rowptr; P.colidx = h->colidx; P.m = h->m; P.v = h->v; P.flag = h->flag;
@@ -1411,7 +1411,7 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     StepKKernel ks;
     InitKKernel ki;
     PackKKernel kp;
-    if (!pick_kary(s.KP, step_mode(*cfg, s.weighted), ks, ki, kp)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no K-ary kernel"));
+    if (!pick_kary(s.KP, s.K, step_mode(*cfg, s.weighted), ks, ki, kp)) return cleanup(fail(QQA_ERR_UNSUPPORTED, "no K-ary kernel"));
     const int64_t chunks = (s.S_local + s.LK - 1) / s.LK;   // work item = (variable, replica chunk)
     if ((st = grid_for((const void*)ks, h->sm_count, (int64_t)s.n * chunks, s.LK, h->grid_step))) return cleanup(st);
     {  // colour quads for KP 12 / 16 (QQA_KARY_QUAD=0 keeps k_step_K)
@@ -1790,7 +1790,7 @@ int evaluate_core_kary(qqa_handle* h) {
   StepKKernel ks;
   InitKKernel ki;
   PackKKernel kp;
-  pick_kary(s.KP, step_mode(h->cfg, h->s.weighted), ks, ki, kp);
+  pick_kary(s.KP, s.K, step_mode(h->cfg, h->s.weighted), ks, ki, kp);
   uint8_t* X8 = (uint8_t*)h->X;
   const int64_t ns = (int64_t)s.n * s.S_local;
   if (ns > 0) {  // K3: x = argmax_k P

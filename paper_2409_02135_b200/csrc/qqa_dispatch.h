@@ -77,7 +77,7 @@ RunKernel cluster_kernel(int mode);
 bool seg_kernels(int lanes, int mode, StepKernel& first, StepKernel& mid, StepKernel& last);
 
 // K-ary kernels for KP in {4, 8, 12, 16}; false otherwise.
-bool kary_kernels(int KP, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);
+bool kary_kernels(int KP, int K, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);
 // k_step_Kq<KP, MODE> (colour quads, KP = 12 / 16); nullptr otherwise.
 StepKKernel kary_quad_kernel(int KP, int mode);
 }  // namespace qqa

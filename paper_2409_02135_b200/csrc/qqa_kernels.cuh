@@ -1653,7 +1653,8 @@ __device__ __forceinline__ void normalize_colours(float (&w)[KP], int K, float u
 #ifndef QQA_KARY_MINB_NARROW
 #define QQA_KARY_MINB_NARROW 4   // min CTAs per SM for k_step_K, KP <= 8
 #endif
-template <int KP, int MODE>
+// FK: K == KP (no padding colours), so the per-colour K tests compile away.
+template <int KP, int MODE, bool FK = false>
 __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_NARROW)) k_step_K(const StepKParams P) {
   constexpr int U = (KP <= 8) ? 4 : QQA_KARY_U_WIDE;     // neighbour rows in flight per lane
   const int L = P.L;
@@ -1664,10 +1665,18 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
   const int nch = (P.S + L - 1) / L;
   const long long items = (long long)P.n * nch;
   bool bad = false;
-  for (long long it = (long long)blockIdx.x * groups_cta + gl; it < items; it += (long long)gridDim.x * groups_cta) {
-    int i, ch;
-    if (P.cmaj) { ch = (int)(it / P.n); i = (int)(it - (long long)ch * P.n); }
-    else { i = (int)(it / nch); ch = (int)(it - (long long)i * nch); }
+  // item it = (chunk-major) ch n + i, or (row-major) i nch + ch; the pair is advanced by the grid stride with
+  // one quotient / remainder per thread instead of a 64-bit division per item
+  const long long it0 = (long long)blockIdx.x * groups_cta + gl, stride = (long long)gridDim.x * groups_cta;
+  const long long inner = P.cmaj ? P.n : nch;             // the fast-moving index's range
+  const int sq = (int)(stride / inner), sr = (int)(stride % inner);
+  int outer_ix = (int)(it0 / inner), inner_ix = (int)(it0 % inner);
+  for (long long it = it0; it < items; it += stride) {
+    const int i = P.cmaj ? inner_ix : outer_ix;
+    const int ch = P.cmaj ? outer_ix : inner_ix;
+    inner_ix += sr;
+    outer_ix += sq;
+    if (inner_ix >= inner) { inner_ix -= (int)inner; ++outer_ix; }
     const int r = ch * L + lane;
     const bool live = r < P.S;
     float w[KP];                                          // the replica's new P (0 on idle lanes)
@@ -1707,7 +1716,7 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
       ld_colours<KP>(P.v + at, vv2);
 #pragma unroll
       for (int k = 0; k < KP; ++k) {              // g_k = dR/dp_k (into q[k])
-        if (k >= P.K) continue;
+        if (!FK && k >= P.K) continue;
         const float pi = w[k];
         const float2 st = P.ms[(size_t)i * P.K + k];
         const float e = fsub(fmul(P.Kf, pi), 1.0f);
@@ -1720,14 +1729,14 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
         float gb = 0.0f;
 #pragma unroll
         for (int k = 0; k < KP; ++k)
-          if (k < P.K) gb = fadd(gb, fmul(q[k], w[k]));
+          if (FK || k < P.K) gb = fadd(gb, fmul(q[k], w[k]));
 #pragma unroll
         for (int k = 0; k < KP; ++k) q[k] = fsub(q[k], gb);
       }
       float xi = 0.0f, xi_odd = 0.0f;              // colours pair up (k even, k + 1) on one noise hash
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
-        if (k >= P.K) continue;
+        if (!FK && k >= P.K) continue;
         if (MODE & kModeNoise) {
           if ((k & 1) == 0)
             gauss_pair_c(mix64(rkey + (unsigned long long)k * P.S_total_u + (unsigned long long)r), xi, xi_odd);
@@ -1745,7 +1754,7 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
         bad |= !isfinite(x);
         w[k] = x;
       }
-      normalize_colours<KP>(w, P.K, P.unif);
+      normalize_colours<KP>(w, FK ? KP : P.K, P.unif);
       st_colours<KP>(P.m + at, mm);
       st_colours<KP>(P.v + at, vv2);
       st_colours<KP>(P.p_next + at, w);
@@ -1753,7 +1762,7 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
     // fixed-point statistics of the new P per colour: shuffle-reduce over the group's replicas
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
-      if (k >= P.K) continue;
+      if (!FK && k >= P.K) continue;
       const size_t ik = (size_t)i * P.K + k, nk = (size_t)P.n * P.K;
       long long D = 0, D2 = 0;
       if (live) stat_terms(w[k], P.ms[ik].x, D, D2);
