@@ -57,8 +57,9 @@ def test_step_kernels_keep_64_registers(usage, lanes, mode):
 @pytest.mark.parametrize("kp,cap", [(4, 64), (8, 64), (12, 80), (16, 80)])
 def test_kary_kernels_register_caps(usage, kp, cap):
     for mode in (0, 2):
-        reg, stack = _get(usage, f"_ZN3qqa8k_step_KILi{kp}ELi{mode}EEEvNS_11StepKParamsE")
-        assert reg <= cap and stack <= 64
+        for fk in (0, 1):   # K == KP specialisation
+            reg, stack = _get(usage, f"_ZN3qqa8k_step_KILi{kp}ELi{mode}ELb{fk}EEEvNS_11StepKParamsE")
+            assert reg <= cap and stack <= 80
 
 
 @pytest.mark.parametrize("kp", [12, 16])
