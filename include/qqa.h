@@ -165,8 +165,10 @@ QQA_API const char* qqa_last_error(void);               /* thread-local message 
 QQA_API const char* qqa_status_string(int status);
 
 /* Device bytes the workspace must have for (graph, config): the replica state theta / m / v / p x 2
- * ([B][n+1][SB] float32), the padded CSR, the statistics and evaluation buffers.
- * Host-only; INVALID_ARG / UNSUPPORTED as qqa_create. */
+ * ([B][n+1][SB] float32), the padded CSR, the statistics and evaluation buffers (and,
+ * with the opt-in segmented gather QQA_SEGMENTS=KS, the KS segment CSRs). The layout environment
+ * (QQA_BLOCK_REPLICAS, QQA_SEGMENTS) is read here and at qqa_create: it must be the same for both calls
+ * (otherwise qqa_create reports WORKSPACE). Host-only; INVALID_ARG / UNSUPPORTED as qqa_create. */
 QQA_API int qqa_workspace_bytes(const qqa_graph* g, const qqa_config* cfg, size_t* bytes);
 
 /* Validate and copy the graph, carve the workspace, initialise the replicas: the S parallel runs
