@@ -651,8 +651,10 @@ static int update_row_K(int32_t i, int32_t n, int64_t t, const int64_t* rowptr, 
             const float e = Kf * pi - 1.0f;
             float ep = e;
             for (int32_t a = 2; a < cf->alpha; ++a) ep = ep * e;       /* (K p - 1)^(alpha-1) */
-            const float com = (sd[k] >= 1e-6f) ? (-ac) * ((pi - mu[k]) / sd[k]) : 0.0f;
-            q[k] = fmaf(kt, ep, q[k]) + com;                   /* (q + entropy) + comm, fused */
+            /* Eq. 10 term -alpha_c (p - mu) / STD as (p - mu) kc with the (variable, colour)'s
+             * kc = fl(-alpha_c / STD) (0 if STD < 1e-6), as the binary contract (R6) */
+            const float kc = (sd[k] >= 1e-6f) ? (-ac) / sd[k] : 0.0f;
+            q[k] = fmaf(pi - mu[k], kc, fmaf(kt, ep, q[k]));   /* (q + entropy) + comm, fused */
         }
         if (cf->kary_grad) {                      /* through the map: g - <g, p>, <g, p> in colour order */
             float gb = 0.0f;

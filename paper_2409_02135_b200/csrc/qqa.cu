@@ -766,8 +766,8 @@ int do_steps_kary(qqa_handle* h, const float* gamma, int64_t n_steps) {
     P.sums_next = h->sums[sb];
     P.sums_zero = h->sums[sz];
     if (s.n > 0) {
-      qqa::k_finalize<<<h->grid_fin, 256, 0, h->stream>>>(h->c[a], h->sums[sa], (int)nk, (double)s.S_total, h->ms,
-                                                           h->c[b]);
+      qqa::k_finalize_kc<<<h->grid_fin, 256, 0, h->stream>>>(h->c[a], h->sums[sa], (int)nk, (double)s.S_total,
+                                                              c.comm, h->ms, h->c[b]);
       QQA_CUDA(cudaGetLastError());
       h->launches++;
       int st;

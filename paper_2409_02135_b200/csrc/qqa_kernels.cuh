@@ -478,6 +478,18 @@ __global__ void k_finalize(const float* __restrict__ c_cur, const long long* __r
   }
 }
 
+// K-ary: (mu, kc) per (variable, colour), kc = -alpha_c / STD (0 if STD < 1e-6): the Eq. 10 coefficient
+// computed once per (i, k) and step instead of a division per element (reading R6).
+__global__ void k_finalize_kc(const float* __restrict__ c_cur, const long long* __restrict__ sums, int n,
+                              double S_total, float comm, float2* __restrict__ ms, float* __restrict__ c_next) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float mu, sd;
+    finalize_stats(c_cur[i], sums[i], sums[n + i], S_total, mu, sd);
+    ms[i] = make_float2(mu, comm_coef(comm, sd));
+    c_next[i] = mu;
+  }
+}
+
 #endif  // QQA_INST_ONLY
 
 // K2: the fused step. Per item (b, i): gather q = A p over block b (4 neighbour
@@ -1718,12 +1730,11 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
       for (int k = 0; k < KP; ++k) {              // g_k = dR/dp_k (into q[k])
         if (!FK && k >= P.K) continue;
         const float pi = w[k];
-        const float2 st = P.ms[(size_t)i * P.K + k];
+        const float2 st = P.ms[(size_t)i * P.K + k];          // (mu, kc) of (i, k), k_finalize_kc
         const float e = fsub(fmul(P.Kf, pi), 1.0f);
         float ep = e;
         for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e);            // (K p - 1)^(alpha-1)
-        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
-        q[k] = fadd(__fmaf_rn(P.kt, ep, q[k]), com);             // (q + entropy) + comm, fused
+        q[k] = __fmaf_rn(fsub(pi, st.x), st.y, __fmaf_rn(P.kt, ep, q[k]));   // (q + entropy) + comm, fused
       }
       if (P.kgrad) {                              // through the map: g - <g, p>, <g, p> in colour order
         float gb = 0.0f;
@@ -1857,12 +1868,11 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
         const int k = k0 + c;
         if (k >= P.K) continue;
         const float pi = w[c];
-        const float2 st = P.ms[(size_t)i * P.K + k];
+        const float2 st = P.ms[(size_t)i * P.K + k];          // (mu, kc) of (i, k), k_finalize_kc
         const float e1f = fsub(fmul(P.Kf, pi), 1.0f);
         float ep = e1f;
         for (int a = 2; a < P.alpha; ++a) ep = fmul(ep, e1f);          // (K p - 1)^(alpha-1)
-        const float com = (st.y >= 1e-6f) ? fmul(-P.comm, fdiv(fsub(pi, st.x), st.y)) : 0.0f;
-        qv[c] = fadd(__fmaf_rn(P.kt, ep, qv[c]), com);           // (q + entropy) + comm, fused
+        qv[c] = __fmaf_rn(fsub(pi, st.x), st.y, __fmaf_rn(P.kt, ep, qv[c]));   // (q + entropy) + comm, fused
       }
     }
     // through the map (reading R33): g - <g, p>, <g, p> summed in colour order -- the running sum
