@@ -437,6 +437,12 @@ __device__ __forceinline__ void obj_coefs(const StepParams& P, float degf, float
   oc = cut ? -degf : -1.0f;
 }
 
+// Fire-and-forget int64 add (exact, order-free). Inline PTX so the front end does not wrap it in its
+// warp-aggregation prologue (MATCH / REDUX / VOTEU per call): the callers' lanes never share an address.
+__device__ __forceinline__ void red_add_s64(long long* p, long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"((unsigned long long)v) : "memory");
+}
+
 // Reduce the group's fixed-point partial sums and publish them for variable i.
 template <int LANES>
 __device__ __forceinline__ void publish_sums(long long sD, long long sD2, unsigned gmask, int lane, int i, int b,
@@ -452,8 +458,8 @@ __device__ __forceinline__ void publish_sums(long long sD, long long sD2, unsign
       sums[i] = sD;
       sums[n + i] = sD2;
     } else {  // blocks of one variable meet here: exact, order-free integer atomics
-      atomicAdd(reinterpret_cast<unsigned long long*>(sums + i), (unsigned long long)sD);
-      atomicAdd(reinterpret_cast<unsigned long long*>(sums + n + i), (unsigned long long)sD2);
+      red_add_s64(sums + i, sD);
+      red_add_s64(sums + n + i, sD2);
     }
     if (b == 0 && zero) { zero[i] = 0; zero[n + i] = 0; }
   }
@@ -1672,7 +1678,6 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
   const int L = P.L;
   const int lane = threadIdx.x & (L - 1);
   const int gl = threadIdx.x / L;
-  const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
   const int groups_cta = blockDim.x / L;
   const int nch = (P.S + L - 1) / L;
   const long long items = (long long)P.n * nch;
@@ -1683,14 +1688,19 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
   const long long inner = P.cmaj ? P.n : nch;             // the fast-moving index's range
   const int sq = (int)(stride / inner), sr = (int)(stride % inner);
   int outer_ix = (int)(it0 / inner), inner_ix = (int)(it0 % inner);
-  for (long long it = it0; it < items; it += stride) {
+  // warp-uniform trip count: the warp's groups hold consecutive items (it0 - wg is its first), so every lane
+  // runs the same iterations and the statistics shuffles take the full mask (no per-call mask match); a
+  // group past the end (valid = false) only joins the shuffles with zeros
+  const long long wg = (threadIdx.x & 31) / L;
+  for (long long it = it0; it - wg < items; it += stride) {
+    const bool valid = it < items;
     const int i = P.cmaj ? inner_ix : outer_ix;
     const int ch = P.cmaj ? outer_ix : inner_ix;
     inner_ix += sr;
     outer_ix += sq;
     if (inner_ix >= inner) { inner_ix -= (int)inner; ++outer_ix; }
     const int r = ch * L + lane;
-    const bool live = r < P.S;
+    const bool live = valid && r < P.S;
     float w[KP];                                          // the replica's new P (0 on idle lanes)
 #pragma unroll
     for (int k = 0; k < KP; ++k) w[k] = 0.0f;
@@ -1778,16 +1788,16 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
       long long D = 0, D2 = 0;
       if (live) stat_terms(w[k], P.ms[ik].x, D, D2);
       for (int off = L / 2; off > 0; off >>= 1) {
-        D += __shfl_xor_sync(gmask, D, off, L);
-        D2 += __shfl_xor_sync(gmask, D2, off, L);
+        D += __shfl_xor_sync(0xffffffffu, D, off, L);
+        D2 += __shfl_xor_sync(0xffffffffu, D2, off, L);
       }
-      if (lane == (k & (L - 1))) {
+      if (valid && lane == (k & (L - 1))) {
         if (nch == 1) {
           P.sums_next[ik] = D;
           P.sums_next[nk + ik] = D2;
         } else {
-          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + ik), (unsigned long long)D);
-          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + nk + ik), (unsigned long long)D2);
+          red_add_s64(P.sums_next + ik, D);
+          red_add_s64(P.sums_next + nk + ik, D2);
           if (ch == 0) { P.sums_zero[ik] = 0; P.sums_zero[nk + ik] = 0; }
         }
       }
@@ -1951,8 +1961,8 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
           P.sums_next[ik] = D;
           P.sums_next[nk + ik] = D2;
         } else {
-          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + ik), (unsigned long long)D);
-          atomicAdd(reinterpret_cast<unsigned long long*>(P.sums_next + nk + ik), (unsigned long long)D2);
+          red_add_s64(P.sums_next + ik, D);
+          red_add_s64(P.sums_next + nk + ik, D2);
           if (ch == 0) { P.sums_zero[ik] = 0; P.sums_zero[nk + ik] = 0; }
         }
       }
