@@ -1668,6 +1668,10 @@ __device__ __forceinline__ void normalize_colours(float (&w)[KP], int K, float u
 #ifndef QQA_KARY_U_WIDE
 #define QQA_KARY_U_WIDE 2    // neighbour rows in flight per lane for KP > 8
 #endif
+#ifndef QQA_KARY_REDUX
+#define QQA_KARY_REDUX 0     // 1: k_step_K statistics of 32-lane groups by redux.sync on 32-bit halves (measured:
+                             // q13 with k_step_K 97.5 -> 90.7 us, but k8 603 -> 607 us from the extra code: off)
+#endif
 #ifndef QQA_KARY_MINB_NARROW
 #define QQA_KARY_MINB_NARROW 4   // min CTAs per SM for k_step_K, KP <= 8
 #endif
@@ -1787,9 +1791,23 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
       const size_t ik = (size_t)i * P.K + k, nk = (size_t)P.n * P.K;
       long long D = 0, D2 = 0;
       if (live) stat_terms(w[k], P.ms[ik].x, D, D2);
-      for (int off = L / 2; off > 0; off >>= 1) {
-        D += __shfl_xor_sync(0xffffffffu, D, off, L);
-        D2 += __shfl_xor_sync(0xffffffffu, D2, off, L);
+      if (QQA_KARY_REDUX && L == 32) {
+        // whole-warp groups: exact sums of D, D2 as two 32-bit halves, one redux.sync each. |p - c| <= 1
+        // bounds |D|, D2 by 2^40, so hi = D >> 24 (|hi| <= 2^16) and lo = D mod 2^24 summed over 32 lanes
+        // fit 32 bits, and D = hi 2^24 + lo recombines exactly. (Measured: a win with the full mask, q13's
+        // k_step_K 97.5 -> 90.7 us; with 8-lane group masks the redux is far slower than the shuffles, k8
+        // 604 -> 803 us, so only 32-lane groups could take it; QQA_KARY_REDUX.)
+        const int dh = __reduce_add_sync(0xffffffffu, (int)(D >> 24));
+        const unsigned dl = __reduce_add_sync(0xffffffffu, (unsigned)(D & 0xFFFFFF));
+        const int eh = __reduce_add_sync(0xffffffffu, (int)(D2 >> 24));
+        const unsigned el = __reduce_add_sync(0xffffffffu, (unsigned)(D2 & 0xFFFFFF));
+        D = (long long)dh * (1ll << 24) + (long long)dl;
+        D2 = (long long)eh * (1ll << 24) + (long long)el;
+      } else {
+        for (int off = L / 2; off > 0; off >>= 1) {
+          D += __shfl_xor_sync(0xffffffffu, D, off, L);
+          D2 += __shfl_xor_sync(0xffffffffu, D2, off, L);
+        }
       }
       if (valid && lane == (k & (L - 1))) {
         if (nch == 1) {
