@@ -556,8 +556,9 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 #pragma unroll
               for (int w = 0; w < VPL; ++w) {
                 const int col8 = lane + w * LANES;
-                buf[u][w] = ((FULL || col8 < SB8) && (!SKIP || js[h + u] != P.n))
-                                ? ld8_gather(pc + (size_t)js[h + u] * P.SB + col8 * 8) : zero8();
+                const int col8c = (FULL || col8 < SB8) ? col8 : SB8 - 1;   // idle lanes: a duplicate, unused
+                buf[u][w] = (!SKIP || js[h + u] != P.n) ? ld8_gather(pc + (size_t)js[h + u] * P.SB + col8c * 8)
+                                                        : zero8();
               }
             if (h == 2) nxt[0] = (e + 4 < e1) ? ld_idx4(P.colidx_pad + e + 4) : make_int4(P.n, P.n, P.n, P.n);
 #pragma unroll
@@ -586,8 +587,11 @@ __device__ __forceinline__ void step_item(const StepParams& P, const StepVar& V,
 #pragma unroll
           for (int w = 0; w < VPL; ++w) {
             const int col8 = lane + w * LANES;
-            buf[u][w] = ((FULL || col8 < SB8) && (!SKIP || js[u] != P.n))
-                            ? ld8_gather(pc + (size_t)js[u] * P.SB + col8 * 8) : zero8();
+            // lanes past the block's last vector (non-FULL shapes) load the last vector again (same sectors as
+            // its owner, no extra traffic) instead of zeros: no zeroing or predication per load; their sums
+            // are never used (the update skips them)
+            const int col8c = (FULL || col8 < SB8) ? col8 : SB8 - 1;
+            buf[u][w] = (!SKIP || js[u] != P.n) ? ld8_gather(pc + (size_t)js[u] * P.SB + col8c * 8) : zero8();
           }
         if constexpr (!kIdxPipe) {
 #pragma unroll
