@@ -21,8 +21,11 @@ bool kary_kernels(int KP, int K, int mode, StepKKernel& ks, InitKKernel& ki, Pac
 
 StepKKernel kary_quad_kernel(int KP, int mode) {
   const bool noise = (mode & kModeNoise) != 0;
+  if (KP == 8) return noise ? k_step_Kq<8, kModeNoise> : k_step_Kq<8, 0>;
   if (KP == 12) return noise ? k_step_Kq<12, kModeNoise> : k_step_Kq<12, 0>;
   if (KP == 16) return noise ? k_step_Kq<16, kModeNoise> : k_step_Kq<16, 0>;
   return nullptr;
 }
+
+int kary_quad_reps(int KP) { return KP == 8 ? quad_reps<8>() : quad_reps<16>(); }
 }  // namespace qqa

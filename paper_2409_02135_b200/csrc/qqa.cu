@@ -1416,9 +1416,12 @@ int qqa_create(qqa_handle** out, const qqa_graph* g, const qqa_config* cfg, void
     if ((st = grid_for((const void*)ks, h->sm_count, (int64_t)s.n * chunks, s.LK, h->grid_step))) return cleanup(st);
     {  // colour quads for KP 12 / 16 (QQA_KARY_QUAD=0 keeps k_step_K)
       const char* env = std::getenv("QQA_KARY_QUAD");
-      h->kq = (env && std::atoi(env) == 0) ? nullptr : qqa::kary_quad_kernel(s.KP, step_mode(*cfg, s.weighted));
+      // KP = 8 (2 lanes per replica) only with QQA_KARY_QUAD=2 (experiment)
+      const int qsel = env ? std::atoi(env) : 1;
+      h->kq = (qsel == 0 || (s.KP == 8 && qsel != 2)) ? nullptr : qqa::kary_quad_kernel(s.KP, step_mode(*cfg, s.weighted));
       if (h->kq) {
-        const int64_t qitems = (int64_t)s.n * ((s.S_local + qqa::kQuadReps - 1) / qqa::kQuadReps);
+        const int reps = qqa::kary_quad_reps(s.KP);   // replicas per warp (16 for KP = 8: two items)
+        const int64_t qitems = ((int64_t)s.n * ((s.S_local + qqa::kQuadReps - 1) / qqa::kQuadReps) * qqa::kQuadReps + reps - 1) / reps;
         if ((st = grid_for((const void*)h->kq, h->sm_count, qitems, 32, h->grid_kq))) return cleanup(st);
       }
     }

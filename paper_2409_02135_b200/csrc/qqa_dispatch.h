@@ -80,4 +80,5 @@ bool seg_kernels(int lanes, int mode, StepKernel& first, StepKernel& mid, StepKe
 bool kary_kernels(int KP, int K, int mode, StepKKernel& ks, InitKKernel& ki, PackKKernel& kp);
 // k_step_Kq<KP, MODE> (colour quads, KP = 12 / 16); nullptr otherwise.
 StepKKernel kary_quad_kernel(int KP, int mode);
+int kary_quad_reps(int KP);   // replicas per warp of kary_quad_kernel(KP)
 }  // namespace qqa

@@ -1835,7 +1835,11 @@ __global__ void __launch_bounds__(256, (KP > 8 ? QQA_KARY_MINB : QQA_KARY_MINB_N
 // gather, the per-colour update, the normaliser Z summed in colour order by passing the running sum
 // from lane to lane, per-colour statistics reduced over the warp's 8 replicas (u64 atomics across
 // chunks). Bit-identical to k_step_K.
-constexpr int kQuadReps = 8;   // replicas per warp
+// KP = 8 runs the same kernel with 2 lanes per replica (2 quads): a warp then holds two work items
+// (two variables of one 8-replica chunk), 16 lanes each.
+constexpr int kQuadReps = 8;   // replicas per work item (chunk)
+template <int KP> __host__ __device__ constexpr int quad_lanes() { return KP <= 8 ? 2 : 4; }   // lanes per replica
+template <int KP> __host__ __device__ constexpr int quad_reps() { return 32 / quad_lanes<KP>(); }   // replicas per warp
 #ifndef QQA_KQ_U
 #define QQA_KQ_U 4               // neighbour rows in flight per lane (measured: 4 at 5 CTAs/SM)
 #endif
@@ -1845,20 +1849,25 @@ constexpr int kQuadReps = 8;   // replicas per warp
 template <int KP, int MODE>
 __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams P) {
   constexpr int U = QQA_KQ_U;                            // neighbour rows in flight per lane
-  constexpr int NQ = KP / 4;                             // quads holding colours (3 or 4)
+  constexpr int NQ = KP / 4;                             // quads holding colours (2, 3 or 4)
+  constexpr int LPR = quad_lanes<KP>(), REPS = kQuadReps, IL = LPR * REPS, IPW = 32 / IL;   // IPW items per warp
   const int lane = threadIdx.x & 31;
-  const int rq = lane >> 2, q = lane & 3;                // replica in the chunk, colour quad
+  const int sub = lane / IL, li = lane & (IL - 1);      // item of the warp, lane within the item
+  const int rq = li / LPR, q = li & (LPR - 1);          // replica in the chunk, colour quad
   const int warps_cta = blockDim.x >> 5;
-  const int nch = (P.S + kQuadReps - 1) / kQuadReps;
+  const int nch = (P.S + REPS - 1) / REPS;
   const long long items = (long long)P.n * nch;
   bool bad = false;
-  for (long long it = (long long)blockIdx.x * warps_cta + (threadIdx.x >> 5); it < items;
-       it += (long long)gridDim.x * warps_cta) {
-    int i, ch;
-    if (P.cmaj) { ch = (int)(it / P.n); i = (int)(it - (long long)ch * P.n); }
-    else { i = (int)(it / nch); ch = (int)(it - (long long)i * nch); }
-    const int r = ch * kQuadReps + rq;
-    const bool rep = r < P.S;                            // a live replica (all 4 lanes)
+  for (long long itw = (long long)blockIdx.x * warps_cta + (threadIdx.x >> 5); itw * IPW < items;
+       itw += (long long)gridDim.x * warps_cta) {       // warp-uniform trip count: shuffles take the full mask
+    const long long it = itw * IPW + sub;
+    int i = 0, ch = P.S;                                 // past the end: no live replica
+    if (it < items) {
+      if (P.cmaj) { ch = (int)(it / P.n); i = (int)(it - (long long)ch * P.n); }
+      else { i = (int)(it / nch); ch = (int)(it - (long long)i * nch); }
+    }
+    const int r = ch * REPS + rq;
+    const bool rep = r < P.S;                            // a live replica (all LPR lanes)
     const bool live = rep && q < NQ;                     // ... and a quad holding colours
     const int k0 = 4 * q;
     float w[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -1917,7 +1926,7 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (k0 + c < P.K) gb = fadd(gb, fmul(qv[c], w[c]));
-        gb = __shfl_sync(0xffffffffu, gb, (lane & ~3) + qq);
+        gb = __shfl_sync(0xffffffffu, gb, (lane & ~(LPR - 1)) + qq);
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) qv[c] = fsub(qv[c], gb);
@@ -1956,7 +1965,7 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           if (k0 + c < P.K) Z = fadd(Z, cl4[c]);
-      Z = __shfl_sync(0xffffffffu, Z, (lane & ~3) + qq);
+      Z = __shfl_sync(0xffffffffu, Z, (lane & ~(LPR - 1)) + qq);
     }
     if (live) {
 #pragma unroll
@@ -1973,11 +1982,11 @@ __global__ void __launch_bounds__(256, QQA_KQ_MINB) k_step_Kq(const StepKParams 
       long long D = 0, D2 = 0;
       if (live && k < P.K) stat_terms(w[c], P.ms[(size_t)i * P.K + k].x, D, D2);
 #pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
+      for (int off = LPR; off < IL; off <<= 1) {
         D += __shfl_xor_sync(0xffffffffu, D, off);
         D2 += __shfl_xor_sync(0xffffffffu, D2, off);
       }
-      if (rq == 0 && q < NQ && k < P.K) {
+      if (rq == 0 && q < NQ && k < P.K && it < items) {
         const size_t ik = (size_t)i * P.K + k, nk = (size_t)P.n * P.K;
         if (nch == 1) {
           P.sums_next[ik] = D;

@@ -135,13 +135,15 @@ def test_invalid_colouring_configs(Q):
 
 
 @pytest.mark.parametrize("kary_grad", [1, 0])
-@pytest.mark.parametrize("K,S,T,steps", [(13, 1000, 0.0, 40), (10, 37, 0.002, 60), (16, 8, 0.0, 30), (9, 100, 0.001, 4100)])
+@pytest.mark.parametrize("K,S,T,steps", [(13, 1000, 0.0, 40), (10, 37, 0.002, 60), (16, 8, 0.0, 30), (9, 100, 0.001, 4100),
+                                         (8, 64, 0.0, 40), (6, 37, 0.002, 60), (7, 100, 0.001, 4100), (8, 5, 0.0, 30)])
 def test_colour_quad_kernel_equals_k_step_K(Q, monkeypatch, K, S, T, steps, kary_grad):
-    """k_step_Kq (4 colours per thread, 8 replicas per warp; KP = 12 / 16) is bit-identical to k_step_K,
+    """k_step_Kq (4 colours per thread; KP = 12 / 16: 4 lanes per replica, 8 replicas per warp; KP = 8 with
+    QQA_KARY_QUAD=2: 2 lanes per replica, 16 replicas per warp) is bit-identical to k_step_K,
     including noise pairs, ragged replica chunks and a schedule longer than one run() call."""
     g = gen.queens(7, 7)
     out = []
-    for flag in ("1", "0"):
+    for flag in ("2", "0"):
         monkeypatch.setenv("QQA_KARY_QUAD", flag)
         sol = Q.Solver(g.rowptr, g.colidx, Q.make_config("coloring", S_total=S, seed=3, n_colors=K, lr=0.01,
                                                          temperature=T, comm=0.3, kary_grad=kary_grad))

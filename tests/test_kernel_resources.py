@@ -62,7 +62,7 @@ def test_kary_kernels_register_caps(usage, kp, cap):
             assert reg <= cap and stack <= 80
 
 
-@pytest.mark.parametrize("kp", [12, 16])
+@pytest.mark.parametrize("kp", [8, 12, 16])
 def test_colour_quad_kernels_fit_five_ctas_without_spills(usage, kp):
     for mode in (0, 2):
         reg, stack = _get(usage, f"_ZN3qqa9k_step_KqILi{kp}ELi{mode}EEEvNS_11StepKParamsE")
