@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include "qqa_sigdiv.cuh"
 
 namespace qqa {
 
@@ -91,7 +92,8 @@ __device__ __forceinline__ float sigmoid_c(float th) {
   const float Ec = exp_neg_c(fminf(a, 87.0f));     // evaluated unconditionally (no branch)
   const float E = (a > 87.0f) ? 0.0f : Ec;
   const float den = fadd(1.0f, E);
-  return fdiv((th >= 0.0f) ? 1.0f : E, den);   // one division (the numerator is selected, not the quotient)
+  return sig_div((th >= 0.0f) ? 1.0f : E, den);   // one division (the numerator is selected, not the quotient);
+                                                  // = __fdiv_rn for every reachable operand (qqa_sigdiv.cuh)
 }
 
 // Clamp(w) into [0, 1]; NaN and -0 map to +0 (non-finite is flagged first).
