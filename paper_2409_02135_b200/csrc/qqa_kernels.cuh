@@ -107,7 +107,7 @@ __device__ __forceinline__ float ln_c(float u) {
   float m = __uint_as_float((b & 0x007fffffu) | 0x3f800000u);
   if (m > 1.41421356f) { m = fmul(m, 0.5f); e = e + 1; }
   const float f = fsub(m, 1.0f);
-  const float sv = fdiv(f, fadd(2.0f, f));
+  const float sv = sig_div(f, fadd(2.0f, f));   // divisor in [1.70, 2.42]: = __fdiv_rn for every f (qqa_sigdiv.cuh)
   const float z = fmul(sv, sv);
   float P = 1.0f / 9.0f;   // Horner steps as __fmaf_rn (== C fmaf)
   P = __fmaf_rn(P, z, 1.0f / 7.0f);
