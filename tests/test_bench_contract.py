@@ -93,3 +93,27 @@ def test_kary_chunk_width_rule():
     assert bench.kary_chunk_floats(100_000, 64, 8) == 8 * 8
     assert bench.kary_chunk_floats(169, 1000, 13) == 32 * 16
     assert bench.kary_chunk_floats(1000, 3, 4) == 4 * 4
+
+
+def test_traffic_json_cites_committed_ncu_summaries():
+    """roofline.traffic comes from profiles/traffic.json: every entry is a positive byte count, every ncu
+    summary its source names is committed, and c5's bytes are the read + write sums that summary prints."""
+    import re
+    with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+        d = json.load(f)
+    for k, v in d.items():
+        if k != "_source":
+            assert re.fullmatch(r"[a-z0-9_]+_x\d+", k) and isinstance(v, int) and v > 0, k
+    names = re.findall(r"r2u?_[A-Za-z0-9_]+_full\.txt", d["_source"])
+    assert names
+    for nm in names:
+        assert os.path.exists(os.path.join(ROOT, "profiles", nm)), nm
+    c5 = next(nm for nm in names if "_c5_" in nm)
+    unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+    total = 0.0
+    with open(os.path.join(ROOT, "profiles", c5)) as f:
+        for line in f:
+            m = re.match(r"dram__bytes_(read|write)\.sum\s+([0-9.]+)\s+(\w+)", line)
+            if m:
+                total += float(m.group(2)) * unit[m.group(3)]
+    assert abs(total - d["c5_x1"]) <= 1e-5 * total
